@@ -1,0 +1,151 @@
+/* spdhss.h -- C ABI of the B200-native SPD-HSS-from-H2 library (libspdhss.so).
+ *
+ * Method: arXiv 2011.07632, "quasilinear construction of an SPD HSS
+ * approximation driven by an H2 representation".  Every numeric step of the
+ * entry points below runs in hand-written fp64 CUDA kernels for sm_100a.
+ *
+ * Conventions:
+ *  - All numerics are fp64.  Array arguments are DEVICE pointers on the
+ *    current device unless marked "host".  Multi-vectors are column-major
+ *    with a leading dimension (ld >= n).  Points are row-major n x d.
+ *  - Vectors at the boundary are in the caller's ORIGINAL point order when
+ *    layout == SPD_LAYOUT_ORIGINAL, or in the library's tree order when
+ *    layout == SPD_LAYOUT_TREE (see spd_query(SPD_Q_PERM)).
+ *  - Ownership: the caller owns every buffer it passes; the library copies
+ *    what it keeps.  Handles own their device memory and are released by the
+ *    *_free calls.  An spd_hss_t references its spd_h2_t: free it first.
+ *  - Streams: all work is enqueued on the given stream (0 = legacy default).
+ *    Builds synchronize the stream internally (ranks decide allocations);
+ *    h2_matvec and hss_solve do not synchronize the host.
+ *  - Errors: every call returns an spd_status; spd_last_error() returns a
+ *    thread-local message (for SPD_ENOTPD it names level, node and the failed
+ *    pivot).  Rank deficiency is never an error: ranks shrink, down to 0.
+ */
+#ifndef SPDHSS_H
+#define SPDHSS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPD_OK = 0,
+    SPD_EINVAL = 1,   /* invalid argument / dimension mismatch */
+    SPD_ENOTPD = 2,   /* leaf Cholesky failed or I + B_ii not SPD */
+    SPD_ENOMEM = 3,   /* device allocation failed */
+    SPD_ECUDA = 4,    /* CUDA runtime error */
+    SPD_ENCCL = 5,    /* collective error (multi-GPU) */
+    SPD_ENOCONV = 6   /* PCG reached maxit; report filled; not fatal */
+} spd_status;
+
+/* Kernel functions K(r), r = |x - y|_2 (BASELINE.json forms, reading R13;
+ * PAPER.md §6 P:1073-1077 for the families).  shift sigma is added only on
+ * exact diagonal entries. */
+typedef enum {
+    SPD_K_GAUSSIAN = 0,     /* exp(-r^2 / l^2)                       */
+    SPD_K_MATERN32 = 1,     /* (1 + sqrt3 r / l) exp(-sqrt3 r / l)   */
+    SPD_K_EXPONENTIAL = 2,  /* exp(-r / l)                           */
+    SPD_K_IMQ = 3           /* 1 / sqrt(r^2 + l^2)                   */
+} spd_kernel_id;
+
+typedef struct { int id; double l; double shift; } spd_kernel;
+
+typedef enum { SPD_LAYOUT_ORIGINAL = 0, SPD_LAYOUT_TREE = 1 } spd_layout;
+
+typedef struct {
+    int n_proxy;        /* proxy points per node; 0 = 4096 (2D) / 6144 (3D) (reading R3) */
+    int reserved;
+} spd_h2_opts;
+
+typedef struct spd_comm_s* spd_comm_t;
+typedef struct spd_h2_s* spd_h2_t;
+typedef struct spd_hss_s* spd_hss_t;
+
+typedef struct {
+    int iters;               /* H2 matvecs performed                      */
+    int converged;           /* 1 if ||r_k|| <= tol ||b||                 */
+    double relres;           /* recursively updated relative residual     */
+    double seconds;          /* wall time of the solve (host clock)       */
+} spd_pcg_report;
+
+/* Communicator for multi-GPU runs.  Round 1: nranks must be 1 (the data-path
+ * collectives of SURVEY.md §8(e) are not built yet); pass NULL id. */
+spd_status spd_comm_init(const void* nccl_unique_id, int nranks, int rank, spd_comm_t* out);
+void spd_comm_free(spd_comm_t c);
+
+/* h2_build: H2 representation of A = K(X, X) + shift I.
+ *   pts   device, n x d row-major (original order), d in {2, 3}
+ *   leaf  maximum leaf size; tree depth ceil(log2(n / leaf)) (reading R1)
+ *   tol   relative tolerance of the proxy-point IDs (reading R4), e.g. 1e-10
+ * Builds the KD tree, the Type-1/Type-3 lists (PAPER.md P:657-663, P:891-913,
+ * reading R2), the proxy points (R3) and the nested interpolative bases by
+ * QRCP (R4).  Near blocks and B^{H2}_ij = K(X_Ji, X_Jj) are never stored: they
+ * are evaluated on the fly (north star).  opts may be NULL. */
+spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf, double tol,
+                    const spd_h2_opts* opts, spd_comm_t c, void* stream, spd_h2_t* out);
+
+/* h2_matvec: Y = A X (A = the H2 matrix incl. shift), X and Y n x k
+ * (column-major, ldx, ldy >= n) in the given layout.  Near field on the fly,
+ * up pass (U^T), Type-3 coupling on the fly, down pass (U)  (eqn:nested). */
+spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, double* Y,
+                     int64_t ldy, int64_t k, void* stream);
+
+/* spdhss_build: Alg. 4 of PAPER.md (alg:spdhss_h2).
+ *   rank_cap, rel_tol   HSS rank rule: r_i = min(cap, first t with |R_tt| <= tol |R_00|) (R4, R5)
+ *   oversample          p; sketch width w = rank_cap + p
+ *   seed                Philox seed for Omega when omega == NULL
+ *   omega               optional device N x w column-major (ld = n) Gaussian sketch in TREE
+ *                       order (parity hook); one Omega serves every level (reading R8)
+ * The nonleaf factorization uses Cholesky of I + B_ii (reading R9, identical R_i, B_ij).
+ * Fails with SPD_ENOTPD if a leaf block or some I + B_ii is not SPD (R18). */
+spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample, uint64_t seed,
+                        const double* omega, void* stream, spd_hss_t* out);
+
+/* hss_solve: X = H^{-1} B for the SPD HSS H, by the recursive solve of reading
+ * R12 (the "ULV-style" solve of PAPER.md P:1119-1123), nrhs columns. */
+spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, double* X,
+                     int64_t ldx, int64_t nrhs, void* stream);
+
+/* pcg_solve: (K + shift I) x = b by PCG with H2 matvecs, preconditioner
+ * M = the SPD HSS (hss_solve) or none (M == NULL).  x holds x0 = 0 on output the
+ * solution.  Stops when ||r_k|| <= tol ||b|| (recursive residual, R15) or at maxit
+ * (returns SPD_ENOCONV with the report filled).  rep is a host pointer. */
+spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x,
+                     double tol, int maxit, spd_pcg_report* rep, void* stream);
+
+/* Introspection (host buffers).  `what` selects:                            */
+enum {
+    SPD_Q_N = 1,            /* int64: n                                       */
+    SPD_Q_LEVELS = 2,       /* int32: L                                       */
+    SPD_Q_PERM = 3,         /* int64[n]: tree position -> original index     */
+    SPD_Q_NODES = 4,        /* int64[nnodes*2]: begin, end per heap node      */
+    SPD_Q_BOXES = 5,        /* double[nnodes*2*d]: lo[d], hi[d] per node      */
+    SPD_Q_NNODES = 6,       /* int32: number of nodes                         */
+    SPD_Q_H2_RANKS = 7,     /* int32[nnodes]: skeleton size s_i (0 inactive)  */
+    SPD_Q_SKELETONS = 8,    /* int64[sum s_i]: skeleton tree positions, node order */
+    SPD_Q_LIST_COUNTS = 9,  /* int64[1 + 2L]: near pairs, then type1[k], type3[k] k=1..L */
+    SPD_Q_NEAR = 10,        /* int32[2 * nnear]: ordered near leaf pairs      */
+    SPD_Q_TYPE3 = 11,       /* int32[3 * n3]: (level, i, j) ordered Type-3 pairs */
+    SPD_Q_TYPE1 = 12,       /* int32[3 * n1]: (level, i, j) ordered Type-1 pairs */
+    SPD_Q_HSS_RANKS = 20,   /* int32[nnodes]: HSS rank r_i (levels 1..L-1)    */
+    SPD_Q_HSS_EXPORT_SIZE = 21, /* int64: doubles needed by SPD_Q_HSS_EXPORT */
+    SPD_Q_HSS_EXPORT = 22,  /* double[]: leaf D_i (n_i^2), U_i (n_i r_i) per leaf in node
+                               order; R_i (m_i r_i) per nonleaf at levels 2..L-1; then the
+                               sibling B_{c1 c2} (r_c1 r_c2) for every nonleaf parent
+                               in heap order; all column-major                   */
+    SPD_Q_HSS_PIVOTS = 23,  /* int32[sum w]: QRCP pivots of every node (w each) */
+    SPD_Q_TIMINGS = 30      /* double[16]: phase seconds of the last build      */
+};
+spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
+
+void h2_free(spd_h2_t h);
+void hss_free(spd_hss_t H);
+const char* spd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPDHSS_H */

@@ -1,0 +1,27 @@
+/* spdhss_testing.h -- internal kernels of libspdhss exported for the GPU unit
+ * tests only (single-matrix wrappers around the batched device kernels).
+ * All pointers are device pointers, column-major.  Not part of the product API. */
+#ifndef SPDHSS_TESTING_H
+#define SPDHSS_TESTING_H
+#include "spdhss.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C = alpha op(A) op(B) + beta C on FP64 DMMA tiles */
+spd_status spd_test_gemm(int transA, int transB, int m, int n, int k, double alpha, const double* A, int lda,
+                         const double* B, int ldb, double beta, double* C, int ldc, void* stream);
+/* in-place lower Cholesky; *info_host = 0 or failing column + 1 */
+spd_status spd_test_potrf(double* A, int n, int lda, int* info_host, void* stream);
+/* X := op(T)^{-1} X, uplo 'L'/'U' */
+spd_status spd_test_trsm(char uplo, int trans, const double* T, int n, int ldt, double* X, int nrhs, int ldx,
+                         void* stream);
+/* pivoted QR (R4) of `batch` matrices A_b = A + b*stride (m x n, ld); forms Q (m x r) into Q + b*qstride
+ * (ld m) when Q != NULL; piv (n per matrix) and rank (1 per matrix) on the device */
+spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t stride, int max_rank,
+                         double rel_tol, int* piv, int* rank, double* Q, int64_t qstride, void* stream);
+/* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major */
+spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,288 @@
+"""Thin Python binding of libspdhss.so (the C ABI in include/spdhss.h).
+
+Argument marshalling only: every numeric step runs in the library's CUDA
+kernels.  PyTorch provides device memory and the current stream.  There is no
+fallback: if libspdhss.so is missing or a CUDA device is absent, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspdhss.so")
+
+SPD_OK, SPD_EINVAL, SPD_ENOTPD, SPD_ENOMEM, SPD_ECUDA, SPD_ENCCL, SPD_ENOCONV = range(7)
+GAUSSIAN, MATERN32, EXPONENTIAL, IMQ = range(4)
+LAYOUT_ORIGINAL, LAYOUT_TREE = 0, 1
+Q_N, Q_LEVELS, Q_PERM, Q_NODES, Q_BOXES, Q_NNODES, Q_H2_RANKS, Q_SKELETONS = 1, 2, 3, 4, 5, 6, 7, 8
+Q_LIST_COUNTS, Q_NEAR, Q_TYPE3, Q_TYPE1 = 9, 10, 11, 12
+Q_HSS_RANKS, Q_HSS_EXPORT_SIZE, Q_HSS_EXPORT, Q_HSS_PIVOTS, Q_TIMINGS = 20, 21, 22, 23, 30
+
+
+class SpdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[spd status {code}] {msg}")
+        self.code = code
+
+
+class NotPositiveDefinite(SpdError):
+    pass
+
+
+class _Kernel(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int), ("l", ctypes.c_double), ("shift", ctypes.c_double)]
+
+
+class _H2Opts(ctypes.Structure):
+    _fields_ = [("n_proxy", ctypes.c_int), ("reserved", ctypes.c_int)]
+
+
+class PcgReport(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("converged", ctypes.c_int),
+                ("relres", ctypes.c_double), ("seconds", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libspdhss.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() or ./build_lib.sh")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, c_int, c_double = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    P = ctypes.POINTER
+    sigs = {
+        "spd_last_error": ([], ctypes.c_char_p),
+        "spd_comm_init": ([vp, c_int, c_int, P(vp)], c_int),
+        "spd_comm_free": ([vp], None),
+        "h2_build": ([vp, i64, c_int, _Kernel, c_int, c_double, P(_H2Opts), vp, vp, P(vp)], c_int),
+        "h2_matvec": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
+        "spdhss_build": ([vp, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp)], c_int),
+        "hss_solve": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
+        "pcg_solve": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
+        "spd_query": ([vp, c_int, vp, ctypes.c_size_t], c_int),
+        "h2_free": ([vp], None),
+        "hss_free": ([vp], None),
+        "spd_test_gemm": ([c_int, c_int, c_int, c_int, c_int, c_double, vp, c_int, vp, c_int, c_double,
+                           vp, c_int, vp], c_int),
+        "spd_test_potrf": ([vp, c_int, c_int, P(c_int), vp], c_int),
+        "spd_test_trsm": ([ctypes.c_char, c_int, vp, c_int, c_int, vp, c_int, c_int, vp], c_int),
+        "spd_test_qrcp": ([c_int, vp, c_int, c_int, c_int, i64, c_int, c_double, vp, vp, vp, i64, vp], c_int),
+        "spd_test_proxies": ([vp, c_int, vp, vp], c_int),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = ["spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
+            "pcg_solve", "spd_query", "h2_free", "hss_free", "spd_last_error"]
+
+
+def _check(status):
+    if status in (SPD_OK, SPD_ENOCONV):
+        return status
+    msg = lib().spd_last_error().decode()
+    if status == SPD_ENOTPD:
+        raise NotPositiveDefinite(status, msg)
+    raise SpdError(status, msg)
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dptr(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _mat(t, name):
+    """(n,) or (n, k) column-major CUDA float64 -> (ptr, ld, k)."""
+    if t.dim() == 1:
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        return _dptr(t, name), t.shape[0], 1
+    if t.stride(0) != 1:
+        raise ValueError(f"{name} must be column-major (use .t().contiguous().t())")
+    return _dptr(t, name), max(t.stride(1), t.shape[0]), t.shape[1]
+
+
+def empty_colmajor(n, k, device="cuda"):
+    import torch
+    return torch.empty((k, n), dtype=torch.float64, device=device).t()
+
+
+class H2:
+    """Handle of an H2 representation (h2_build)."""
+
+    def __init__(self, ptr, n, d):
+        self.ptr = ptr
+        self.n = n
+        self.d = d
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.h2_free(self.ptr)
+            self.ptr = None
+
+    def query(self, what, dtype, count):
+        buf = np.zeros(count, dtype=dtype)
+        _check(lib().spd_query(self.ptr, what, buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes))
+        return buf
+
+    @property
+    def levels(self):
+        return int(self.query(Q_LEVELS, np.int32, 1)[0])
+
+    @property
+    def nnodes(self):
+        return int(self.query(Q_NNODES, np.int32, 1)[0])
+
+    @property
+    def perm(self):
+        return self.query(Q_PERM, np.int64, self.n)
+
+    def nodes(self):
+        return self.query(Q_NODES, np.int64, 2 * self.nnodes).reshape(-1, 2)
+
+    def boxes(self):
+        return self.query(Q_BOXES, np.float64, 2 * self.d * self.nnodes).reshape(-1, 2, self.d)
+
+    def ranks(self):
+        return self.query(Q_H2_RANKS, np.int32, self.nnodes)
+
+    def skeletons(self):
+        r = self.ranks()
+        flat = self.query(Q_SKELETONS, np.int64, max(1, int(r.sum())))
+        out, off = {}, 0
+        for i, s in enumerate(r):
+            if s:
+                out[i] = flat[off:off + s]
+                off += s
+        return out
+
+    def list_counts(self):
+        return self.query(Q_LIST_COUNTS, np.int64, 1 + 2 * self.levels)
+
+    def near_pairs(self):
+        c = self.list_counts()
+        return self.query(Q_NEAR, np.int32, 2 * int(c[0])).reshape(-1, 2)
+
+    def type3(self):
+        c = self.list_counts()
+        n3 = int(c[1 + self.levels:].sum())
+        return self.query(Q_TYPE3, np.int32, 3 * n3).reshape(-1, 3)
+
+    def type1(self):
+        c = self.list_counts()
+        n1 = int(c[1:1 + self.levels].sum())
+        return self.query(Q_TYPE1, np.int32, 3 * n1).reshape(-1, 3)
+
+    def timings(self):
+        return self.query(Q_TIMINGS, np.float64, 16)
+
+    def proxies(self, node):
+        n_p = 4096 if self.d == 2 else 6144
+        return None if node < 0 else _proxies(self, node)
+
+
+def _proxies(h, node, n_proxy=None):
+    import torch
+    n_p = n_proxy or (4096 if h.d == 2 else 6144)
+    out = np.zeros((n_p, h.d))
+    _check(lib().spd_test_proxies(h.ptr, node, out.ctypes.data_as(ctypes.c_void_p), _stream()))
+    return out
+
+
+def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0):
+    """points: CUDA float64 (n, d) row-major, original order."""
+    if points.dim() != 2 or not points.is_contiguous():
+        raise ValueError("points must be a contiguous (n, d) tensor")
+    n, d = points.shape
+    out = ctypes.c_void_p()
+    opts = _H2Opts(int(n_proxy), 0)
+    _check(lib().h2_build(_dptr(points, "points"), n, d, _Kernel(int(kernel_id), float(ell), float(shift)),
+                          int(leaf), float(tol), ctypes.byref(opts), None, _stream(), ctypes.byref(out)))
+    return H2(out, n, d)
+
+
+def h2_matvec(h2, X, layout=LAYOUT_ORIGINAL, out=None):
+    x, ldx, k = _mat(X, "X")
+    if out is None:
+        out = empty_colmajor(h2.n, k) if X.dim() == 2 else X.new_empty(X.shape)
+    y, ldy, _ = _mat(out, "out")
+    _check(lib().h2_matvec(h2.ptr, layout, x, ldx, y, ldy, k, _stream()))
+    return out
+
+
+class HSS:
+    """Handle of an SPD HSS approximation (spdhss_build)."""
+
+    def __init__(self, ptr, h2):
+        self.ptr = ptr
+        self.h2 = h2          # keeps the H2 alive (freed after the HSS)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.hss_free(self.ptr)
+            self.ptr = None
+
+    def query(self, what, dtype, count):
+        buf = np.zeros(count, dtype=dtype)
+        _check(lib().spd_query(self.ptr, what, buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes))
+        return buf
+
+    def ranks(self):
+        return self.query(Q_HSS_RANKS, np.int32, self.h2.nnodes)
+
+    def export(self):
+        size = int(self.query(Q_HSS_EXPORT_SIZE, np.int64, 1)[0])
+        return self.query(Q_HSS_EXPORT, np.float64, max(1, size))
+
+    def timings(self):
+        return self.query(Q_TIMINGS, np.float64, 16)
+
+
+def spdhss_build(h2, rank_cap, rel_tol, oversample=10, seed=0, omega=None):
+    out = ctypes.c_void_p()
+    om = None
+    if omega is not None:
+        om, ld, w = _mat(omega, "omega")
+        if ld != h2.n or w != rank_cap + oversample:
+            raise ValueError("omega must be n x (rank_cap + oversample) with ld = n")
+    _check(lib().spdhss_build(h2.ptr, int(rank_cap), float(rel_tol), int(oversample), int(seed), om,
+                              _stream(), ctypes.byref(out)))
+    return HSS(out, h2)
+
+
+def hss_solve(hss, B, layout=LAYOUT_ORIGINAL, out=None):
+    b, ldb, k = _mat(B, "B")
+    if out is None:
+        out = empty_colmajor(hss.h2.n, k) if B.dim() == 2 else B.new_empty(B.shape)
+    x, ldx, _ = _mat(out, "out")
+    _check(lib().hss_solve(hss.ptr, layout, b, ldb, x, ldx, k, _stream()))
+    return out
+
+
+def pcg_solve(h2, hss, b, tol=1e-8, maxit=3000, layout=LAYOUT_ORIGINAL, x=None):
+    """Returns (x, PcgReport).  hss=None: unpreconditioned CG."""
+    if x is None:
+        x = b.new_zeros(b.shape)
+    rep = PcgReport()
+    _check(lib().pcg_solve(h2.ptr, hss.ptr if hss is not None else None, layout, _dptr(b, "b"),
+                           _dptr(x, "x"), float(tol), int(maxit), ctypes.byref(rep), _stream()))
+    return x, rep

@@ -1,0 +1,240 @@
+// capi.cpp -- the extern "C" boundary of libspdhss (include/spdhss.h).
+// Argument validation, error translation, layout handling.  No numerics here.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include "h2.hpp"
+#include "hss.hpp"
+#include "../../include/spdhss_testing.h"
+
+namespace spd {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace spd
+
+struct spd_comm_s { int nranks, rank; };
+
+using namespace spd;
+
+#define SPD_TRY(...)                                                      \
+    try { __VA_ARGS__; return SPD_OK; }                                   \
+    catch (const spd::Error& e) { set_last_error(e.what()); return e.code; } \
+    catch (const std::bad_alloc&) { set_last_error("host allocation failed"); return SPD_ENOMEM; } \
+    catch (const std::exception& e) { set_last_error(e.what()); return SPD_ECUDA; }
+
+extern "C" {
+
+const char* spd_last_error(void) { return g_last_error.c_str(); }
+
+spd_status spd_comm_init(const void* id, int nranks, int rank, spd_comm_t* out) {
+    SPD_TRY({
+        SPD_REQUIRE(out != nullptr, "spd_comm_init: out is NULL");
+        SPD_REQUIRE(nranks == 1 && rank == 0 && id == nullptr,
+                    "spd_comm_init: only nranks == 1 is supported in this build (subtree sharding not built)");
+        *out = new spd_comm_s{nranks, rank};
+    })
+}
+void spd_comm_free(spd_comm_t c) { delete c; }
+
+spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf, double tol,
+                    const spd_h2_opts* opts, spd_comm_t c, void* stream, spd_h2_t* out) {
+    SPD_TRY({
+        SPD_REQUIRE(out != nullptr, "h2_build: out is NULL");
+        *out = nullptr;
+        SPD_REQUIRE(pts != nullptr && n >= 1, "h2_build: need n >= 1 points");
+        SPD_REQUIRE(d == 2 || d == 3, "h2_build: d must be 2 or 3");
+        SPD_REQUIRE(leaf >= 1, "h2_build: leaf >= 1");
+        SPD_REQUIRE(tol >= 0.0 && tol < 1.0, "h2_build: tol in [0, 1)");
+        SPD_REQUIRE(k.id >= 0 && k.id <= 3, "h2_build: unknown kernel id");
+        SPD_REQUIRE(k.l > 0.0 && std::isfinite(k.l), "h2_build: kernel length l must be > 0");
+        SPD_REQUIRE(k.shift >= 0.0 && std::isfinite(k.shift), "h2_build: shift must be >= 0");
+        SPD_REQUIRE(n <= (int64_t)1 << 30, "h2_build: n too large");
+        auto* h = new spd_h2_s();
+        h->N = n; h->d = d; h->kern = k; h->kp = make_kernel(k); h->tol = tol; h->leaf = leaf;
+        h->n_proxy = (opts && opts->n_proxy > 0) ? opts->n_proxy : (d == 2 ? 4096 : 6144);
+        h->comm = c;
+        try { h2_build_impl(h, pts, (cudaStream_t)stream); }
+        catch (...) { delete h; throw; }
+        *out = h;
+    })
+}
+
+void h2_free(spd_h2_t h) { delete h; }
+
+spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t k,
+                     void* stream) {
+    SPD_TRY({
+        SPD_REQUIRE(h != nullptr, "h2_matvec: null handle");
+        SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "h2_matvec: bad layout");
+        SPD_REQUIRE(k >= 0 && ldx >= h->N && ldy >= h->N, "h2_matvec: ld must be >= n");
+        SPD_REQUIRE(k <= (1 << 20), "h2_matvec: k too large");
+        if (k == 0) return SPD_OK;
+        SPD_REQUIRE(X != nullptr && Y != nullptr, "h2_matvec: null X or Y");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (layout == SPD_LAYOUT_TREE) {
+            h2_apply_tree(h, X, ldx, Y, ldy, (int)k, s);
+        } else {
+            DBuf<double> xt((size_t)h->N * k), yt((size_t)h->N * k);
+            permute_rows(s, h->perm.p, h->N, (int)k, X, ldx, xt.p, h->N, true);
+            h2_apply_tree(h, xt.p, h->N, yt.p, h->N, (int)k, s);
+            permute_rows(s, h->perm.p, h->N, (int)k, yt.p, h->N, Y, ldy, false);
+            SPD_CUDA(cudaStreamSynchronize(s));
+        }
+    })
+}
+
+static size_t need(size_t have, size_t want) {
+    if (have < want) throw Error(SPD_EINVAL, "spd_query: buffer too small (" + std::to_string(want) + " bytes needed)");
+    return want;
+}
+
+spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
+    SPD_TRY({
+        SPD_REQUIRE(handle != nullptr && buf != nullptr, "spd_query: null argument");
+        if (what >= SPD_Q_HSS_RANKS && what < SPD_Q_TIMINGS) {
+            hss_query((const spd_hss_s*)handle, what, buf, bytes);
+            return SPD_OK;
+        }
+        if (what == SPD_Q_TIMINGS) {
+            // handle may be either kind: the first field tells (magic)
+            const spd_hss_s* H = hss_if_hss(handle);
+            const double* tm = H ? hss_timings(H) : ((const spd_h2_s*)handle)->timings;
+            need(bytes, 16 * sizeof(double));
+            std::memcpy(buf, tm, 16 * sizeof(double));
+            return SPD_OK;
+        }
+        const spd_h2_s* h = (const spd_h2_s*)handle;
+        const TreeH& t = h->tree;
+        switch (what) {
+        case SPD_Q_N: { int64_t v = h->N; std::memcpy(buf, &v, need(bytes, 8)); break; }
+        case SPD_Q_LEVELS: { int32_t v = t.L; std::memcpy(buf, &v, need(bytes, 4)); break; }
+        case SPD_Q_NNODES: { int32_t v = t.nnodes; std::memcpy(buf, &v, need(bytes, 4)); break; }
+        case SPD_Q_PERM: std::memcpy(buf, t.perm.data(), need(bytes, 8 * t.perm.size())); break;
+        case SPD_Q_NODES: {
+            std::vector<int64_t> v;
+            for (int i = 0; i < t.nnodes; ++i) { v.push_back(t.begin[i]); v.push_back(t.end[i]); }
+            std::memcpy(buf, v.data(), need(bytes, 8 * v.size()));
+            break;
+        }
+        case SPD_Q_BOXES: {
+            std::vector<double> v;
+            for (int i = 0; i < t.nnodes; ++i) {
+                for (int a = 0; a < t.d; ++a) v.push_back(t.lo[(size_t)i * t.d + a]);
+                for (int a = 0; a < t.d; ++a) v.push_back(t.hi[(size_t)i * t.d + a]);
+            }
+            std::memcpy(buf, v.data(), need(bytes, 8 * v.size()));
+            break;
+        }
+        case SPD_Q_H2_RANKS: {
+            std::vector<int32_t> v(t.nnodes, 0);
+            for (int k = 1; k < t.L; ++k)
+                for (int a = 0; a < h->lv[k].count; ++a) v[h->lv[k].first + a] = h->lv[k].rank[a];
+            std::memcpy(buf, v.data(), need(bytes, 4 * v.size()));
+            break;
+        }
+        case SPD_Q_SKELETONS: {
+            std::vector<int64_t> v;
+            for (int i = 0; i < t.nnodes; ++i) {
+                int k = t.level(i);
+                if (k >= t.L) continue;
+                const H2Level& lv = h->lv[k];
+                int a = i - lv.first;
+                if (lv.rank[a] == 0) continue;
+                std::vector<int> tmp(lv.rank[a]);
+                SPD_CUDA(cudaMemcpy(tmp.data(), lv.skel.p + lv.off[a], 4 * tmp.size(), cudaMemcpyDeviceToHost));
+                for (int x : tmp) v.push_back(x);
+            }
+            std::memcpy(buf, v.data(), need(bytes, 8 * v.size()));
+            break;
+        }
+        case SPD_Q_LIST_COUNTS: {
+            std::vector<int64_t> v{(int64_t)h->lists.near.size()};
+            for (int k = 1; k <= t.L; ++k) v.push_back((int64_t)h->lists.type1[k].size());
+            for (int k = 1; k <= t.L; ++k) v.push_back((int64_t)h->lists.type3[k].size());
+            std::memcpy(buf, v.data(), need(bytes, 8 * v.size()));
+            break;
+        }
+        case SPD_Q_NEAR: {
+            std::vector<int32_t> v;
+            for (auto& p : h->lists.near) { v.push_back(p.first); v.push_back(p.second); }
+            std::memcpy(buf, v.data(), need(bytes, 4 * v.size()));
+            break;
+        }
+        case SPD_Q_TYPE3:
+        case SPD_Q_TYPE1: {
+            std::vector<int32_t> v;
+            for (int k = 1; k <= t.L; ++k)
+                for (auto& p : (what == SPD_Q_TYPE3 ? h->lists.type3[k] : h->lists.type1[k])) {
+                    v.push_back(k); v.push_back(p.first); v.push_back(p.second);
+                }
+            std::memcpy(buf, v.data(), need(bytes, 4 * v.size()));
+            break;
+        }
+        default: throw Error(SPD_EINVAL, "spd_query: unknown query " + std::to_string(what));
+        }
+    })
+}
+
+// ------------------------------------------------------------------ testing entry points
+spd_status spd_test_gemm(int transA, int transB, int m, int n, int k, double alpha, const double* A, int lda,
+                         const double* B, int ldb, double beta, double* C, int ldc, void* stream) {
+    SPD_TRY({
+        std::vector<GemmDesc> d{{A, B, C, m, n, k, lda, ldb, ldc}};
+        gemm_batched((cudaStream_t)stream, d, transA != 0, transB != 0, alpha, beta);
+        SPD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    })
+}
+
+spd_status spd_test_potrf(double* A, int n, int lda, int* info_host, void* stream) {
+    SPD_TRY({
+        cudaStream_t s = (cudaStream_t)stream;
+        DBuf<int> info(1);
+        DBuf<double> bad(1);
+        info.zero(s);
+        potrf_batched(s, {{A, n, n, lda}}, info.p, bad.p);
+        *info_host = info.download(s)[0];
+    })
+}
+
+spd_status spd_test_trsm(char uplo, int trans, const double* T, int n, int ldt, double* X, int nrhs, int ldx,
+                         void* stream) {
+    SPD_TRY({
+        trsm_batched((cudaStream_t)stream, {{T, X, n, nrhs, ldt, ldx}}, uplo, trans != 0);
+        SPD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    })
+}
+
+spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t stride, int max_rank,
+                         double rel_tol, int* piv, int* rank, double* Q, int64_t qstride, void* stream) {
+    SPD_TRY({
+        cudaStream_t s = (cudaStream_t)stream;
+        DBuf<double> beta((size_t)batch * std::max(1, std::min(m, n)));
+        DBuf<double> norms((size_t)batch * std::max(1, n));
+        std::vector<QrcpDesc> d;
+        for (int b = 0; b < batch; ++b)
+            d.push_back({A + b * stride, m, n, ld, max_rank, piv + (size_t)b * n,
+                         beta.p + (size_t)b * std::max(1, std::min(m, n)), rank + b, norms.p + (size_t)b * std::max(1, n)});
+        qrcp_batched(s, d, rel_tol);
+        if (Q) {
+            std::vector<FormQDesc> f;
+            for (int b = 0; b < batch; ++b)
+                f.push_back({A + b * stride, d[b].beta, rank + b, Q + b * qstride, m, n, ld, m});
+            formq_batched(s, f);
+        }
+        SPD_CUDA(cudaStreamSynchronize(s));
+    })
+}
+
+spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) {
+    SPD_TRY({
+        SPD_REQUIRE(h != nullptr && P_host != nullptr, "spd_test_proxies: null argument");
+        cudaStream_t s = (cudaStream_t)stream;
+        DBuf<double> P((size_t)h->n_proxy * h->d);
+        proxies_for_node(h, node, P.p, s);
+        std::vector<double> v = P.download(s);
+        for (int p = 0; p < h->n_proxy; ++p)
+            for (int a = 0; a < h->d; ++a) P_host[(size_t)p * h->d + a] = v[(size_t)a * h->n_proxy + p];
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// common.cuh -- shared device/host helpers of libspdhss (product path).
+// Independent of oracle/: nothing here is shared with the CPU oracle.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <stdexcept>
+#include "../../include/spdhss.h"
+
+namespace spd {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    spd_status code;
+    Error(spd_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string& m);
+
+#define SPD_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw ::spd::Error(e_ == cudaErrorMemoryAllocation ? SPD_ENOMEM : SPD_ECUDA,\
+                std::string(#call) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \
+                std::to_string(__LINE__));                                              \
+    } while (0)
+#define SPD_LAUNCH() SPD_CUDA(cudaGetLastError())
+#define SPD_REQUIRE(cond, msg) do { if (!(cond)) throw ::spd::Error(SPD_EINVAL, msg); } while (0)
+
+// ---------------------------------------------------------------- device memory
+template <class T>
+struct DBuf {                       // owning device buffer
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this; }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) SPD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    void zero(cudaStream_t s) { if (n) SPD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    void upload(const std::vector<T>& h, cudaStream_t s) {
+        if (h.size() != n) alloc(h.size());
+        if (n) SPD_CUDA(cudaMemcpyAsync(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    std::vector<T> download(cudaStream_t s) const {
+        std::vector<T> h(n);
+        if (n) {
+            SPD_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+            SPD_CUDA(cudaStreamSynchronize(s));
+        }
+        return h;
+    }
+};
+
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- kernel functions
+// K as a function of r^2 (BASELINE.json forms, reading R13).
+struct KernelParams {
+    int id;
+    double l, inv_l, inv_l2, sqrt3_inv_l, l2;
+};
+inline KernelParams make_kernel(const spd_kernel& k) {
+    KernelParams p;
+    p.id = k.id; p.l = k.l; p.inv_l = 1.0 / k.l; p.inv_l2 = 1.0 / (k.l * k.l);
+    p.sqrt3_inv_l = 1.7320508075688772 / k.l; p.l2 = k.l * k.l;
+    return p;
+}
+#if defined(__CUDACC__)
+__device__ __forceinline__ double kernel_r2(const KernelParams& kp, double r2) {
+    switch (kp.id) {
+    case SPD_K_GAUSSIAN: return exp(-r2 * kp.inv_l2);
+    case SPD_K_MATERN32: { double t = sqrt(r2) * kp.sqrt3_inv_l; return (1.0 + t) * exp(-t); }
+    case SPD_K_EXPONENTIAL: return exp(-sqrt(r2) * kp.inv_l);
+    default: return rsqrt(r2 + kp.l2);
+    }
+}
+
+// ---------------------------------------------------------------- DMMA m8n8k4 fp64
+// Fragment layout (PTX ISA mma.m8n8k4 .f64): lane = 4*g + q (g = lane>>2, q = lane&3)
+//   A (8x4, row):  a = A[g][q]      B (4x8, col): b = B[q][g]
+//   C (8x8):       c0 = C[g][2q], c1 = C[g][2q+1]
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+#endif  // __CUDACC__
+
+// ---------------------------------------------------------------- batched descriptors
+struct GemmDesc {          // C = alpha op(A) op(B) + beta C ; column-major
+    const double* A; const double* B; double* C;
+    int m, n, k;
+    int lda, ldb, ldc;
+};
+struct MatDesc {           // generic m x n matrix with leading dimension
+    double* A; int m, n, ld;
+};
+struct TrsmDesc {          // X := op(T)^{-1} X, T n x n triangular, X n x nrhs
+    const double* T; double* X; int n, nrhs, ldt, ldx;
+};
+struct QrcpDesc {          // pivoted QR of A (m x n) in place
+    double* A; int m, n, ld;
+    int max_rank;
+    int* piv;              // n
+    double* beta;          // min(m, n)
+    int* rank;             // out (device)
+    double* norms;         // scratch n
+};
+
+// host launchers (dense.cu)
+void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, bool transB,
+                  double alpha, double beta);
+// info[b] = 0 on success, else first failing column + 1; bad[b] = that pivot value
+void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev, double* bad_dev);
+// uplo: 'L' lower / 'U' upper storage of T; trans: false -> T^{-1} X, true -> T^{-T} X
+void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans);
+void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol);
+// form Q[:, :r] (m x r, ld ldq) from the reflectors left in A by qrcp
+struct FormQDesc { const double* A; const double* beta; const int* rank; double* Q; int m, n, lda, ldq; };
+void formq_batched(cudaStream_t s, const std::vector<FormQDesc>& d);
+// copy/transposed copy of sub-blocks: C[m x n] (+)= alpha * (trans ? A^T : A)
+struct CopyDesc { const double* A; double* C; int m, n, lda, ldc; int trans; };
+void copy_batched(cudaStream_t s, const std::vector<CopyDesc>& d, double alpha, bool accumulate);
+void set_identity_plus(cudaStream_t s, const std::vector<MatDesc>& d);   // A += I, zero upper? no: A += I
+void zero_upper_batched(cudaStream_t s, const std::vector<MatDesc>& d);
+
+// descriptor arrays: stream-ordered device copy, freed after the launch
+template <class T>
+struct DevArray {
+    T* p = nullptr;
+    cudaStream_t s;
+    DevArray(cudaStream_t st, const std::vector<T>& h) : s(st) {
+        if (h.empty()) return;
+        SPD_CUDA(cudaMallocAsync((void**)&p, h.size() * sizeof(T), s));
+        SPD_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    ~DevArray() { if (p) cudaFreeAsync(p, s); }
+};
+
+}  // namespace spd

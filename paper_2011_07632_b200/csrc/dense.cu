@@ -1,0 +1,575 @@
+// dense.cu -- ragged batched fp64 dense kernels for sm_100a (product path).
+//
+//   gemm_batched   C = alpha op(A) op(B) + beta C, 64x64 CTA tiles, FP64 DMMA (m8n8k4)
+//   potrf_batched  A = L L^T in place (one CTA per matrix)               [P:282, P:1014]
+//   trsm_batched   X := op(T)^{-1} X, 32-row blocked substitution
+//   qrcp_batched   Businger-Golub pivoted Householder QR (reading R4) with
+//                  recomputed column norms, lowest-index ties, diag(R) >= 0.
+//                  A group of CTAs cooperates on one matrix (column-cyclic
+//                  ownership, in-kernel group barrier) so large proxy
+//                  matrices use many SMs; small matrices get one CTA.  [P:827]
+//   formq_batched  explicit Q[:, :r] from the stored reflectors
+#include "common.cuh"
+#include <algorithm>
+#include <cooperative_groups.h>
+
+namespace spd {
+
+// ================================================================= GEMM
+constexpr int GT = 64, GK = 16;
+
+struct TileRef { int desc, tm, tn; };
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ descs,
+                                                   const TileRef* __restrict__ tiles,
+                                                   double alpha, double beta) {
+    __shared__ double As[GK][GT + 1];
+    __shared__ double Bs[GK][GT + 1];
+    const TileRef tr = tiles[blockIdx.x];
+    const GemmDesc d = descs[tr.desc];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int m0 = tr.tm * GT, n0 = tr.tn * GT;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    for (int k0 = 0; k0 < d.k; k0 += GK) {
+        // load A tile (GT rows x GK k) and B tile (GK k x GT cols)
+        for (int e = tid; e < GT * GK; e += 128) {
+            int i, kk;
+            if (TA) { kk = e % GK; i = e / GK; } else { i = e % GT; kk = e / GT; }
+            int gi = m0 + i, gk = k0 + kk;
+            double v = 0.0;
+            if (gi < d.m && gk < d.k) v = TA ? d.A[gk + (size_t)gi * d.lda] : d.A[gi + (size_t)gk * d.lda];
+            As[kk][i] = v;
+        }
+        for (int e = tid; e < GT * GK; e += 128) {
+            int j, kk;
+            if (TB) { j = e % GT; kk = e / GT; } else { kk = e % GK; j = e / GK; }
+            int gj = n0 + j, gk = k0 + kk;
+            double v = 0.0;
+            if (gj < d.n && gk < d.k) v = TB ? d.B[gj + (size_t)gk * d.ldb] : d.B[gk + (size_t)gj * d.ldb];
+            Bs[kk][j] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < GK / 4; ++ks) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = As[ks * 4 + q][wm * 32 + a * 8 + g];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bf[b] = Bs[ks * 4 + q][wn * 32 + b * 8 + g];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                int i = m0 + wm * 32 + a * 8 + g;
+                int j = n0 + wn * 32 + b * 8 + 2 * q + h;
+                if (i < d.m && j < d.n) {
+                    double* c = d.C + i + (size_t)j * d.ldc;
+                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[a][b][h];
+                }
+            }
+}
+
+void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, bool transB,
+                  double alpha, double beta) {
+    std::vector<TileRef> tiles;
+    for (int i = 0; i < (int)d.size(); ++i) {
+        if (d[i].m <= 0 || d[i].n <= 0) continue;
+        if (d[i].k <= 0 && beta == 1.0) continue;
+        for (int tn = 0; tn < ceil_div(d[i].n, GT); ++tn)
+            for (int tm = 0; tm < ceil_div(d[i].m, GT); ++tm) tiles.push_back({i, tm, tn});
+    }
+    if (tiles.empty()) return;
+    DevArray<GemmDesc> dd(s, d);
+    DevArray<TileRef> dt(s, tiles);
+    for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
+        unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
+        if (!transA && !transB) gemm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+        else if (transA && !transB) gemm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+        else if (!transA && transB) gemm_kernel<false, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+        else gemm_kernel<true, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+        SPD_LAUNCH();
+    }
+}
+
+// ================================================================= POTRF
+// right-looking, column by column, in place (lower); upper triangle zeroed.
+__global__ void __launch_bounds__(256) potrf_kernel(const MatDesc* descs, int* info, double* badval) {
+    const MatDesc d = descs[blockIdx.x];
+    double* A = d.A;
+    const int n = d.m, ld = d.ld;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ double piv;
+    __shared__ int bad;
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        if (tid == 0) {
+            double a = A[j + (size_t)j * ld];
+            if (!(a > 0.0)) {               // not PD (or NaN): record first failure
+                bad = 1;
+                if (info) info[blockIdx.x] = j + 1;
+                if (badval) badval[blockIdx.x] = a;
+                a = 1.0;
+            }
+            piv = sqrt(a);
+            A[j + (size_t)j * ld] = piv;
+        }
+        __syncthreads();
+        if (bad) break;
+        const double inv = 1.0 / piv;
+        for (int i = j + 1 + tid; i < n; i += blockDim.x) A[i + (size_t)j * ld] *= inv;
+        __syncthreads();
+        for (int k = j + 1 + warp; k < n; k += nw) {
+            const double lkj = A[k + (size_t)j * ld];
+            double* ck = A + (size_t)k * ld;
+            const double* cj = A + (size_t)j * ld;
+            for (int i = k + lane; i < n; i += 32) ck[i] -= cj[i] * lkj;
+        }
+        __syncthreads();
+    }
+    for (int j = 1 + warp; j < n; j += nw)
+        for (int i = lane; i < j; i += 32) A[i + (size_t)j * ld] = 0.0;
+}
+
+void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev, double* bad_dev) {
+    if (d.empty()) return;
+    DevArray<MatDesc> dd(s, d);
+    potrf_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p, info_dev, bad_dev);
+    SPD_LAUNCH();
+}
+
+// ================================================================= TRSM
+// X := op(T)^{-1} X ; T n x n triangular.  "forward" when the effective
+// matrix op(T) is lower triangular.
+template <bool LOWER, bool TRANS>
+__global__ void __launch_bounds__(128) trsm_kernel(const TrsmDesc* descs, const int2* work) {
+    constexpr bool FWD = (LOWER != TRANS);
+    __shared__ double Td[32][33];
+    __shared__ double Xs[32][33];
+    const int2 wk = work[blockIdx.x];
+    const TrsmDesc d = descs[wk.x];
+    const int c0 = wk.y * 32;
+    const int nc = min(32, d.nrhs - c0);
+    const int n = d.n;
+    const int tid = threadIdx.x;
+    auto Tel = [&](int i, int k) -> double {   // element (i, k) of op(T)
+        return TRANS ? d.T[k + (size_t)i * d.ldt] : d.T[i + (size_t)k * d.ldt];
+    };
+    const int nblk = ceil_div(n, 32);
+    for (int bb = 0; bb < nblk; ++bb) {
+        const int blk = FWD ? bb * 32 : (nblk - 1 - bb) * 32;
+        const int nb = min(32, n - blk);
+        for (int e = tid; e < 32 * 32; e += 128) {
+            int i = e & 31, k = e >> 5;
+            Td[i][k] = (i < nb && k < nb) ? Tel(blk + i, blk + k) : 0.0;
+            Xs[i][k] = (i < nb && k < nc) ? d.X[blk + i + (size_t)(c0 + k) * d.ldx] : 0.0;
+        }
+        __syncthreads();
+        if (tid < 32 && tid < nc) {
+            const int c = tid;
+            if (FWD) {
+                for (int i = 0; i < nb; ++i) {
+                    double v = Xs[i][c];
+                    for (int k = 0; k < i; ++k) v -= Td[i][k] * Xs[k][c];
+                    Xs[i][c] = v / Td[i][i];
+                }
+            } else {
+                for (int i = nb - 1; i >= 0; --i) {
+                    double v = Xs[i][c];
+                    for (int k = i + 1; k < nb; ++k) v -= Td[i][k] * Xs[k][c];
+                    Xs[i][c] = v / Td[i][i];
+                }
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < 32 * 32; e += 128) {
+            int i = e & 31, k = e >> 5;
+            if (i < nb && k < nc) d.X[blk + i + (size_t)(c0 + k) * d.ldx] = Xs[i][k];
+        }
+        // update the remaining rows: X[r, :] -= op(T)[r, blk:blk+nb] Xblk
+        const int r_begin = FWD ? blk + nb : 0;
+        const int r_end = FWD ? n : blk;
+        for (int e = tid; e < (r_end - r_begin) * nc; e += 128) {
+            int r = r_begin + e % (r_end - r_begin);
+            int c = e / (r_end - r_begin);
+            double v = 0.0;
+            for (int k = 0; k < nb; ++k) v += Tel(r, blk + k) * Xs[k][c];
+            d.X[r + (size_t)(c0 + c) * d.ldx] -= v;
+        }
+        __syncthreads();
+    }
+}
+
+void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans) {
+    std::vector<int2> work;
+    for (int i = 0; i < (int)d.size(); ++i) {
+        if (d[i].n <= 0 || d[i].nrhs <= 0) continue;
+        for (int c = 0; c < ceil_div(d[i].nrhs, 32); ++c) work.push_back(make_int2(i, c));
+    }
+    if (work.empty()) return;
+    DevArray<TrsmDesc> dd(s, d);
+    DevArray<int2> dw(s, work);
+    unsigned nb = (unsigned)work.size();
+    bool lower = (uplo == 'L' || uplo == 'l');
+    if (lower && !trans) trsm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dw.p);
+    else if (lower && trans) trsm_kernel<true, true><<<nb, 128, 0, s>>>(dd.p, dw.p);
+    else if (!lower && !trans) trsm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dw.p);
+    else trsm_kernel<false, true><<<nb, 128, 0, s>>>(dd.p, dw.p);
+    SPD_LAUNCH();
+}
+
+// ================================================================= QRCP
+constexpr int QR_THREADS = 256;
+
+struct QrItem { int desc, g, G; };
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+// barrier among the G CTAs working on one matrix (all co-resident: cooperative launch)
+__device__ void group_barrier(unsigned* bar, int G) {
+    __syncthreads();
+    if (G > 1 && threadIdx.x == 0) {
+        volatile unsigned* vgen = bar + 1;
+        unsigned gen = *vgen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == (unsigned)G - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == gen) { __nanosleep(32); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ void block_argmax(double v, int idx, double* sv, int* si, double& bv, int& bi) {
+    // max value, lowest index on ties
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    if (lane == 0) { sv[warp] = v; si[warp] = idx; }
+    __syncthreads();
+    if (warp == 0) {
+        int nw = blockDim.x >> 5;
+        v = lane < nw ? sv[lane] : -1.0;
+        idx = lane < nw ? si[lane] : 0x7fffffff;
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+            if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+        }
+        if (lane == 0) { sv[0] = v; si[0] = idx; }
+    }
+    __syncthreads();
+    bv = sv[0];
+    bi = si[0];
+    __syncthreads();
+}
+
+__device__ double block_sum(double v, double* sv) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) sv[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int nw = blockDim.x >> 5;
+        v = lane < nw ? sv[lane] : 0.0;
+        v = warp_sum(v);
+        if (lane == 0) sv[0] = v;
+    }
+    __syncthreads();
+    double r = sv[0];
+    __syncthreads();
+    return r;
+}
+
+// squared norm of column j over rows [r0, m), one warp
+__device__ __forceinline__ double col_norm2(const double* c, int r0, int m) {
+    double s = 0.0;
+    for (int i = r0 + (threadIdx.x & 31); i < m; i += 32) { double x = ldcg(c + i); s += x * x; }
+    return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs, const QrItem* items,
+                                                          const int2* cta_items, unsigned* barriers,
+                                                          double rel_tol) {
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    __shared__ int s_stop;
+    __shared__ double s_nu0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = QR_THREADS / 32;
+    const int2 range = cta_items[blockIdx.x];
+    for (int it = range.x; it < range.y; ++it) {
+        const QrItem item = items[it];
+        const QrcpDesc d = descs[item.desc];
+        const int g = item.g, G = item.G;
+        unsigned* bar = barriers + 2 * item.desc;
+        const int m = d.m, n = d.n, ld = d.ld;
+        double* A = d.A;
+        const int kmax = min(min(m, n), d.max_rank);
+        // initial norms (rows 0..m-1) of owned columns
+        {
+            int local = 0;
+            for (int j = g; j < n; j += G, ++local)
+                if (local % nw == warp) {
+                    double s = col_norm2(A + (size_t)j * ld, 0, m);
+                    if (lane == 0) d.norms[j] = s;
+                }
+            if (g == 0)
+                for (int j = threadIdx.x; j < n; j += QR_THREADS) d.piv[j] = j;
+        }
+        if (threadIdx.x == 0) { s_stop = 0; s_nu0 = 0.0; }
+        group_barrier(bar, G);
+        for (int t = 0;; ++t) {
+            // ---- leader: pivot, stop test, Householder of column t
+            if (g == 0) {
+                double bv = -1.0;
+                int bi = 0x7fffffff;
+                if (t < kmax) {
+                    double v = -1.0;
+                    int idx = 0x7fffffff;
+                    for (int j = t + threadIdx.x; j < n; j += QR_THREADS) {
+                        double x = ldcg(d.norms + j);
+                        if (x > v) { v = x; idx = j; }   // ascending j: keeps lowest on ties
+                    }
+                    block_argmax(v, idx, sv, si, bv, bi);
+                }
+                const double nu = bv > 0.0 ? sqrt(bv) : 0.0;
+                if (threadIdx.x == 0) {
+                    if (t == 0) s_nu0 = nu;
+                    s_stop = (t >= kmax || nu == 0.0 || nu <= rel_tol * s_nu0) ? 1 : 0;
+                }
+                __syncthreads();
+                if (!s_stop) {
+                    const int p = bi;
+                    if (p != t) {
+                        double* ct = A + (size_t)t * ld;
+                        double* cp = A + (size_t)p * ld;
+                        for (int i = threadIdx.x; i < m; i += QR_THREADS) {
+                            double a = ldcg(ct + i), b = ldcg(cp + i);
+                            ct[i] = b; cp[i] = a;
+                        }
+                        if (threadIdx.x == 0) { int tp = d.piv[t]; d.piv[t] = d.piv[p]; d.piv[p] = tp; }
+                    }
+                    __syncthreads();
+                    double* ct = A + (size_t)t * ld;
+                    double sig = 0.0;
+                    for (int i = t + 1 + threadIdx.x; i < m; i += QR_THREADS) { double x = ct[i]; sig += x * x; }
+                    sig = block_sum(sig, sv);
+                    const double x0 = ct[t];
+                    double beta, mu, v0;
+                    if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
+                    else {
+                        mu = sqrt(x0 * x0 + sig);
+                        v0 = (x0 <= 0.0) ? x0 - mu : -sig / (x0 + mu);
+                        beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+                    }
+                    const double inv0 = 1.0 / v0;
+                    for (int i = t + 1 + threadIdx.x; i < m; i += QR_THREADS) ct[i] = (sig == 0.0) ? 0.0 : ct[i] * inv0;
+                    if (threadIdx.x == 0) { ct[t] = mu; d.beta[t] = beta; }
+                } else if (threadIdx.x == 0) {
+                    d.rank[0] = t;                  // stop: publish the rank (host set -1)
+                }
+                __syncthreads();
+            }
+            group_barrier(bar, G);
+            {
+                const int r = __ldcg(d.rank);
+                if (r >= 0) break;
+            }
+            // ---- all CTAs: apply H_t to owned columns j > t, recompute norms over rows t+1..
+            const double* v = A + (size_t)t * ld;     // v_t = 1 (implicit), v_i = A[i, t], i > t
+            const double beta = __ldcg(d.beta + t);
+            int local = 0;
+            for (int j = g; j < n; j += G, ++local) {
+                if (j <= t || local % nw != warp) continue;
+                double* c = A + (size_t)j * ld;
+                double s = ldcg(c + t) * (lane == 0 ? 1.0 : 0.0);
+                for (int i = t + 1 + lane; i < m; i += 32) s += ldcg(v + i) * ldcg(c + i);
+                s = warp_sum(s);
+                // lane 0 above counted c[t] * 1 only once
+                const double w = beta * s;
+                double nn = 0.0;
+                if (lane == 0) c[t] = ldcg(c + t) - w;
+                for (int i = t + 1 + lane; i < m; i += 32) {
+                    double x = ldcg(c + i) - w * ldcg(v + i);
+                    c[i] = x;
+                    nn += x * x;
+                }
+                nn = warp_sum(nn);
+                if (lane == 0) d.norms[j] = nn;
+            }
+            group_barrier(bar, G);
+        }
+        group_barrier(bar, G);
+    }
+}
+
+void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol) {
+    if (d.empty()) return;
+    int dev = 0;
+    SPD_CUDA(cudaGetDevice(&dev));
+    int nsm = 0, per_sm = 0;
+    SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_kernel, QR_THREADS, 0));
+    const int cap = std::max(1, nsm * std::max(1, per_sm));
+    // work estimate per matrix ~ m * n * min(m, n, max_rank)
+    std::vector<double> work(d.size());
+    double total = 0.0;
+    for (size_t i = 0; i < d.size(); ++i) {
+        double k = std::max(1, std::min(std::min(d[i].m, d[i].n), d[i].max_rank));
+        work[i] = (double)std::max(d[i].m, 1) * std::max(d[i].n, 1) * k;
+        total += work[i];
+    }
+    std::vector<QrItem> items;
+    std::vector<int2> cta;
+    if ((int)d.size() >= cap) {
+        // one CTA per matrix, CTAs loop over matrices (largest first, greedy balance)
+        std::vector<int> order(d.size());
+        for (size_t i = 0; i < d.size(); ++i) order[i] = (int)i;
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+        std::vector<std::vector<int>> bins(cap);
+        std::vector<double> load(cap, 0.0);
+        for (int i : order) {
+            int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            bins[b].push_back(i);
+            load[b] += work[i];
+        }
+        for (int b = 0; b < cap; ++b) {
+            int begin = (int)items.size();
+            for (int i : bins[b]) items.push_back({i, 0, 1});
+            cta.push_back(make_int2(begin, (int)items.size()));
+        }
+    } else {
+        int spare = cap - (int)d.size();
+        std::vector<int> G(d.size(), 1);
+        for (size_t i = 0; i < d.size(); ++i) {
+            int extra = (int)(spare * (work[i] / total));
+            int maxg = std::max(1, std::min(d[i].n, 64));
+            G[i] = std::min(maxg, 1 + extra);
+        }
+        for (size_t i = 0; i < d.size(); ++i)
+            for (int g = 0; g < G[i]; ++g) {
+                cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
+                items.push_back({(int)i, g, G[i]});
+            }
+    }
+    DevArray<QrcpDesc> dd(s, d);
+    DevArray<QrItem> di(s, items);
+    DevArray<int2> dc(s, cta);
+    unsigned* bars = nullptr;
+    SPD_CUDA(cudaMallocAsync((void**)&bars, sizeof(unsigned) * 2 * d.size(), s));
+    SPD_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * d.size(), s));
+    // rank = -1 marks "running"
+    std::vector<int> minus1(1, -1);
+    for (auto& q : d) SPD_CUDA(cudaMemcpyAsync(q.rank, minus1.data(), sizeof(int), cudaMemcpyHostToDevice, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    const QrcpDesc* a0 = dd.p;
+    const QrItem* a1 = di.p;
+    const int2* a2 = dc.p;
+    double tol = rel_tol;
+    void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
+    SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
+                                         args, 0, s));
+    SPD_CUDA(cudaFreeAsync(bars, s));
+}
+
+// ================================================================= FORM Q
+__global__ void __launch_bounds__(256) formq_kernel(const FormQDesc* descs) {
+    const FormQDesc d = descs[blockIdx.x];
+    const int r = *d.rank;
+    const int m = d.m;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < r; j += nw)
+        for (int i = lane; i < m; i += 32) d.Q[i + (size_t)j * d.ldq] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int t = r - 1; t >= 0; --t) {
+        const double* v = d.A + (size_t)t * d.lda;
+        const double beta = d.beta[t];
+        for (int j = t + warp; j < r; j += nw) {
+            double* q = d.Q + (size_t)j * d.ldq;
+            double s = (lane == 0) ? q[t] : 0.0;
+            for (int i = t + 1 + lane; i < m; i += 32) s += v[i] * q[i];
+            s = warp_sum(s) * beta;
+            if (lane == 0) q[t] -= s;
+            for (int i = t + 1 + lane; i < m; i += 32) q[i] -= s * v[i];
+        }
+        __syncthreads();
+    }
+}
+
+void formq_batched(cudaStream_t s, const std::vector<FormQDesc>& d) {
+    if (d.empty()) return;
+    DevArray<FormQDesc> dd(s, d);
+    formq_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p);
+    SPD_LAUNCH();
+}
+
+// ================================================================= copies
+__global__ void copy_kernel(const CopyDesc* descs, double alpha, int accumulate) {
+    const CopyDesc d = descs[blockIdx.y];
+    const int64_t total = (int64_t)d.m * d.n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int i = (int)(e % d.m), j = (int)(e / d.m);
+        double v = d.trans ? d.A[j + (size_t)i * d.lda] : d.A[i + (size_t)j * d.lda];
+        double* c = d.C + i + (size_t)j * d.ldc;
+        *c = accumulate ? *c + alpha * v : alpha * v;
+    }
+}
+
+void copy_batched(cudaStream_t s, const std::vector<CopyDesc>& d, double alpha, bool accumulate) {
+    if (d.empty()) return;
+    DevArray<CopyDesc> dd(s, d);
+    for (size_t off = 0; off < d.size(); off += 65535) {
+        unsigned ny = (unsigned)std::min<size_t>(65535, d.size() - off);
+        copy_kernel<<<dim3(8, ny), 256, 0, s>>>(dd.p + off, alpha, accumulate ? 1 : 0);
+        SPD_LAUNCH();
+    }
+}
+
+__global__ void add_identity_kernel(const MatDesc* descs) {
+    const MatDesc d = descs[blockIdx.x];
+    for (int i = threadIdx.x; i < min(d.m, d.n); i += blockDim.x) d.A[i + (size_t)i * d.ld] += 1.0;
+}
+void set_identity_plus(cudaStream_t s, const std::vector<MatDesc>& d) {
+    if (d.empty()) return;
+    DevArray<MatDesc> dd(s, d);
+    add_identity_kernel<<<(unsigned)d.size(), 128, 0, s>>>(dd.p);
+    SPD_LAUNCH();
+}
+
+__global__ void zero_upper_kernel(const MatDesc* descs) {
+    const MatDesc d = descs[blockIdx.x];
+    for (int j = 1; j < d.n; ++j)
+        for (int i = threadIdx.x; i < min(j, d.m); i += blockDim.x) d.A[i + (size_t)j * d.ld] = 0.0;
+}
+void zero_upper_batched(cudaStream_t s, const std::vector<MatDesc>& d) {
+    if (d.empty()) return;
+    DevArray<MatDesc> dd(s, d);
+    zero_upper_kernel<<<(unsigned)d.size(), 128, 0, s>>>(dd.p);
+    SPD_LAUNCH();
+}
+
+}  // namespace spd

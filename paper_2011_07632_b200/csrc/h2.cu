@@ -1,0 +1,502 @@
+// h2.cu -- H2 construction by proxy-point ID and the H2 multi-vector product.
+//
+// Build (readings R3/R4; the paper delegates the method to H2Pack,
+// P:1113-1118): per active node, proxies from a Halton sequence, the proxy
+// matrix M^T = K(Y_proxy, X_cand) evaluated on the device, pivoted QR (qrcp)
+// at relative tolerance tol, T = R11^{-1} R12 (trsm), interpolation matrix E
+// with E[piv[:s]] = I and E[piv[s+c]] = T[:, c]^T, skeleton J = cand[piv[:s]].
+// Nested: nonleaf candidates = children skeletons (eqn:nested P:218-226).
+//
+// Apply (eqn:uniformbasis_h2): near field on the fly (kblock), up pass
+// xh_i = E_i^T [x_i | xh_children] (batched DMMA GEMM), Type-3 coupling on the
+// fly (kblock over skeleton points), down pass, leaf accumulation.
+#include "h2.hpp"
+#include <algorithm>
+#include <chrono>
+
+namespace spd {
+
+// ================================================================= proxies (R3)
+struct ProxyDesc { int node; double* P; };     // P: d x n_p SoA (stride n_p)
+
+__device__ double halton_dev(long long k, int base) {
+    long long num = 0, den = 1;
+    while (k > 0) { den *= base; num = num * base + (k % base); k /= base; }
+    return __ddiv_rn((double)num, (double)den);
+}
+
+__global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, const double* lo, const double* hi,
+                                                    int d, int n_proxy) {
+    __shared__ double ilo[3], ihi[3], slo[3], shi[3], dlo[3], dhi[3];
+    __shared__ int s_cnt[8];
+    __shared__ long long s_klast;
+    const ProxyDesc pd = descs[blockIdx.x];
+    const int i = pd.node;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bases[3] = {2, 3, 5};
+    if (tid == 0) {
+        double e[3], emax = 0.0, rmax = 0.0;
+        for (int a = 0; a < d; ++a) {
+            e[a] = __dmul_rn(0.5, __dsub_rn(hi[i * d + a], lo[i * d + a]));
+            emax = fmax(emax, e[a]);
+            rmax = fmax(rmax, __dsub_rn(hi[a], lo[a]));      // root box: node 0
+        }
+        const double t3 = __dmul_rn(3.0, emax);
+        const double ext = __dmul_rn(0.1, rmax);
+        for (int a = 0; a < d; ++a) {
+            double eh = fmax(e[a], __dmul_rn(0.25, emax));
+            ilo[a] = __dsub_rn(lo[i * d + a], eh);
+            ihi[a] = __dadd_rn(hi[i * d + a], eh);
+            double c = __dmul_rn(0.5, __dadd_rn(lo[i * d + a], hi[i * d + a]));
+            slo[a] = __dsub_rn(c, t3);
+            shi[a] = __dadd_rn(c, t3);
+            dlo[a] = __dsub_rn(lo[a], ext);
+            dhi[a] = __dadd_rn(hi[a], ext);
+        }
+    }
+    __syncthreads();
+    const int n_shell = n_proxy / 2, n_dom = n_proxy - n_shell;
+    // generic ordered-acceptance scan; returns number accepted, writes at P[pos0 + idx]
+    auto scan = [&](const double* blo, const double* bhi, long long k_first, long long k_last,
+                    int quota, int pos0, bool record_last) -> int {
+        int got = 0;
+        for (long long base = k_first; base <= k_last && got < quota; base += blockDim.x) {
+            const long long k = base + tid;
+            double p[3];
+            bool ok = false;
+            if (k <= k_last) {
+                bool inside = true;
+                for (int a = 0; a < d; ++a) {
+                    double h = halton_dev(k, bases[a]);
+                    p[a] = __dadd_rn(blo[a], __dmul_rn(h, __dsub_rn(bhi[a], blo[a])));
+                    inside = inside && (ilo[a] < p[a] && p[a] < ihi[a]);
+                }
+                ok = !inside;
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, ok);
+            int wpre = __popc(bal & ((1u << lane) - 1u));
+            if (lane == 0) s_cnt[warp] = __popc(bal);
+            __syncthreads();
+            int pre = 0, tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { if (w < warp) pre += s_cnt[w]; tot += s_cnt[w]; }
+            const int pos = got + pre + wpre;
+            if (ok && pos < quota) {
+                for (int a = 0; a < d; ++a) pd.P[(size_t)a * n_proxy + pos0 + pos] = p[a];
+                if (record_last && pos == quota - 1) s_klast = k;
+            }
+            got += tot;
+            __syncthreads();
+        }
+        return min(got, quota);
+    };
+    if (tid == 0) s_klast = 0;
+    __syncthreads();
+    scan(slo, shi, 1, 1LL << 40, n_shell, 0, true);
+    __syncthreads();
+    const long long k_shell = s_klast;
+    int got = scan(dlo, dhi, 1, 64LL * n_proxy, n_dom, n_shell, false);
+    if (got < n_dom) scan(slo, shi, k_shell + 1, 1LL << 40, n_dom - got, n_shell + got, false);
+}
+
+// ================================================================= proxy matrix
+struct ProxyMatDesc {
+    const double* P;          // d x n_p
+    const double* cx; int64_t cds;   // candidate coords (stride cds)
+    int nc;
+    double* Mt;               // n_p x nc, ld n_p
+};
+__global__ void proxy_matrix_kernel(const ProxyMatDesc* descs, KernelParams kp, int d, int n_proxy) {
+    const ProxyMatDesc md = descs[blockIdx.y];
+    const int64_t total = (int64_t)n_proxy * md.nc;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int p = (int)(e % n_proxy), c = (int)(e / n_proxy);
+        double r2 = 0.0;
+        for (int a = 0; a < d; ++a) {
+            double df = md.P[(size_t)a * n_proxy + p] - md.cx[(size_t)a * md.cds + c];
+            r2 += df * df;
+        }
+        md.Mt[e] = kernel_r2(kp, r2);
+    }
+}
+
+// ================================================================= interpolation matrix
+struct IdDesc {
+    const double* Mt; int ldm;   // R11 | T in the top rows (after qrcp + trsm)
+    const int* piv; int s, nc;
+    double* E;                   // nc x s (ld nc)
+    const int* cand_ids; int64_t cand_base;   // ids = cand_ids[c] or cand_base + c
+    int* skel;                   // s tree positions
+    double* skelX; int64_t sds;  // skeleton coords (stride sds)
+};
+__global__ void build_id_kernel(const IdDesc* descs, const double* X, int64_t N, int d) {
+    const IdDesc id = descs[blockIdx.x];
+    const int s = id.s, nc = id.nc;
+    for (int64_t e = threadIdx.x; e < (int64_t)nc * s; e += blockDim.x) id.E[e] = 0.0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < s; k += blockDim.x) {
+        id.E[id.piv[k] + (size_t)k * nc] = 1.0;
+        const int c = id.piv[k];
+        const int pos = id.cand_ids ? id.cand_ids[c] : (int)(id.cand_base + c);
+        id.skel[k] = pos;
+        for (int a = 0; a < d; ++a) id.skelX[(size_t)a * id.sds + k] = X[(size_t)a * N + pos];
+    }
+    for (int64_t e = threadIdx.x; e < (int64_t)(nc - s) * s; e += blockDim.x) {
+        int k = (int)(e % s), c = (int)(e / s);
+        id.E[id.piv[s + c] + (size_t)k * nc] = id.Mt[k + (size_t)(s + c) * id.ldm];
+    }
+}
+
+// ================================================================= permutations
+__global__ void permute_kernel(const int64_t* perm, int64_t N, int k, const double* src, int64_t lds,
+                               double* dst, int64_t ldd, int to_tree) {
+    const int64_t total = N * k;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = e % N, c = e / N;
+        if (to_tree) dst[p + c * ldd] = src[perm[p] + c * lds];
+        else dst[perm[p] + c * ldd] = src[p + c * lds];
+    }
+}
+void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const double* src, int64_t lds,
+                  double* dst, int64_t ldd, bool to_tree) {
+    if (N == 0 || k == 0) return;
+    int64_t total = N * k;
+    unsigned nb = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    permute_kernel<<<nb, 256, 0, s>>>(perm, N, k, src, lds, dst, ldd, to_tree ? 1 : 0);
+    SPD_LAUNCH();
+}
+
+__global__ void points_soa_kernel(const int64_t* perm, int64_t N, int d, const double* pts, double* X) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < d; ++a) X[(size_t)a * N + p] = pts[perm[p] * d + a];
+}
+
+// ================================================================= build
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
+    const int64_t N = h->N;
+    const int d = h->d;
+    double t0 = now_s();
+    // --- tree + lists (host metadata; R1, R2)
+    std::vector<double> pts((size_t)N * d);
+    SPD_CUDA(cudaMemcpyAsync(pts.data(), pts_dev, sizeof(double) * N * d, cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    for (double v : pts) SPD_REQUIRE(std::isfinite(v), "h2_build: non-finite point coordinate");
+    build_tree(pts.data(), N, d, h->leaf, h->tree);
+    build_lists(h->tree, h->lists);
+    const TreeH& t = h->tree;
+    const int L = t.L;
+    // active nodes: Type-3 partner at own or ancestor level
+    h->active.assign(t.nnodes, 0);
+    for (int k = 1; k <= L; ++k)
+        for (auto& pr : h->lists.type3[k]) h->active[pr.first] = 1;
+    for (int i = 1; i < t.nnodes; ++i)
+        if (h->active[(i - 1) / 2]) h->active[i] = 1;
+    h->active[0] = 0;
+    double t1 = now_s();
+    h->timings[0] = t1 - t0;
+    // --- device points (tree order, SoA)
+    h->perm.upload(t.perm, s);
+    DBuf<double> pts_d((size_t)N * d);
+    SPD_CUDA(cudaMemcpyAsync(pts_d.p, pts_dev, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, s));
+    h->X.alloc((size_t)N * d);
+    points_soa_kernel<<<148 * 4, 256, 0, s>>>(h->perm.p, N, d, pts_d.p, h->X.p);
+    SPD_LAUNCH();
+    DBuf<double> lo_d, hi_d;
+    lo_d.upload(t.lo, s);
+    hi_d.upload(t.hi, s);
+
+    h->lv.clear();
+    h->lv.resize(L);
+    const int n_p = h->n_proxy;
+    const size_t budget = (size_t)6 << 30;       // bytes of proxy matrices in flight
+    for (int k = 1; k < L; ++k) {
+        H2Level& lv = h->lv[k];
+        lv.k = k; lv.first = t.first(k); lv.count = t.count(k);
+        lv.rank.assign(lv.count, 0);
+        lv.ncand.assign(lv.count, 0);
+        lv.off.assign(lv.count + 1, 0);
+        const H2Level* prev = (k > 1) ? &h->lv[k - 1] : nullptr;
+        std::vector<int> nodes;
+        for (int a = 0; a < lv.count; ++a) {
+            int i = lv.first + a;
+            if (!h->active[i]) continue;
+            if (k == 1) lv.ncand[a] = (int)t.size(i);
+            else {
+                int c1 = 2 * i + 1 - prev->first;
+                lv.ncand[a] = prev->rank[c1] + prev->rank[c1 + 1];
+            }
+            nodes.push_back(a);
+        }
+        // per-node rank, piv storage
+        std::vector<int64_t> piv_off(lv.count + 1, 0);
+        for (int a = 0; a < lv.count; ++a) piv_off[a + 1] = piv_off[a] + lv.ncand[a];
+        DBuf<int> piv_d(std::max<int64_t>(1, piv_off[lv.count]));
+        DBuf<int> rank_d(lv.count + 1);
+        rank_d.zero(s);
+        DBuf<double> beta_d(std::max<int64_t>(1, piv_off[lv.count]));
+        DBuf<double> norms_d(std::max<int64_t>(1, piv_off[lv.count]));
+        // process in chunks bounded by the proxy-matrix budget
+        struct Chunk { std::vector<int> nodes; };
+        std::vector<Chunk> chunks;
+        {
+            Chunk cur;
+            size_t bytes = 0;
+            for (int a : nodes) {
+                size_t b = (size_t)n_p * lv.ncand[a] * 8 + (size_t)n_p * d * 8;
+                if (!cur.nodes.empty() && bytes + b > budget) { chunks.push_back(cur); cur = Chunk(); bytes = 0; }
+                cur.nodes.push_back(a);
+                bytes += b;
+            }
+            if (!cur.nodes.empty()) chunks.push_back(cur);
+        }
+        // final outputs need ranks: keep each chunk's Mt until E is built
+        std::vector<int> rank_h(lv.count, 0);
+        // E, skel built per chunk into temporaries, then packed
+        struct Pending { int a; DBuf<double> E; DBuf<int> skel; DBuf<double> sx; };
+        std::vector<Pending> pend;
+        for (auto& ch : chunks) {
+            std::vector<size_t> mt_off(ch.nodes.size() + 1, 0), p_off(ch.nodes.size() + 1, 0);
+            for (size_t q = 0; q < ch.nodes.size(); ++q) {
+                mt_off[q + 1] = mt_off[q] + (size_t)n_p * lv.ncand[ch.nodes[q]];
+                p_off[q + 1] = p_off[q] + (size_t)n_p * d;
+            }
+            DBuf<double> Mt(std::max<size_t>(1, mt_off.back()));
+            DBuf<double> P(std::max<size_t>(1, p_off.back()));
+            std::vector<ProxyDesc> pdesc;
+            std::vector<ProxyMatDesc> mdesc;
+            std::vector<QrcpDesc> qdesc;
+            for (size_t q = 0; q < ch.nodes.size(); ++q) {
+                const int a = ch.nodes[q], i = lv.first + a;
+                pdesc.push_back({i, P.p + p_off[q]});
+                ProxyMatDesc md;
+                md.P = P.p + p_off[q];
+                if (k == 1) { md.cx = h->X.p + t.begin[i]; md.cds = N; }
+                else {
+                    int c1 = 2 * i + 1 - prev->first;
+                    md.cx = prev->skelX.p + prev->off[c1]; md.cds = prev->S;
+                }
+                md.nc = lv.ncand[a];
+                md.Mt = Mt.p + mt_off[q];
+                mdesc.push_back(md);
+                QrcpDesc qd;
+                qd.A = Mt.p + mt_off[q]; qd.m = n_p; qd.n = lv.ncand[a]; qd.ld = n_p;
+                qd.max_rank = std::min(n_p, lv.ncand[a]);
+                qd.piv = piv_d.p + piv_off[a];
+                qd.beta = beta_d.p + piv_off[a];
+                qd.rank = rank_d.p + a;
+                qd.norms = norms_d.p + piv_off[a];
+                qdesc.push_back(qd);
+            }
+            {
+                DevArray<ProxyDesc> dp(s, pdesc);
+                proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, d, n_p);
+                SPD_LAUNCH();
+                DevArray<ProxyMatDesc> dm(s, mdesc);
+                proxy_matrix_kernel<<<dim3(64, (unsigned)mdesc.size()), 256, 0, s>>>(dm.p, h->kp, d, n_p);
+                SPD_LAUNCH();
+            }
+            qrcp_batched(s, qdesc, h->tol);
+            std::vector<int> rk(lv.count + 1);
+            SPD_CUDA(cudaMemcpyAsync(rk.data(), rank_d.p, sizeof(int) * (lv.count + 1), cudaMemcpyDeviceToHost, s));
+            SPD_CUDA(cudaStreamSynchronize(s));
+            std::vector<TrsmDesc> tdesc;
+            for (size_t q = 0; q < ch.nodes.size(); ++q) {
+                const int a = ch.nodes[q];
+                rank_h[a] = rk[a];
+                const int sr = rk[a], nc = lv.ncand[a];
+                if (sr > 0 && nc > sr)
+                    tdesc.push_back({Mt.p + mt_off[q], Mt.p + mt_off[q] + (size_t)sr * n_p, sr, nc - sr, n_p, n_p});
+            }
+            trsm_batched(s, tdesc, 'U', false);
+            // interpolation matrices into per-node temporaries
+            std::vector<IdDesc> idesc;
+            for (size_t q = 0; q < ch.nodes.size(); ++q) {
+                const int a = ch.nodes[q], i = lv.first + a;
+                Pending pe;
+                pe.a = a;
+                const int sr = rank_h[a], nc = lv.ncand[a];
+                pe.E.alloc(std::max<int64_t>(1, (int64_t)nc * sr));
+                pe.skel.alloc(std::max(1, sr));
+                pe.sx.alloc(std::max(1, sr * d));
+                IdDesc id;
+                id.Mt = Mt.p + mt_off[q]; id.ldm = n_p;
+                id.piv = piv_d.p + piv_off[a]; id.s = sr; id.nc = nc;
+                id.E = pe.E.p;
+                if (k == 1) { id.cand_ids = nullptr; id.cand_base = t.begin[i]; }
+                else { int c1 = 2 * i + 1 - prev->first; id.cand_ids = prev->skel.p + prev->off[c1]; id.cand_base = 0; }
+                id.skel = pe.skel.p;
+                id.skelX = pe.sx.p; id.sds = std::max(1, sr);
+                idesc.push_back(id);
+                pend.push_back(std::move(pe));
+            }
+            {
+                DevArray<IdDesc> di(s, idesc);
+                build_id_kernel<<<(unsigned)idesc.size(), 256, 0, s>>>(di.p, h->X.p, N, d);
+                SPD_LAUNCH();
+            }
+            SPD_CUDA(cudaStreamSynchronize(s));   // Mt, P freed at scope exit
+        }
+        // pack level arrays
+        for (int a = 0; a < lv.count; ++a) {
+            lv.rank[a] = rank_h[a];
+            lv.off[a + 1] = lv.off[a] + lv.rank[a];
+        }
+        lv.S = lv.off[lv.count];
+        lv.E_off.assign(lv.count + 1, 0);
+        for (int a = 0; a < lv.count; ++a) lv.E_off[a + 1] = lv.E_off[a] + (int64_t)lv.ncand[a] * lv.rank[a];
+        lv.E.alloc(std::max<int64_t>(1, lv.E_off[lv.count]));
+        lv.skel.alloc(std::max<int64_t>(1, lv.S));
+        lv.skelX.alloc(std::max<int64_t>(1, lv.S * d));
+        for (auto& pe : pend) {
+            const int a = pe.a, sr = lv.rank[a];
+            if (sr == 0) continue;
+            SPD_CUDA(cudaMemcpyAsync(lv.E.p + lv.E_off[a], pe.E.p, sizeof(double) * lv.ncand[a] * sr, cudaMemcpyDeviceToDevice, s));
+            SPD_CUDA(cudaMemcpyAsync(lv.skel.p + lv.off[a], pe.skel.p, sizeof(int) * sr, cudaMemcpyDeviceToDevice, s));
+            SPD_CUDA(cudaMemcpy2DAsync(lv.skelX.p + lv.off[a], sizeof(double) * lv.S, pe.sx.p, sizeof(double) * sr,
+                                       sizeof(double) * sr, d, cudaMemcpyDeviceToDevice, s));
+        }
+        SPD_CUDA(cudaStreamSynchronize(s));
+    }
+    h->timings[1] = now_s() - t1;
+}
+
+void proxies_for_node(spd_h2_s* h, int node, double* P_dev, cudaStream_t s) {
+    SPD_REQUIRE(node >= 0 && node < h->tree.nnodes, "proxies_for_node: bad node");
+    DBuf<double> lo_d, hi_d;
+    lo_d.upload(h->tree.lo, s);
+    hi_d.upload(h->tree.hi, s);
+    std::vector<ProxyDesc> pd{{node, P_dev}};
+    DevArray<ProxyDesc> dp(s, pd);
+    proxy_kernel<<<1, 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, h->d, h->n_proxy);
+    SPD_LAUNCH();
+    SPD_CUDA(cudaStreamSynchronize(s));
+}
+
+// ================================================================= apply
+static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
+    (void)s;
+    if (h->ws_k >= k && !h->xh.empty()) return;
+    const int L = h->tree.L;
+    h->xt.alloc((size_t)h->N * k);
+    h->yt.alloc((size_t)h->N * k);
+    h->xh.clear();
+    h->yh.clear();
+    h->xh.resize(L);
+    h->yh.resize(L);
+    for (int lk = 1; lk < L; ++lk) {
+        h->xh[lk].alloc(std::max<int64_t>(1, h->lv[lk].S * k));
+        h->yh[lk].alloc(std::max<int64_t>(1, h->lv[lk].S * k));
+    }
+    h->ws_k = k;
+}
+
+// Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]
+static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
+                       std::vector<KbBlock>& blocks, std::vector<KbTarget>& targets,
+                       std::vector<KbEntry>& entries) {
+    const TreeH& t = h->tree;
+    const int l1 = t.first(1), nl = t.count(1);
+    blocks.clear(); targets.clear(); entries.clear();
+    for (int a = 0; a < nl; ++a) {
+        int i = l1 + a;
+        blocks.push_back({h->X.p + t.begin[i], h->N, (int)t.size(i), t.begin[i]});
+    }
+    size_t e = 0;
+    for (int a = 0; a < nl; ++a) {
+        int i = l1 + a;
+        KbTarget tg{a, (int)entries.size(), 0};
+        while (e < h->lists.near.size() && h->lists.near[e].first == i) {
+            int j = h->lists.near[e].second;
+            entries.push_back({j - l1, x + t.begin[j], (int)ldx, y + t.begin[i], (int)ldy, k});
+            ++e;
+        }
+        tg.e_end = (int)entries.size();
+        targets.push_back(tg);
+    }
+}
+
+void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s) {
+    const TreeH& t = h->tree;
+    const int L = t.L;
+    const int64_t N = h->N;
+    SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
+    // near field
+    {
+        std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
+        near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
+        kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
+    }
+    if (L == 1) return;
+    ensure_ws(h, k, s);
+    // up pass
+    for (int lk = 1; lk < L; ++lk) {
+        const H2Level& lv = h->lv[lk];
+        std::vector<GemmDesc> gd;
+        for (int a = 0; a < lv.count; ++a) {
+            if (lv.rank[a] == 0) continue;
+            const int i = lv.first + a;
+            GemmDesc g;
+            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
+            if (lk == 1) { g.B = x + t.begin[i]; g.ldb = (int)ldx; }
+            else {
+                const H2Level& pv = h->lv[lk - 1];
+                int c1 = 2 * i + 1 - pv.first;
+                g.B = h->xh[lk - 1].p + pv.off[c1]; g.ldb = (int)pv.S;
+            }
+            g.C = h->xh[lk].p + lv.off[a]; g.ldc = (int)lv.S;
+            g.m = lv.rank[a]; g.n = k; g.k = lv.ncand[a];
+            gd.push_back(g);
+        }
+        gemm_batched(s, gd, true, false, 1.0, 0.0);
+        if (lv.S) SPD_CUDA(cudaMemsetAsync(h->yh[lk].p, 0, sizeof(double) * lv.S * k, s));
+    }
+    // Type-3 coupling per level
+    for (int lk = 1; lk < L; ++lk) {
+        const H2Level& lv = h->lv[lk];
+        if (h->lists.type3[lk].empty()) continue;
+        std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
+        for (int a = 0; a < lv.count; ++a)
+            blocks.push_back({lv.skelX.p + lv.off[a], lv.S, lv.rank[a], -1});
+        const auto& T3 = h->lists.type3[lk];
+        size_t e = 0;
+        while (e < T3.size()) {
+            const int i = T3[e].first, a = i - lv.first;
+            KbTarget tg{a, (int)entries.size(), 0};
+            while (e < T3.size() && T3[e].first == i) {
+                const int bj = T3[e].second - lv.first;
+                if (lv.rank[bj] > 0 && lv.rank[a] > 0)
+                    entries.push_back({bj, h->xh[lk].p + lv.off[bj], (int)lv.S, h->yh[lk].p + lv.off[a], (int)lv.S, k});
+                ++e;
+            }
+            tg.e_end = (int)entries.size();
+            targets.push_back(tg);
+        }
+        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries);
+    }
+    // down pass
+    for (int lk = L - 1; lk >= 1; --lk) {
+        const H2Level& lv = h->lv[lk];
+        std::vector<GemmDesc> gd;
+        for (int a = 0; a < lv.count; ++a) {
+            if (lv.rank[a] == 0) continue;
+            const int i = lv.first + a;
+            GemmDesc g;
+            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
+            g.B = h->yh[lk].p + lv.off[a]; g.ldb = (int)lv.S;
+            if (lk == 1) { g.C = y + t.begin[i]; g.ldc = (int)ldy; }
+            else {
+                const H2Level& pv = h->lv[lk - 1];
+                int c1 = 2 * i + 1 - pv.first;
+                g.C = h->yh[lk - 1].p + pv.off[c1]; g.ldc = (int)pv.S;
+            }
+            g.m = lv.ncand[a]; g.n = k; g.k = lv.rank[a];
+            gd.push_back(g);
+        }
+        gemm_batched(s, gd, false, false, 1.0, 1.0);
+    }
+}
+
+}  // namespace spd

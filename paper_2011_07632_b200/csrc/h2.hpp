@@ -1,0 +1,58 @@
+// h2.hpp -- H2 handle (internal).  PAPER.md §5.1.
+#pragma once
+#include "common.cuh"
+#include "kblock.cuh"
+#include "tree.hpp"
+
+namespace spd {
+
+struct H2Level {
+    int k = 0, first = 0, count = 0;
+    std::vector<int> rank;        // s_i per node of the level (0 when inactive)
+    std::vector<int> ncand;       // candidates n_c per node
+    std::vector<int64_t> off;     // row offset of node i in the level's coefficient space
+    int64_t S = 0;                // sum of ranks
+    DBuf<int> skel;               // S skeleton tree positions
+    DBuf<double> skelX;           // d x S skeleton coordinates (SoA, stride S)
+    std::vector<int64_t> E_off;   // offset of E_i (n_c x s_i, col-major) in E
+    DBuf<double> E;               // leaf U_i / nonleaf R_i (interpolation matrices)
+};
+
+struct Timer;
+
+}  // namespace spd
+
+struct spd_h2_s {
+    uint32_t magic = 0x48324832u;   // 'H2H2'
+    spd::TreeH tree;
+    spd::ListsH lists;
+    std::vector<char> active;
+    spd_kernel kern{};
+    spd::KernelParams kp{};
+    double tol = 0.0;
+    int n_proxy = 0;
+    int leaf = 0;
+    int d = 0;
+    int64_t N = 0;
+    spd::DBuf<double> X;          // d x N tree-order points (SoA)
+    spd::DBuf<int64_t> perm;      // tree position -> original index
+    std::vector<spd::H2Level> lv; // [0..L-1], level k at lv[k] (lv[0] unused)
+    double timings[16] = {0};
+    // matvec workspace
+    int64_t ws_k = 0;
+    spd::DBuf<double> xt, yt;
+    std::vector<spd::DBuf<double>> xh, yh;
+    spd_comm_t comm = nullptr;
+};
+
+namespace spd {
+// y = A x in tree order (x, y: N x k, ld >= N); y is overwritten
+void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
+                   cudaStream_t s);
+// gather/scatter between original and tree order
+void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const double* src, int64_t lds,
+                  double* dst, int64_t ldd, bool to_tree);
+void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s);
+// proxy points of heap node `node` into P_dev (d x n_proxy SoA)
+void proxies_for_node(spd_h2_s* h, int node, double* P_dev, cudaStream_t s);
+}  // namespace spd

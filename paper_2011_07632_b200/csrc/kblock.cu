@@ -1,0 +1,142 @@
+// kblock.cu -- on-the-fly kernel-block x multi-vector products (product path).
+//
+// Y_e += K(P_t, P_s) X_e for every (target t, source s) entry e, where P_t, P_s
+// are point sets (tree-order points for near-field leaf blocks, skeleton points
+// for Type-3 couplings, PAPER.md eqn:uniformbasis_h2 with B^{H2}_ij =
+// K(X_{J_i}, X_{J_j}) never stored -- north star "evaluated on the fly").
+// The kernel tile is evaluated in registers/shared memory and contracted with
+// FP64 DMMA (mma.sync m8n8k4).  Owner-computes: a CTA owns a (target rows x
+// columns) tile and accumulates over all its entries, flushing when the output
+// pointer changes, so there are no atomics and the summation order is fixed.
+#include "common.cuh"
+#include "kblock.cuh"
+#include <algorithm>
+
+namespace spd {
+
+constexpr int KB_M = 64, KB_N = 64, KB_K = 16, KB_THREADS = 128;
+
+struct KbWork { int target, tm, tn; };
+
+__global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
+    KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
+    const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
+    const KbWork* __restrict__ work) {
+    __shared__ double Ks[KB_K][KB_M + 1];
+    __shared__ double Xs[KB_K][KB_N + 1];
+    __shared__ double Sx[3][KB_K];
+    const KbWork wk = work[blockIdx.x];
+    const KbTarget tg = targets[wk.target];
+    const KbBlock tb = blocks[tg.blk];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, q = lane & 3, wm = warp >> 1, wn = warp & 1;
+    const int r0 = wk.tm * KB_M, c0 = wk.tn * KB_N;
+    const int nrows = min(KB_M, tb.n - r0);
+    // my evaluation row and its coordinates
+    const int er = tid & (KB_M - 1), ec0 = (tid >> 6) * 8;
+    double rx[3] = {0.0, 0.0, 0.0};
+    if (er < nrows)
+        for (int a = 0; a < d; ++a) rx[a] = tb.x[(size_t)a * tb.ds + r0 + er];
+    const int64_t rid = tb.id0 >= 0 ? tb.id0 + r0 + er : -1;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    for (int e = tg.e_begin; e < tg.e_end; ++e) {
+        const KbEntry en = entries[e];
+        if (c0 < en.ncols) {
+            const KbBlock sb = blocks[en.src];
+            const int ncols = min(KB_N, en.ncols - c0);
+            const bool use_shift = (shift != 0.0) && rid >= 0 && sb.id0 >= 0;
+            for (int k0 = 0; k0 < sb.n; k0 += KB_K) {
+                const int nk = min(KB_K, sb.n - k0);
+                __syncthreads();
+                if (tid < KB_K * 3) {
+                    int a = tid / KB_K, c = tid % KB_K;
+                    Sx[a][c] = (a < d && c < nk) ? sb.x[(size_t)a * sb.ds + k0 + c] : 0.0;
+                }
+                for (int idx = tid; idx < KB_K * KB_N; idx += KB_THREADS) {
+                    int kk = idx % KB_K, j = idx / KB_K;
+                    Xs[kk][j] = (kk < nk && j < ncols) ? en.X[k0 + kk + (size_t)(c0 + j) * en.ldx] : 0.0;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int kc = ec0 + c;
+                    double r2 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        if (a < d) { double df = rx[a] - Sx[a][kc]; r2 += df * df; }
+                    }
+                    double kv = kernel_r2(kp, r2);
+                    if (use_shift && rid == sb.id0 + k0 + kc) kv += shift;
+                    Ks[kc][er] = (er < nrows && kc < nk) ? kv : 0.0;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int ks = 0; ks < KB_K / 4; ++ks) {
+                    double af[4], bf[4];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) af[a] = Ks[ks * 4 + q][wm * 32 + a * 8 + g];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) bf[b] = Xs[ks * 4 + q][wn * 32 + b * 8 + g];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+                }
+            }
+        }
+        const bool flush = (e + 1 == tg.e_end) || entries[e + 1].Y != en.Y;
+        if (flush) {
+            if (c0 < en.ncols) {
+                const int ncols = min(KB_N, en.ncols - c0);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            int i = wm * 32 + a * 8 + g, j = wn * 32 + b * 8 + 2 * q + h;
+                            if (i < nrows && j < ncols) en.Y[r0 + i + (size_t)(c0 + j) * en.ldy] += acc[a][b][h];
+                        }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        }
+    }
+}
+
+void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
+                  const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
+                  const std::vector<KbEntry>& entries) {
+    std::vector<KbWork> work;
+    for (int t = 0; t < (int)targets.size(); ++t) {
+        const KbTarget& tg = targets[t];
+        if (tg.e_end <= tg.e_begin) continue;
+        int maxc = 0;
+        for (int e = tg.e_begin; e < tg.e_end; ++e) maxc = std::max(maxc, entries[e].ncols);
+        const int nr = blocks[tg.blk].n;
+        for (int tn = 0; tn < ceil_div(maxc, KB_N); ++tn)
+            for (int tm = 0; tm < ceil_div(nr, KB_M); ++tm) work.push_back({t, tm, tn});
+    }
+    if (work.empty()) return;
+    // heaviest tiles first (crude LPT over the launch order)
+    std::vector<long long> cost(targets.size(), 0);
+    for (int t = 0; t < (int)targets.size(); ++t)
+        for (int e = targets[t].e_begin; e < targets[t].e_end; ++e) cost[t] += blocks[entries[e].src].n;
+    std::stable_sort(work.begin(), work.end(), [&](const KbWork& a, const KbWork& b) { return cost[a.target] > cost[b.target]; });
+    DevArray<KbBlock> db(s, blocks);
+    DevArray<KbTarget> dt(s, targets);
+    DevArray<KbEntry> de(s, entries);
+    DevArray<KbWork> dw(s, work);
+    kblock_kernel<<<(unsigned)work.size(), KB_THREADS, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);
+    SPD_LAUNCH();
+}
+
+}  // namespace spd

@@ -1,0 +1,105 @@
+"""GPU unit parity of the batched dense kernels (DMMA GEMM, potrf, trsm, QRCP)
+against numpy / the oracle's QRCP."""
+import numpy as np
+import pytest
+
+from gpu_util import cuda, host, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spd():
+    import paper_2011_07632_b200 as spd
+    spd.lib()
+    return spd
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k", [(0, 0, 64, 64, 16), (0, 0, 130, 77, 45), (1, 0, 50, 200, 300),
+                                         (0, 1, 7, 9, 3), (1, 1, 129, 65, 257), (0, 0, 1, 1, 1)])
+def test_gemm(spd, ta, tb, m, n, k):
+    import ctypes
+    rng = np.random.default_rng(m * n + k)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((n, k) if tb else (k, n))
+    C = rng.standard_normal((m, n))
+    dA, dB, dC = cuda(A), cuda(B), cuda(C)
+    st = spd.lib().spd_test_gemm(ta, tb, m, n, k, 0.7, ctypes.c_void_p(dA.data_ptr()), A.shape[0],
+                                 ctypes.c_void_p(dB.data_ptr()), B.shape[0], -0.3,
+                                 ctypes.c_void_p(dC.data_ptr()), m, spd._stream())
+    assert st == 0
+    want = 0.7 * (A.T if ta else A) @ (B.T if tb else B) - 0.3 * C
+    assert rel(host(dC), want) < 1e-14
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 100, 256, 300])
+def test_potrf_trsm(spd, n):
+    import ctypes
+    rng = np.random.default_rng(n)
+    G = rng.standard_normal((n, n))
+    A = G @ G.T + n * np.eye(n)
+    dA = cuda(A)
+    info = ctypes.c_int(-1)
+    assert spd.lib().spd_test_potrf(ctypes.c_void_p(dA.data_ptr()), n, n, ctypes.byref(info), spd._stream()) == 0
+    assert info.value == 0
+    Lg = host(dA)
+    Lw = np.linalg.cholesky(A)
+    assert rel(Lg, Lw) < 1e-13
+    X = rng.standard_normal((n, 37))
+    for uplo, trans in [("L", 0), ("L", 1), ("U", 0), ("U", 1)]:
+        T = Lw if uplo == "L" else Lw.T.copy()
+        dT, dX = cuda(T), cuda(X)
+        assert spd.lib().spd_test_trsm(uplo.encode(), trans, ctypes.c_void_p(dT.data_ptr()), n, n,
+                                       ctypes.c_void_p(dX.data_ptr()), 37, n, spd._stream()) == 0
+        want = np.linalg.solve(T.T if trans else T, X)
+        assert rel(host(dX), want) < 1e-12, (uplo, trans)
+
+
+def test_potrf_reports_not_pd(spd):
+    import ctypes
+    A = np.array([[1.0, 2.0], [2.0, 1.0]])
+    dA = cuda(A)
+    info = ctypes.c_int(0)
+    spd.lib().spd_test_potrf(ctypes.c_void_p(dA.data_ptr()), 2, 2, ctypes.byref(info), spd._stream())
+    assert info.value == 2
+
+
+@pytest.mark.parametrize("batch,m,n,cap,tol", [(3, 40, 25, 25, 0.0), (2, 300, 160, 150, 1e-3),
+                                               (5, 128, 110, 100, 1e-3), (1, 6144, 300, 300, 1e-10),
+                                               (4, 20, 60, 20, 0.0), (1, 2000, 900, 900, 1e-10)])
+def test_qrcp_matches_oracle(spd, batch, m, n, cap, tol):
+    import ctypes
+    import torch
+    import oracle
+    rng = np.random.default_rng(m + n)
+    mats = []
+    for b in range(batch):
+        # decaying spectrum so the rank rule is exercised
+        U, _ = np.linalg.qr(rng.standard_normal((m, min(m, n))))
+        V, _ = np.linalg.qr(rng.standard_normal((n, min(m, n))))
+        s = np.logspace(0, -14, min(m, n))
+        mats.append((U * s) @ V.T)
+    A = np.stack(mats)                                   # batch x m x n
+    dA = torch.tensor(np.ascontiguousarray(A.transpose(0, 2, 1)), device="cuda")  # col-major each
+    piv = torch.zeros(batch * n, dtype=torch.int32, device="cuda")
+    rank = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    Q = torch.zeros(batch * m * min(m, n, cap), dtype=torch.float64, device="cuda")
+    st = spd.lib().spd_test_qrcp(batch, ctypes.c_void_p(dA.data_ptr()), m, n, m, m * n, cap, tol,
+                                 ctypes.c_void_p(piv.data_ptr()), ctypes.c_void_p(rank.data_ptr()),
+                                 ctypes.c_void_p(Q.data_ptr()), m * min(m, n, cap), spd._stream())
+    assert st == 0, spd.lib().spd_last_error()
+    Rg = host(dA).reshape(batch, n, m).transpose(0, 2, 1)
+    pg = host(piv).reshape(batch, n)
+    rg = host(rank)
+    Qg = host(Q).reshape(batch, min(m, n, cap), m).transpose(0, 2, 1)
+    for b in range(batch):
+        Qo, Ro, po, ro = oracle.qrcp(A[b], cap, tol)
+        assert rg[b] == ro
+        r = ro
+        # pivots: equal, or a certified near-tie (reading R19) -> compare the prefix
+        same = int(np.argmax(pg[b][:r] != po[:r])) if (pg[b][:r] != po[:r]).any() else r
+        assert same >= min(r, 20), f"pivot mismatch at {same}"
+        Rb = np.triu(Rg[b][:r])
+        np.testing.assert_allclose(Rb[:, :same], Ro[:, :same], atol=1e-12 * abs(Ro[0, 0]))
+        if same == r:
+            assert rel(Qg[b][:, :r], Qo) < 1e-10
