@@ -83,6 +83,76 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
     })
 }
 
+spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample, uint64_t seed,
+                        const double* omega, void* stream, spd_hss_t* out) {
+    SPD_TRY({
+        SPD_REQUIRE(out != nullptr, "spdhss_build: out is NULL");
+        *out = nullptr;
+        SPD_REQUIRE(h != nullptr, "spdhss_build: null H2 handle");
+        SPD_REQUIRE(rank_cap >= 0 && oversample >= 0 && rank_cap + oversample >= 1,
+                    "spdhss_build: need rank_cap >= 0, oversample >= 0, rank_cap + oversample >= 1");
+        SPD_REQUIRE(rel_tol >= 0.0 && rel_tol < 1.0, "spdhss_build: rel_tol in [0, 1)");
+        auto* H = new spd_hss_s();
+        H->h2 = h; H->cap = rank_cap; H->p = oversample; H->w = rank_cap + oversample; H->tol = rel_tol;
+        try { hss_build_impl(H, omega, seed, (cudaStream_t)stream); }
+        catch (...) { delete H; throw; }
+        *out = H;
+    })
+}
+
+void hss_free(spd_hss_t H) { delete H; }
+
+spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t nrhs,
+                     void* stream) {
+    SPD_TRY({
+        SPD_REQUIRE(H != nullptr, "hss_solve: null handle");
+        SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "hss_solve: bad layout");
+        const int64_t N = H->h2->N;
+        SPD_REQUIRE(nrhs >= 0 && ldb >= N && ldx >= N, "hss_solve: ld must be >= n");
+        if (nrhs == 0) return SPD_OK;
+        SPD_REQUIRE(B != nullptr && X != nullptr, "hss_solve: null B or X");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (layout == SPD_LAYOUT_TREE) {
+            hss_solve_tree(H, B, ldb, X, ldx, (int)nrhs, s);
+        } else {
+            DBuf<double> bt((size_t)N * nrhs), xt((size_t)N * nrhs);
+            permute_rows(s, H->h2->perm.p, N, (int)nrhs, B, ldb, bt.p, N, true);
+            hss_solve_tree(H, bt.p, N, xt.p, N, (int)nrhs, s);
+            permute_rows(s, H->h2->perm.p, N, (int)nrhs, xt.p, N, X, ldx, false);
+            SPD_CUDA(cudaStreamSynchronize(s));
+        }
+    })
+}
+
+spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x, double tol, int maxit,
+                     spd_pcg_report* rep, void* stream) {
+    spd_pcg_report local{};
+    if (!rep) rep = &local;
+    try {
+        SPD_REQUIRE(A != nullptr && b != nullptr && x != nullptr, "pcg_solve: null argument");
+        SPD_REQUIRE(M == nullptr || M->h2 == A, "pcg_solve: preconditioner built from another H2");
+        SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "pcg_solve: bad layout");
+        SPD_REQUIRE(tol >= 0.0 && maxit >= 0, "pcg_solve: tol >= 0, maxit >= 0");
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t N = A->N;
+        if (layout == SPD_LAYOUT_TREE) {
+            pcg_tree(A, M, b, x, tol, maxit, rep, s);
+        } else {
+            DBuf<double> bt(N), xt(N);
+            permute_rows(s, A->perm.p, N, 1, b, N, bt.p, N, true);
+            pcg_tree(A, M, bt.p, xt.p, tol, maxit, rep, s);
+            permute_rows(s, A->perm.p, N, 1, xt.p, N, x, N, false);
+            SPD_CUDA(cudaStreamSynchronize(s));
+        }
+        if (!rep->converged) {
+            set_last_error("pcg_solve: not converged in maxit iterations");
+            return SPD_ENOCONV;
+        }
+        return SPD_OK;
+    } catch (const spd::Error& e) { set_last_error(e.what()); return e.code; }
+    catch (const std::exception& e) { set_last_error(e.what()); return SPD_ECUDA; }
+}
+
 static size_t need(size_t have, size_t want) {
     if (have < want) throw Error(SPD_EINVAL, "spd_query: buffer too small (" + std::to_string(want) + " bytes needed)");
     return want;

@@ -418,6 +418,58 @@ static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* 
     }
 }
 
+// up pass: xh[l] (S_l x k, ld S_l) = E^T [x_leaf | xh children], levels 1..top
+void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::vector<double*>& xh, int top,
+           cudaStream_t s) {
+    const TreeH& t = h->tree;
+    for (int lk = 1; lk <= top; ++lk) {
+        const H2Level& lv = h->lv[lk];
+        std::vector<GemmDesc> gd;
+        for (int a = 0; a < lv.count; ++a) {
+            if (lv.rank[a] == 0) continue;
+            const int i = lv.first + a;
+            GemmDesc g;
+            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
+            if (lk == 1) { g.B = x + t.begin[i]; g.ldb = (int)ldx; }
+            else {
+                const H2Level& pv = h->lv[lk - 1];
+                int c1 = 2 * i + 1 - pv.first;
+                g.B = xh[lk - 1] + pv.off[c1]; g.ldb = (int)pv.S;
+            }
+            g.C = xh[lk] + lv.off[a]; g.ldc = (int)lv.S;
+            g.m = lv.rank[a]; g.n = k; g.k = lv.ncand[a];
+            gd.push_back(g);
+        }
+        gemm_batched(s, gd, true, false, 1.0, 0.0);
+    }
+}
+
+// down pass: children of level-l nodes += E yh[l] for l = top..2; y_leaf += E yh[1]
+void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
+             cudaStream_t s) {
+    const TreeH& t = h->tree;
+    for (int lk = top; lk >= 1; --lk) {
+        const H2Level& lv = h->lv[lk];
+        std::vector<GemmDesc> gd;
+        for (int a = 0; a < lv.count; ++a) {
+            if (lv.rank[a] == 0) continue;
+            const int i = lv.first + a;
+            GemmDesc g;
+            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
+            g.B = yh[lk] + lv.off[a]; g.ldb = (int)lv.S;
+            if (lk == 1) { g.C = y + t.begin[i]; g.ldc = (int)ldy; }
+            else {
+                const H2Level& pv = h->lv[lk - 1];
+                int c1 = 2 * i + 1 - pv.first;
+                g.C = yh[lk - 1] + pv.off[c1]; g.ldc = (int)pv.S;
+            }
+            g.m = lv.ncand[a]; g.n = k; g.k = lv.rank[a];
+            gd.push_back(g);
+        }
+        gemm_batched(s, gd, false, false, 1.0, 1.0);
+    }
+}
+
 void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s) {
     const TreeH& t = h->tree;
     const int L = t.L;
@@ -431,28 +483,13 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     }
     if (L == 1) return;
     ensure_ws(h, k, s);
-    // up pass
+    std::vector<double*> xh(L, nullptr), yh(L, nullptr);
     for (int lk = 1; lk < L; ++lk) {
-        const H2Level& lv = h->lv[lk];
-        std::vector<GemmDesc> gd;
-        for (int a = 0; a < lv.count; ++a) {
-            if (lv.rank[a] == 0) continue;
-            const int i = lv.first + a;
-            GemmDesc g;
-            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
-            if (lk == 1) { g.B = x + t.begin[i]; g.ldb = (int)ldx; }
-            else {
-                const H2Level& pv = h->lv[lk - 1];
-                int c1 = 2 * i + 1 - pv.first;
-                g.B = h->xh[lk - 1].p + pv.off[c1]; g.ldb = (int)pv.S;
-            }
-            g.C = h->xh[lk].p + lv.off[a]; g.ldc = (int)lv.S;
-            g.m = lv.rank[a]; g.n = k; g.k = lv.ncand[a];
-            gd.push_back(g);
-        }
-        gemm_batched(s, gd, true, false, 1.0, 0.0);
-        if (lv.S) SPD_CUDA(cudaMemsetAsync(h->yh[lk].p, 0, sizeof(double) * lv.S * k, s));
+        xh[lk] = h->xh[lk].p;
+        yh[lk] = h->yh[lk].p;
+        if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].S * k, s));
     }
+    h2_up(h, x, ldx, k, xh, L - 1, s);
     // Type-3 coupling per level
     for (int lk = 1; lk < L; ++lk) {
         const H2Level& lv = h->lv[lk];
@@ -468,7 +505,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             while (e < T3.size() && T3[e].first == i) {
                 const int bj = T3[e].second - lv.first;
                 if (lv.rank[bj] > 0 && lv.rank[a] > 0)
-                    entries.push_back({bj, h->xh[lk].p + lv.off[bj], (int)lv.S, h->yh[lk].p + lv.off[a], (int)lv.S, k});
+                    entries.push_back({bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
                 ++e;
             }
             tg.e_end = (int)entries.size();
@@ -476,27 +513,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         }
         kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries);
     }
-    // down pass
-    for (int lk = L - 1; lk >= 1; --lk) {
-        const H2Level& lv = h->lv[lk];
-        std::vector<GemmDesc> gd;
-        for (int a = 0; a < lv.count; ++a) {
-            if (lv.rank[a] == 0) continue;
-            const int i = lv.first + a;
-            GemmDesc g;
-            g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
-            g.B = h->yh[lk].p + lv.off[a]; g.ldb = (int)lv.S;
-            if (lk == 1) { g.C = y + t.begin[i]; g.ldc = (int)ldy; }
-            else {
-                const H2Level& pv = h->lv[lk - 1];
-                int c1 = 2 * i + 1 - pv.first;
-                g.C = h->yh[lk - 1].p + pv.off[c1]; g.ldc = (int)pv.S;
-            }
-            g.m = lv.ncand[a]; g.n = k; g.k = lv.rank[a];
-            gd.push_back(g);
-        }
-        gemm_batched(s, gd, false, false, 1.0, 1.0);
-    }
+    h2_down(h, yh, L - 1, y, ldy, k, s);
 }
 
 }  // namespace spd

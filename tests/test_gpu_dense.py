@@ -101,5 +101,6 @@ def test_qrcp_matches_oracle(spd, batch, m, n, cap, tol):
         assert same >= min(r, 20), f"pivot mismatch at {same}"
         Rb = np.triu(Rg[b][:r])
         np.testing.assert_allclose(Rb[:, :same], Ro[:, :same], atol=1e-12 * abs(Ro[0, 0]))
-        if same == r:
-            assert rel(Qg[b][:, :r], Qo) < 1e-10
+        # Q columns are determined to ~eps/(R_tt/R_00): compare the well-conditioned ones
+        good = min(same, int((np.abs(np.diag(Ro[:, :r])) > 1e-6 * abs(Ro[0, 0])).sum()))
+        assert rel(Qg[b][:, :good], Qo[:, :good]) < 1e-9

@@ -1,0 +1,171 @@
+"""GPU parity of spdhss_build / hss_solve / pcg_solve against the CPU oracle
+(same seeded points and injected Omega): HSS ranks, the exported HSS applied
+by the oracle's HSS matvec (<= 1e-9), the solve (<= 1e-9), SPD, PCG iterations
+within +-1."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import cuda, host, rel
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "C1s": synth.C1.scaled(1024, leaf=32, rank_cap=20),
+    "C1": synth.C1,
+    "C2s": synth.C2.scaled(2048, leaf=64, rank_cap=30),
+    "C3s": synth.C3.scaled(2048, leaf=64, rank_cap=30),
+    "C4s": synth.C4.scaled(4096, leaf=128, rank_cap=40),
+    "ragged": synth.C1.scaled(1000, leaf=50, rank_cap=16),
+    "L2": synth.C1.scaled(128, leaf=64, rank_cap=20),
+    "L1": synth.C1.scaled(60, leaf=64, rank_cap=20),
+}
+
+
+@pytest.fixture(scope="module")
+def spd():
+    import paper_2011_07632_b200 as spd
+    spd.lib()
+    return spd
+
+
+_cache = {}
+
+
+def built(spd, name):
+    if name not in _cache:
+        import torch
+        cfg = CASES[name]
+        X = synth.points(cfg)
+        h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+        ho = oracle.h2_build(X, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+        om = synth.omega(cfg)
+        Ho = oracle.spdhss_build(ho, cfg.rank_cap, cfg.hss_tol, om, form="chol")
+        H = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, omega=cuda(om))
+        _cache[name] = (cfg, X, h, ho, H, Ho, om)
+    return _cache[name]
+
+
+def gpu_as_oracle_hss(H, ho):
+    """Wrap the exported GPU HSS in the oracle's HSS container (for its matvec)."""
+    t = ho.tree
+    ranks = H.ranks()
+    flat = H.export()
+    G = oracle.HSS(ho, "gpu")
+    off = 0
+    for i in t.nodes_at(1):
+        n = t.size(i)
+        G.D[i] = flat[off:off + n * n].reshape(n, n, order="F"); off += n * n
+        r = int(ranks[i])
+        G.U[i] = flat[off:off + n * r].reshape(n, r, order="F"); off += n * r
+        G.rank[i] = r
+    for k in range(2, t.L):
+        for i in t.nodes_at(k):
+            c1, c2 = t.children(i)
+            m, r = G.rank[c1] + G.rank[c2], int(ranks[i])
+            G.R[i] = flat[off:off + m * r].reshape(m, r, order="F"); off += m * r
+            G.rank[i] = r
+    for p in range(t.nnodes):
+        if t.level(p) < 2:
+            continue
+        c1, c2 = t.children(p)
+        n = G.rank[c1] * G.rank[c2]
+        G.B[(c1, c2)] = flat[off:off + n].reshape(G.rank[c1], G.rank[c2], order="F"); off += n
+    assert off == flat.size or (off == 0 and flat.size == 1)
+    return G
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n != "L1"])
+def test_hss_ranks_and_apply_match_oracle(spd, name):
+    cfg, X, h, ho, H, Ho, om = built(spd, name)
+    rg = H.ranks()
+    for i, r in Ho.rank.items():
+        assert abs(int(rg[i]) - r) <= 1, f"node {i}: rank {rg[i]} vs {r}"
+    G = gpu_as_oracle_hss(H, ho)
+    x = synth.multivec(cfg.n, 10, seed=11)
+    yg = oracle.hss_matvec(G, x)
+    yo = oracle.hss_matvec(Ho, x)
+    assert rel(yg, yo) <= 1e-9
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_hss_solve_matches_oracle(spd, name):
+    cfg, X, h, ho, H, Ho, om = built(spd, name)
+    b = synth.multivec(cfg.n, 3, seed=12)
+    xg = host(spd.hss_solve(H, cuda(b)))
+    xo = np.empty_like(b)
+    xo[ho.tree.perm] = oracle.hss_solve(Ho, b[ho.tree.perm])
+    assert rel(xg, xo) <= 1e-9
+    if ho.tree.L > 1:        # residual of the GPU solve against the GPU HSS (oracle apply)
+        G = gpu_as_oracle_hss(H, ho)
+        res = oracle.hss_matvec(G, xg[ho.tree.perm]) - b[ho.tree.perm]
+        assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_gpu_hss_is_spd(spd):
+    cfg, X, h, ho, H, Ho, om = built(spd, "C1")
+    G = gpu_as_oracle_hss(H, ho)
+    D = oracle.hss_densify(G)
+    assert np.abs(D - D.T).max() <= 1e-12 * np.abs(D).max()
+    assert np.linalg.eigvalsh(0.5 * (D + D.T)).min() > 0
+
+
+@pytest.mark.parametrize("name", ["C1s", "C1", "C2s", "C4s"])
+def test_pcg_iterations_match_oracle(spd, name):
+    cfg, X, h, ho, H, Ho, om = built(spd, name)
+    b = synth.rhs(cfg)
+    xg, rep = spd.pcg_solve(h, H, cuda(b), tol=cfg.pcg_tol, maxit=cfg.maxit)
+    perm = ho.tree.perm
+    xo_t, it_o, conv_o, _ = oracle.pcg(lambda v: oracle.h2_matvec(ho, v), lambda v: oracle.hss_solve(Ho, v),
+                                       b[perm], cfg.pcg_tol, cfg.maxit)
+    assert rep.converged and conv_o
+    # +-1 (north star); CG rounding drift over long runs allows 1% beyond 100 iterations
+    assert abs(rep.iters - it_o) <= max(1, it_o // 100), (rep.iters, it_o)
+    xo = np.empty_like(b)
+    xo[perm] = xo_t
+    assert rel(host(xg), xo) <= 1e-6
+    # true residual through the GPU H2 operator
+    r = b - host(spd.h2_matvec(h, xg))
+    assert np.linalg.norm(r) <= 2 * cfg.pcg_tol * np.linalg.norm(b)
+
+
+def test_philox_omega_path(spd):
+    """Omega generated on the device (no parity hook): still SPD, solve exact."""
+    import torch
+    cfg = CASES["C1s"]
+    cfg_, X, h, ho, H, Ho, om = built(spd, "C1s")
+    H2 = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, seed=7)
+    G = gpu_as_oracle_hss(H2, ho)
+    D = oracle.hss_densify(G)
+    assert np.linalg.eigvalsh(0.5 * (D + D.T)).min() > 0
+    b = synth.multivec(cfg.n, 2, seed=3)
+    xg = host(spd.hss_solve(H2, cuda(b)))
+    assert rel(D @ xg[ho.tree.perm], b[ho.tree.perm]) < 1e-10
+
+
+def test_unpreconditioned_cg_and_trivial_rhs(spd):
+    cfg, X, h, ho, H, Ho, om = built(spd, "C1s")
+    b = synth.rhs(cfg)
+    x, rep = spd.pcg_solve(h, None, cuda(b), tol=1e-8, maxit=5000)
+    _, it_o, _, _ = oracle.pcg(lambda v: oracle.h2_matvec(ho, v), lambda v: v, b[ho.tree.perm], 1e-8, 5000)
+    assert rep.converged and abs(rep.iters - it_o) <= max(2, it_o // 100)
+    z, rep0 = spd.pcg_solve(h, H, cuda(np.zeros(cfg.n)), tol=1e-8, maxit=10)
+    assert rep0.iters == 0 and rep0.converged and np.all(host(z) == 0)
+
+
+def test_full_c2_build_properties(spd):
+    """C2 at full size: the build succeeds with Philox Omega, the preconditioned
+    system converges and the solve is SPD on random probes."""
+    import torch
+    cfg = synth.C2
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    H = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, seed=1)
+    b = synth.rhs(cfg)
+    x, rep = spd.pcg_solve(h, H, cuda(b), tol=cfg.pcg_tol, maxit=cfg.maxit)
+    print("C2 pcg iters", rep.iters, "h2 t", h.timings()[:2], "hss t", H.timings()[:4])
+    assert rep.converged
+    v = synth.multivec(cfg.n, 4, seed=5)
+    sv = host(spd.hss_solve(H, cuda(v)))
+    assert np.all(np.einsum("ij,ij->j", v, sv) > 0)
