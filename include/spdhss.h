@@ -141,6 +141,16 @@ enum {
 };
 spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
 
+/* Instrumentation (bench.py): number of library kernel launches so far, and an
+ * optional per-kernel-class timer (CUDA events recorded on the launching stream
+ * around every launch; flops/bytes are the ALGORITHMIC counts of each launch). */
+long long spd_launch_count(void);
+void spd_prof_enable(int on);
+void spd_prof_reset(void);
+int spd_prof_count(void);
+/* out4 = {launches, total ms, total flops, total bytes}; returns 0 if idx valid */
+int spd_prof_get(int idx, char* name, int name_len, double* out4);
+
 void h2_free(spd_h2_t h);
 void hss_free(spd_hss_t H);
 const char* spd_last_error(void);

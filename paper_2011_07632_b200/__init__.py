@@ -76,6 +76,11 @@ def lib():
         "spd_test_trsm": ([ctypes.c_char, c_int, vp, c_int, c_int, vp, c_int, c_int, vp], c_int),
         "spd_test_qrcp": ([c_int, vp, c_int, c_int, c_int, i64, c_int, c_double, vp, vp, vp, i64, vp], c_int),
         "spd_test_proxies": ([vp, c_int, vp, vp], c_int),
+        "spd_launch_count": ([], ctypes.c_longlong),
+        "spd_prof_enable": ([c_int], None),
+        "spd_prof_reset": ([], None),
+        "spd_prof_count": ([], c_int),
+        "spd_prof_get": ([c_int, ctypes.c_char_p, c_int, P(c_double)], c_int),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)

@@ -26,8 +26,19 @@ void set_last_error(const std::string& m);
                 std::string(#call) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \
                 std::to_string(__LINE__));                                              \
     } while (0)
-#define SPD_LAUNCH() SPD_CUDA(cudaGetLastError())
+void count_launch();
+#define SPD_LAUNCH() do { ::spd::count_launch(); SPD_CUDA(cudaGetLastError()); } while (0)
 #define SPD_REQUIRE(cond, msg) do { if (!(cond)) throw ::spd::Error(SPD_EINVAL, msg); } while (0)
+
+// ---------------------------------------------------------------- instrumentation
+// Per-kernel-class CUDA events on the launching stream (enabled by spd_prof_enable;
+// bench.py uses it for the roofline line).  flops / bytes are ALGORITHMIC counts.
+struct ProfScope {
+    int slot = -1;
+    cudaStream_t s;
+    ProfScope(cudaStream_t st, const char* name, double flops, double bytes);
+    ~ProfScope();
+};
 
 // ---------------------------------------------------------------- device memory
 template <class T>

@@ -96,8 +96,14 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
             for (int tm = 0; tm < ceil_div(d[i].m, GT); ++tm) tiles.push_back({i, tm, tn});
     }
     if (tiles.empty()) return;
+    double fl = 0, by = 0;
+    for (auto& g : d) if (g.m > 0 && g.n > 0 && g.k > 0) {
+        fl += 2.0 * g.m * g.n * g.k;
+        by += 8.0 * ((double)g.m * g.k + (double)g.k * g.n + 2.0 * g.m * g.n);
+    }
     DevArray<GemmDesc> dd(s, d);
     DevArray<TileRef> dt(s, tiles);
+    ProfScope prof(s, "gemm_dmma", fl, by);
     for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
         unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
         if (!transA && !transB) gemm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
@@ -150,7 +156,10 @@ __global__ void __launch_bounds__(256) potrf_kernel(const MatDesc* descs, int* i
 
 void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev, double* bad_dev) {
     if (d.empty()) return;
+    double fl = 0, by = 0;
+    for (auto& m : d) { fl += (double)m.m * m.m * m.m / 3.0; by += 16.0 * m.m * m.m; }
     DevArray<MatDesc> dd(s, d);
+    ProfScope prof(s, "potrf", fl, by);
     potrf_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p, info_dev, bad_dev);
     SPD_LAUNCH();
 }
@@ -224,8 +233,11 @@ void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, boo
         for (int c = 0; c < ceil_div(d[i].nrhs, 32); ++c) work.push_back(make_int2(i, c));
     }
     if (work.empty()) return;
+    double fl = 0, by = 0;
+    for (auto& t : d) { fl += (double)t.n * t.n * t.nrhs; by += 8.0 * ((double)t.n * t.n / 2 + 2.0 * t.n * t.nrhs); }
     DevArray<TrsmDesc> dd(s, d);
     DevArray<int2> dw(s, work);
+    ProfScope prof(s, "trsm", fl, by);
     unsigned nb = (unsigned)work.size();
     bool lower = (uplo == 'L' || uplo == 'l');
     if (lower && !trans) trsm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dw.p);
@@ -476,6 +488,8 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
                 items.push_back({(int)i, g, G[i]});
             }
     }
+    double fl = 0, by = 0;
+    for (size_t i = 0; i < d.size(); ++i) { fl += 4.0 * work[i]; by += 8.0 * d[i].m * d[i].n; }
     DevArray<QrcpDesc> dd(s, d);
     DevArray<QrItem> di(s, items);
     DevArray<int2> dc(s, cta);
@@ -491,8 +505,10 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
     const int2* a2 = dc.p;
     double tol = rel_tol;
     void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
+    ProfScope prof(s, "qrcp", fl, by);     // flops: upper bound 4 m n kmax (rank unknown at launch)
     SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
                                          args, 0, s));
+    count_launch();
     SPD_CUDA(cudaFreeAsync(bars, s));
 }
 
@@ -523,6 +539,7 @@ __global__ void __launch_bounds__(256) formq_kernel(const FormQDesc* descs) {
 void formq_batched(cudaStream_t s, const std::vector<FormQDesc>& d) {
     if (d.empty()) return;
     DevArray<FormQDesc> dd(s, d);
+    ProfScope prof(s, "formq", 0, 0);
     formq_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p);
     SPD_LAUNCH();
 }
@@ -542,6 +559,7 @@ __global__ void copy_kernel(const CopyDesc* descs, double alpha, int accumulate)
 void copy_batched(cudaStream_t s, const std::vector<CopyDesc>& d, double alpha, bool accumulate) {
     if (d.empty()) return;
     DevArray<CopyDesc> dd(s, d);
+    ProfScope prof(s, "copy", 0, 0);
     for (size_t off = 0; off < d.size(); off += 65535) {
         unsigned ny = (unsigned)std::min<size_t>(65535, d.size() - off);
         copy_kernel<<<dim3(8, ny), 256, 0, s>>>(dd.p + off, alpha, accumulate ? 1 : 0);

@@ -292,9 +292,13 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             }
             {
                 DevArray<ProxyDesc> dp(s, pdesc);
+                ProfScope prof(s, "proxy_points", 0, 0);
                 proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, d, n_p);
                 SPD_LAUNCH();
                 DevArray<ProxyMatDesc> dm(s, mdesc);
+                double by = 0;
+                for (auto& m : mdesc) by += 8.0 * n_p * m.nc;
+                ProfScope prof2(s, "proxy_matrix", 0, by);
                 proxy_matrix_kernel<<<dim3(64, (unsigned)mdesc.size()), 256, 0, s>>>(dm.p, h->kp, d, n_p);
                 SPD_LAUNCH();
             }
@@ -334,6 +338,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             }
             {
                 DevArray<IdDesc> di(s, idesc);
+                ProfScope prof(s, "build_id", 0, 0);
                 build_id_kernel<<<(unsigned)idesc.size(), 256, 0, s>>>(di.p, h->X.p, N, d);
                 SPD_LAUNCH();
             }

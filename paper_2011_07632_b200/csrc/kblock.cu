@@ -131,10 +131,19 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     for (int t = 0; t < (int)targets.size(); ++t)
         for (int e = targets[t].e_begin; e < targets[t].e_end; ++e) cost[t] += blocks[entries[e].src].n;
     std::stable_sort(work.begin(), work.end(), [&](const KbWork& a, const KbWork& b) { return cost[a.target] > cost[b.target]; });
+    double fl = 0, by = 0, ev = 0;
+    for (const auto& tg : targets)
+        for (int e = tg.e_begin; e < tg.e_end; ++e) {
+            const double nr = blocks[tg.blk].n, ns = blocks[entries[e].src].n, nc = entries[e].ncols;
+            fl += 2.0 * nr * ns * nc;
+            ev += nr * ns;
+            by += 8.0 * (ns * nc + 2.0 * nr * nc);
+        }
     DevArray<KbBlock> db(s, blocks);
     DevArray<KbTarget> dt(s, targets);
     DevArray<KbEntry> de(s, entries);
     DevArray<KbWork> dw(s, work);
+    ProfScope prof(s, "kblock_dmma", fl, by);
     kblock_kernel<<<(unsigned)work.size(), KB_THREADS, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);
     SPD_LAUNCH();
 }

@@ -1,0 +1,85 @@
+// prof.cpp -- launch counter and per-kernel-class event timing (instrumentation).
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include "common.cuh"
+
+namespace spd {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct Rec { std::string name; double flops, bytes; cudaEvent_t a, b; };
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+cudaEvent_t get_ev() {
+    if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+struct Agg { long long n = 0; double ms = 0, flops = 0, bytes = 0; };
+std::map<std::string, Agg> g_agg;
+void drain() {       // caller holds the mutex
+    for (auto& r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        Agg& a = g_agg[r.name];
+        a.n += 1; a.ms += ms; a.flops += r.flops; a.bytes += r.bytes;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+}
+}  // namespace
+
+ProfScope::ProfScope(cudaStream_t st, const char* name, double flops, double bytes) : s(st) {
+    if (!g_on) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Rec r{name, flops, bytes, get_ev(), get_ev()};
+    cudaEventRecord(r.a, s);
+    g_recs.push_back(r);
+    slot = (int)g_recs.size() - 1;
+}
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaEventRecord(g_recs[slot].b, s);
+    if (g_recs.size() > 20000) drain();
+}
+
+}  // namespace spd
+
+extern "C" {
+void spd_prof_enable(int on) { spd::g_on = on != 0; }
+void spd_prof_reset(void) {
+    std::lock_guard<std::mutex> lk(spd::g_mu);
+    spd::drain();
+    spd::g_agg.clear();
+}
+int spd_prof_count(void) {
+    std::lock_guard<std::mutex> lk(spd::g_mu);
+    spd::drain();
+    return (int)spd::g_agg.size();
+}
+int spd_prof_get(int idx, char* name, int name_len, double* out4) {
+    std::lock_guard<std::mutex> lk(spd::g_mu);
+    spd::drain();
+    int i = 0;
+    for (auto& kv : spd::g_agg) {
+        if (i++ != idx) continue;
+        std::strncpy(name, kv.first.c_str(), name_len - 1);
+        name[name_len - 1] = 0;
+        out4[0] = (double)kv.second.n; out4[1] = kv.second.ms; out4[2] = kv.second.flops; out4[3] = kv.second.bytes;
+        return 0;
+    }
+    return 1;
+}
+long long spd_launch_count(void) { return spd::g_launches.load(); }
+}

@@ -71,6 +71,7 @@ __global__ void dense_kernel_blocks(const DenseKDesc* descs, KernelParams kp, do
 static void dense_blocks(cudaStream_t s, const std::vector<DenseKDesc>& d, const KernelParams& kp, double shift, int dim) {
     if (d.empty()) return;
     DevArray<DenseKDesc> dd(s, d);
+    ProfScope prof(s, "dense_blocks", 0, 0);
     for (size_t off = 0; off < d.size(); off += 65535) {
         unsigned ny = (unsigned)std::min<size_t>(65535, d.size() - off);
         dense_kernel_blocks<<<dim3(16, ny), 256, 0, s>>>(dd.p + off, kp, shift, dim);
