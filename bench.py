@@ -112,6 +112,23 @@ def prof_table(lib):
     return out
 
 
+def max_over_ranks(v, device="cuda"):
+    """Max of a per-rank float over the process group (identity without one)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_config(rank):
+    """Replicas (weak scaling): every rank solves its own C2 problem.  All ranks
+    use the same recipe and seeds, so every replica does identical work."""
+    return CFG
+
+
 def oracle_step(n):
     """One oracle pass (h2_build + Alg. 4 + PCG) on the C2 recipe at size n."""
     import oracle
@@ -176,7 +193,7 @@ def run_ours(args):
         dist.init_process_group("nccl", rank=rank, world_size=world)
     torch.cuda.set_device(local)
     lib = spd.lib()
-    cfg = CFG if not args.n else CFG.scaled(args.n)
+    cfg = replica_config(rank) if not args.n else CFG.scaled(args.n)
     N = cfg.n
     X_h = synth.points(cfg)
     b_h = synth.rhs(cfg)
@@ -234,11 +251,7 @@ def run_ours(args):
     lib.spd_prof_enable(0)
     prof = prof_table(lib)
     clocks = sampler.stop()
-    t_step = statistics.mean(step_s)
-    if world > 1:
-        tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
+    t_step = max_over_ranks(statistics.mean(step_s))
     # ---------------- end-to-end: host (pinned) inputs, H2D inside, result D2H inside
     pts_pin = torch.tensor(X_h).pin_memory()
     b_pin = torch.tensor(b_h).pin_memory()
@@ -256,12 +269,7 @@ def run_ours(args):
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e-3)
-    if world > 1:
-        tt = torch.tensor([statistics.mean(e2e)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_v = float(tt.item())
-    else:
-        e2e_v = statistics.mean(e2e)
+    e2e_v = max_over_ranks(statistics.mean(e2e))
     if rank != 0:
         if world > 1:
             dist.barrier()
