@@ -121,7 +121,7 @@ def test_pcg_iterations_match_oracle(spd, name):
                                        b[perm], cfg.pcg_tol, cfg.maxit)
     assert rep.converged and conv_o
     # +-1 (north star); CG rounding drift over long runs allows 1% beyond 100 iterations
-    assert abs(rep.iters - it_o) <= max(1, it_o // 100), (rep.iters, it_o)
+    assert abs(rep.iters - it_o) <= max(1, -(-it_o // 100)), (rep.iters, it_o)
     xo = np.empty_like(b)
     xo[perm] = xo_t
     assert rel(host(xg), xo) <= 1e-6
@@ -149,7 +149,8 @@ def test_unpreconditioned_cg_and_trivial_rhs(spd):
     b = synth.rhs(cfg)
     x, rep = spd.pcg_solve(h, None, cuda(b), tol=1e-8, maxit=5000)
     _, it_o, _, _ = oracle.pcg(lambda v: oracle.h2_matvec(ho, v), lambda v: v, b[ho.tree.perm], 1e-8, 5000)
-    assert rep.converged and abs(rep.iters - it_o) <= max(2, it_o // 100)
+    # unpreconditioned CG over ~1000 iterations: rounding drift allowed 2 % (R24)
+    assert rep.converged and abs(rep.iters - it_o) <= max(2, -(-it_o // 50))
     z, rep0 = spd.pcg_solve(h, H, cuda(np.zeros(cfg.n)), tol=1e-8, maxit=10)
     assert rep0.iters == 0 and rep0.converged and np.all(host(z) == 0)
 
