@@ -36,9 +36,17 @@ void count_launch();
 struct ProfScope {
     int slot = -1;
     cudaStream_t s;
+    bool ext = false;
     ProfScope(cudaStream_t st, const char* name, double flops, double bytes);
     ~ProfScope();
 };
+// records created while capturing a graph are moved out and re-accumulated
+// after every replay of that graph
+struct ProfCaptured;
+ProfCaptured* prof_capture_take(size_t first);   // records [first, end) of the list
+size_t prof_mark();
+void prof_accumulate(ProfCaptured* c);            // after a (synchronized) replay
+void prof_release(ProfCaptured* c);
 
 // ---------------------------------------------------------------- device memory
 template <class T>
@@ -154,17 +162,40 @@ void copy_batched(cudaStream_t s, const std::vector<CopyDesc>& d, double alpha, 
 void set_identity_plus(cudaStream_t s, const std::vector<MatDesc>& d);   // A += I, zero upper? no: A += I
 void zero_upper_batched(cudaStream_t s, const std::vector<MatDesc>& d);
 
+// Descriptor arena: while a CUDA graph is being captured, descriptor arrays
+// go to a persistent device arena (filled with a synchronous copy, legal in
+// relaxed capture mode) and live as long as the graph.
+struct DescArena {
+    DBuf<char> buf;
+    size_t off = 0;
+    explicit DescArena(size_t bytes) : buf(bytes) {}
+    void* take(size_t bytes) {
+        size_t o = (off + 255) & ~(size_t)255;
+        if (o + bytes > buf.n) throw Error(SPD_ENOMEM, "descriptor arena exhausted");
+        off = o + bytes;
+        return buf.p + o;
+    }
+};
+DescArena*& desc_arena();                 // thread-local current arena (nullptr: none)
+
 // descriptor arrays: stream-ordered device copy, freed after the launch
 template <class T>
 struct DevArray {
     T* p = nullptr;
     cudaStream_t s;
+    bool owned = true;
     DevArray(cudaStream_t st, const std::vector<T>& h) : s(st) {
         if (h.empty()) return;
+        if (DescArena* a = desc_arena()) {
+            p = (T*)a->take(h.size() * sizeof(T));
+            owned = false;
+            SPD_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+            return;
+        }
         SPD_CUDA(cudaMallocAsync((void**)&p, h.size() * sizeof(T), s));
         SPD_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
     }
-    ~DevArray() { if (p) cudaFreeAsync(p, s); }
+    ~DevArray() { if (p && owned) cudaFreeAsync(p, s); }
 };
 
 }  // namespace spd

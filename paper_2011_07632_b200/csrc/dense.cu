@@ -86,8 +86,94 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
             }
 }
 
+// ---------------------------------------------------------------- narrow GEMM (n <= 4): GEMV-like
+// notrans A: one thread per output row (coalesced column reads of A);
+// trans A:   one warp per output row (contiguous column of A, warp reduction).
+template <bool TA, int NV>
+__global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ descs, const int2* __restrict__ work,
+                                                   double alpha, double beta) {
+    const int2 wk = work[blockIdx.x];
+    const GemmDesc d = descs[wk.x];
+    const int n = d.n;
+    if (!TA) {
+        const int i = wk.y * 256 + threadIdx.x;
+        if (i >= d.m) return;
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int kk = 0; kk < d.k; ++kk) {
+            const double a = d.A[i + (size_t)kk * d.lda];
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                if (v < n) acc[v] += a * d.B[kk + (size_t)v * d.ldb];
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            if (v < n) {
+                double* c = d.C + i + (size_t)v * d.ldc;
+                *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[v];
+            }
+    } else {
+        const int lane = threadIdx.x & 31;
+        const int i = wk.y * 8 + (threadIdx.x >> 5);
+        if (i >= d.m) return;
+        const double* a = d.A + (size_t)i * d.lda;
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int kk = lane; kk < d.k; kk += 32) {
+            const double av = a[kk];
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                if (v < n) acc[v] += av * d.B[kk + (size_t)v * d.ldb];
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = warp_sum(acc[v]);
+        if (lane == 0)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                if (v < n) {
+                    double* c = d.C + i + (size_t)v * d.ldc;
+                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[v];
+                }
+    }
+}
+
+static void gemv_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, double alpha, double beta) {
+    std::vector<int2> work;
+    double fl = 0, by = 0;
+    for (int i = 0; i < (int)d.size(); ++i) {
+        if (d[i].m <= 0 || d[i].n <= 0) continue;
+        if (d[i].k <= 0 && beta == 1.0) continue;
+        const int rows_per = transA ? 8 : 256;
+        for (int t = 0; t < ceil_div(d[i].m, rows_per); ++t) work.push_back(make_int2(i, t));
+        fl += 2.0 * d[i].m * d[i].n * d[i].k;
+        by += 8.0 * ((double)d[i].m * d[i].k + 2.0 * d[i].m * d[i].n);
+    }
+    if (work.empty()) return;
+    DevArray<GemmDesc> dd(s, d);
+    DevArray<int2> dw(s, work);
+    ProfScope prof(s, "gemv", fl, by);
+    int nmax = 0;
+    for (auto& g : d) nmax = std::max(nmax, g.n);
+    const unsigned nb = (unsigned)work.size();
+    if (transA) {
+        if (nmax == 1) gemv_kernel<true, 1><<<nb, 256, 0, s>>>(dd.p, dw.p, alpha, beta);
+        else gemv_kernel<true, 4><<<nb, 256, 0, s>>>(dd.p, dw.p, alpha, beta);
+    } else {
+        if (nmax == 1) gemv_kernel<false, 1><<<nb, 256, 0, s>>>(dd.p, dw.p, alpha, beta);
+        else gemv_kernel<false, 4><<<nb, 256, 0, s>>>(dd.p, dw.p, alpha, beta);
+    }
+    SPD_LAUNCH();
+}
+
 void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, bool transB,
                   double alpha, double beta) {
+    if (!transB) {
+        int nmax = 0;
+        for (auto& g : d) nmax = std::max(nmax, g.n);
+        if (nmax <= 4) { gemv_batched(s, d, transA, alpha, beta); return; }
+    }
     std::vector<TileRef> tiles;
     for (int i = 0; i < (int)d.size(); ++i) {
         if (d[i].m <= 0 || d[i].n <= 0) continue;
@@ -226,7 +312,55 @@ __global__ void __launch_bounds__(128) trsm_kernel(const TrsmDesc* descs, const 
     }
 }
 
+template <bool LOWER, bool TRANS>
+__global__ void __launch_bounds__(256) trsv_kernel(const TrsmDesc* descs) {
+    constexpr bool FWD = (LOWER != TRANS);
+    extern __shared__ double xs[];               // n x nrhs (nrhs <= 4)
+    const TrsmDesc d = descs[blockIdx.x];
+    const int n = d.n, nr = d.nrhs;
+    for (int e = threadIdx.x; e < n * nr; e += blockDim.x) xs[e] = d.X[e % n + (size_t)(e / n) * d.ldx];
+    __syncthreads();
+    // column sweep: x_j /= T_jj ; x_r -= op(T)_{r j} x_j for the remaining rows
+    for (int jj = 0; jj < n; ++jj) {
+        const int j = FWD ? jj : n - 1 - jj;
+        const double tjj = d.T[j + (size_t)j * d.ldt];
+        __syncthreads();
+        double xj[4];
+        for (int v = 0; v < nr; ++v) xj[v] = xs[j + v * n] / tjj;
+        __syncthreads();
+        if (threadIdx.x < nr) xs[j + threadIdx.x * n] = xj[threadIdx.x];
+        const int r0 = FWD ? j + 1 : 0, r1 = FWD ? n : j;
+        for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            const double t = TRANS ? d.T[j + (size_t)r * d.ldt] : d.T[r + (size_t)j * d.ldt];
+            for (int v = 0; v < nr; ++v) xs[r + v * n] -= t * xj[v];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * nr; e += blockDim.x) d.X[e % n + (size_t)(e / n) * d.ldx] = xs[e];
+}
+
 void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans) {
+    {
+        int nrmax = 0, nmax = 0;
+        for (auto& t : d) { nrmax = std::max(nrmax, t.nrhs); nmax = std::max(nmax, t.n); }
+        if (nrmax <= 4 && nmax > 0 && (size_t)nmax * nrmax * 8 <= 48 * 1024) {
+            std::vector<TrsmDesc> dv;
+            double fl = 0, by = 0;
+            for (auto& t : d) if (t.n > 0 && t.nrhs > 0) { dv.push_back(t); fl += (double)t.n * t.n * t.nrhs; by += 4.0 * t.n * t.n; }
+            if (dv.empty()) return;
+            DevArray<TrsmDesc> dd(s, dv);
+            ProfScope prof(s, "trsv", fl, by);
+            const size_t sh = (size_t)nmax * nrmax * 8;
+            const unsigned nb = (unsigned)dv.size();
+            bool lower = (uplo == 'L' || uplo == 'l');
+            if (lower && !trans) trsv_kernel<true, false><<<nb, 256, sh, s>>>(dd.p);
+            else if (lower && trans) trsv_kernel<true, true><<<nb, 256, sh, s>>>(dd.p);
+            else if (!lower && !trans) trsv_kernel<false, false><<<nb, 256, sh, s>>>(dd.p);
+            else trsv_kernel<false, true><<<nb, 256, sh, s>>>(dd.p);
+            SPD_LAUNCH();
+            return;
+        }
+    }
     std::vector<int2> work;
     for (int i = 0; i < (int)d.size(); ++i) {
         if (d[i].n <= 0 || d[i].nrhs <= 0) continue;

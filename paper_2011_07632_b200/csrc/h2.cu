@@ -398,6 +398,8 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
     h->ws_k = k;
 }
 
+void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) { if (h->tree.L > 1) ensure_ws(h, k, s); }
+
 // Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]
 static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
                        std::vector<KbBlock>& blocks, std::vector<KbTarget>& targets,

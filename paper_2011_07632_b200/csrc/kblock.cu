@@ -112,9 +112,143 @@ __global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
     }
 }
 
+// ---------------------------------------------------------------- narrow products (k <= 4)
+// Eval-bound path (PCG matvec): lane = target row (32-row tile), the 8 warps of a
+// CTA take the entries of one output group round-robin; a warp walks its entry's
+// source points 32 at a time, broadcasting each point's coordinates and values
+// by shuffles, so every kernel entry is evaluated exactly once; partial sums of
+// the warps are reduced in shared memory before one read-modify-write of Y.
+template <int KID>
+__device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
+    if (KID == SPD_K_GAUSSIAN) return exp(-r2 * kp.inv_l2);
+    if (KID == SPD_K_MATERN32) { const double t = sqrt(r2) * kp.sqrt3_inv_l; return (1.0 + t) * exp(-t); }
+    if (KID == SPD_K_EXPONENTIAL) return exp(-sqrt(r2) * kp.inv_l);
+    return rsqrt(r2 + kp.l2);
+}
+
+template <int KID, int NV>
+__global__ void __launch_bounds__(256) kblock_vec_kernel(
+    KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
+    const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
+    const int2* __restrict__ work) {
+    __shared__ double red[8][32][NV];
+    const int2 wk = work[blockIdx.x];
+    const KbTarget tg = targets[wk.x];
+    const KbBlock tb = blocks[tg.blk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = wk.y * 32;
+    const int row = r0 + lane;
+    const bool valid = row < tb.n;
+    double rx0 = 0.0, rx1 = 0.0, rx2 = 0.0;
+    if (valid) {
+        rx0 = tb.x[row];
+        if (d > 1) rx1 = tb.x[tb.ds + row];
+        if (d > 2) rx2 = tb.x[2 * tb.ds + row];
+    }
+    const int64_t rid = tb.id0 >= 0 ? tb.id0 + row : -1;
+    int g0 = tg.e_begin;
+    while (g0 < tg.e_end) {
+        int g1 = g0 + 1;
+        while (g1 < tg.e_end && entries[g1].Y == entries[g0].Y) ++g1;
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int e = g0 + warp; e < g1; e += 8) {
+            const KbEntry en = entries[e];
+            const KbBlock sb = blocks[en.src];
+            const int nc = min(en.ncols, NV);
+            const bool sh = shift != 0.0 && rid >= 0 && sb.id0 >= 0;
+            for (int c0 = 0; c0 < sb.n; c0 += 32) {
+                const int c = c0 + lane;
+                double sx0 = 0.0, sx1 = 0.0, sx2 = 0.0, xv[NV];
+                if (c < sb.n) {
+                    sx0 = sb.x[c];
+                    if (d > 1) sx1 = sb.x[sb.ds + c];
+                    if (d > 2) sx2 = sb.x[2 * sb.ds + c];
+                }
+#pragma unroll
+                for (int v = 0; v < NV; ++v) xv[v] = (c < sb.n && v < nc) ? en.X[c + (size_t)v * en.ldx] : 0.0;
+                const int cnt = min(32, sb.n - c0);
+                for (int q = 0; q < cnt; ++q) {
+                    const double y0 = __shfl_sync(0xffffffffu, sx0, q);
+                    const double y1 = __shfl_sync(0xffffffffu, sx1, q);
+                    const double y2 = __shfl_sync(0xffffffffu, sx2, q);
+                    const double df0 = rx0 - y0, df1 = rx1 - y1, df2 = rx2 - y2;
+                    const double r2 = df0 * df0 + df1 * df1 + df2 * df2;
+                    double kv = kval<KID>(kp, r2);
+                    if (sh && rid == sb.id0 + c0 + q) kv += shift;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) acc[v] += kv * __shfl_sync(0xffffffffu, xv[v], q);
+                }
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) red[warp][lane][v] = acc[v];
+        __syncthreads();
+        if (warp == 0 && valid) {
+            const KbEntry en = entries[g0];
+            const int nc = min(en.ncols, NV);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                if (v >= nc) break;
+                double sum = 0.0;
+                for (int w = 0; w < 8; ++w) sum += red[w][lane][v];
+                en.Y[row + (size_t)v * en.ldy] += sum;
+            }
+        }
+        __syncthreads();
+        g0 = g1;
+    }
+}
+
+template <int KID>
+static void launch_vec(cudaStream_t s, unsigned nb, int nv, const KernelParams& kp, double shift, int d,
+                       const KbBlock* b, const KbTarget* t, const KbEntry* e, const int2* w) {
+    if (nv == 1) kblock_vec_kernel<KID, 1><<<nb, 256, 0, s>>>(kp, shift, d, b, t, e, w);
+    else kblock_vec_kernel<KID, 4><<<nb, 256, 0, s>>>(kp, shift, d, b, t, e, w);
+}
+
+static void kblock_vec(cudaStream_t s, const KernelParams& kp, double shift, int d,
+                       const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
+                       const std::vector<KbEntry>& entries, int maxc) {
+    std::vector<int2> work;
+    double fl = 0, by = 0;
+    for (int t = 0; t < (int)targets.size(); ++t) {
+        const KbTarget& tg = targets[t];
+        if (tg.e_end <= tg.e_begin) continue;
+        for (int tm = 0; tm < ceil_div(blocks[tg.blk].n, 32); ++tm) work.push_back(make_int2(t, tm));
+        for (int e = tg.e_begin; e < tg.e_end; ++e) {
+            const double nr = blocks[tg.blk].n, ns = blocks[entries[e].src].n;
+            fl += 2.0 * nr * ns * entries[e].ncols;
+            by += 8.0 * (ns * (d + entries[e].ncols) + 2.0 * nr * entries[e].ncols);
+        }
+    }
+    if (work.empty()) return;
+    DevArray<KbBlock> db(s, blocks);
+    DevArray<KbTarget> dt(s, targets);
+    DevArray<KbEntry> de(s, entries);
+    DevArray<int2> dw(s, work);
+    ProfScope prof(s, "kblock_vec", fl, by);
+    const unsigned nb = (unsigned)work.size();
+    const int nv = maxc <= 1 ? 1 : 4;
+    switch (kp.id) {
+    case SPD_K_GAUSSIAN: launch_vec<SPD_K_GAUSSIAN>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
+    case SPD_K_MATERN32: launch_vec<SPD_K_MATERN32>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
+    case SPD_K_EXPONENTIAL: launch_vec<SPD_K_EXPONENTIAL>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
+    default: launch_vec<SPD_K_IMQ>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
+    }
+    SPD_LAUNCH();
+}
+
 void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
                   const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
                   const std::vector<KbEntry>& entries) {
+    {
+        int maxc = 0;
+        for (auto& e : entries) maxc = std::max(maxc, e.ncols);
+        if (maxc == 0) return;
+        if (maxc <= 4) { kblock_vec(s, kp, shift, d, blocks, targets, entries, maxc); return; }
+    }
     std::vector<KbWork> work;
     for (int t = 0; t < (int)targets.size(); ++t) {
         const KbTarget& tg = targets[t];

@@ -1,7 +1,10 @@
 // pcg.cu -- preconditioned conjugate gradient (reading R15)
 // with the H2 matvec as the operator and the SPD HSS solve as the preconditioner.
 // x0 = 0; stop when ||r_k||_2 <= tol ||b||_2 (recursively updated residual) or
-// at maxit.  Dot products use a fixed two-level reduction (deterministic).
+// at maxit.  All scalars live on the device; one iteration (H2 matvec, dots,
+// updates, HSS solve) is captured once as a CUDA graph and replayed, and the
+// host reads back only (p^T q, ||r||^2, r^T z) per iteration for the stop and
+// breakdown tests.  Dot products use a fixed two-level reduction (deterministic).
 #include "hss.hpp"
 #include <chrono>
 #include <cmath>
@@ -9,6 +12,8 @@
 namespace spd {
 
 constexpr int RED_BLOCKS = 296, RED_THREADS = 256;
+// device scalar slots
+enum { S_RZ = 0, S_PQ = 1, S_ALPHA = 2, S_RR = 3, S_RZNEW = 4, S_BETA = 5, S_NSCAL = 8 };
 
 __device__ double block_reduce(double v) {
     __shared__ double sh[RED_THREADS / 32];
@@ -20,7 +25,6 @@ __device__ double block_reduce(double v) {
     return v;
 }
 
-// partial[b] = sum a.b over block b's grid-stride slice
 __global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* a, const double* b, int64_t n, double* partial) {
     double s = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < n; i += (int64_t)RED_BLOCKS * RED_THREADS)
@@ -28,10 +32,20 @@ __global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* a, const
     s = block_reduce(s);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
-// x += alpha p ; r -= alpha q ; partial = r.r
+// out = sum(partial); mode 1: also alpha = rz / pq ; mode 2: also beta = rz_new / rz, rz = rz_new
+__global__ void finish_kernel(const double* partial, double* scal, int slot, int mode) {
+    double v = threadIdx.x < RED_BLOCKS ? partial[threadIdx.x] : 0.0;
+    if (threadIdx.x + 256 < RED_BLOCKS) v += partial[threadIdx.x + 256];
+    v = block_reduce(v);
+    if (threadIdx.x == 0) {
+        scal[slot] = v;
+        if (mode == 1) scal[S_ALPHA] = scal[S_RZ] / v;
+        if (mode == 2) { scal[S_BETA] = v / scal[S_RZ]; scal[S_RZ] = v; }
+    }
+}
 __global__ void __launch_bounds__(RED_THREADS) update_xr_kernel(double* x, double* r, const double* p, const double* q,
                                                                 const double* scal, int64_t n, double* partial) {
-    const double alpha = scal[0];
+    const double alpha = scal[S_ALPHA];
     double s = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < n; i += (int64_t)RED_BLOCKS * RED_THREADS) {
         x[i] += alpha * p[i];
@@ -42,78 +56,130 @@ __global__ void __launch_bounds__(RED_THREADS) update_xr_kernel(double* x, doubl
     s = block_reduce(s);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
-// p = z + beta p
 __global__ void update_p_kernel(double* p, const double* z, const double* scal, int64_t n) {
-    const double beta = scal[1];
+    const double beta = scal[S_BETA];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = z[i] + beta * p[i];
 }
-// final sums of partials -> out[0]
-__global__ void finish_kernel(const double* partial, double* out) {
-    double v = threadIdx.x < RED_BLOCKS ? partial[threadIdx.x] : 0.0;
-    if (threadIdx.x + 256 < RED_BLOCKS) v += partial[threadIdx.x + 256];
-    v = block_reduce(v);
-    if (threadIdx.x == 0) out[0] = v;
-}
 
-struct PcgState {
-    DBuf<double> partial{RED_BLOCKS}, scal{4}, res{2};
+struct PcgWork {
+    DBuf<double> r, z, p, q, partial, scal;
+    explicit PcgWork(int64_t N) : r(N), z(N), p(N), q(N), partial(RED_BLOCKS), scal(S_NSCAL) {}
 };
 
-static double dev_dot(cudaStream_t s, PcgState& st, const double* a, const double* b, int64_t n) {
-    dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(a, b, n, st.partial.p);
-    finish_kernel<<<1, RED_THREADS, 0, s>>>(st.partial.p, st.res.p);
-    SPD_LAUNCH();
-    double v;
-    SPD_CUDA(cudaMemcpyAsync(&v, st.res.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-    SPD_CUDA(cudaStreamSynchronize(s));
-    return v;
+static void dot_into(cudaStream_t s, PcgWork& w, const double* a, const double* b, int64_t n, int slot, int mode) {
+    {
+        ProfScope prof(s, "pcg_vec", 2.0 * n, 16.0 * n);
+        dot_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(a, b, n, w.partial.p);
+        SPD_LAUNCH();
+        finish_kernel<<<1, RED_THREADS, 0, s>>>(w.partial.p, w.scal.p, slot, mode);
+        SPD_LAUNCH();
+    }
 }
 
-// all vectors in tree order, length N
+// one PCG iteration after the first: q = A p, alpha, x/r update, z = M r, beta, p update
+static void iteration_body(spd_h2_s* A, spd_hss_s* M, double* x, PcgWork& w, int64_t N, cudaStream_t s) {
+    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);
+    dot_into(s, w, w.p.p, w.q.p, N, S_PQ, 1);
+    {
+        ProfScope prof(s, "pcg_vec", 4.0 * N, 40.0 * N);
+        update_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, w.r.p, w.p.p, w.q.p, w.scal.p, N, w.partial.p);
+        SPD_LAUNCH();
+        finish_kernel<<<1, RED_THREADS, 0, s>>>(w.partial.p, w.scal.p, S_RR, 0);
+        SPD_LAUNCH();
+    }
+    if (M) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);
+    else SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    dot_into(s, w, w.r.p, w.z.p, N, S_RZNEW, 2);
+    {
+        ProfScope prof(s, "pcg_vec", 2.0 * N, 24.0 * N);
+        update_p_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(w.p.p, w.z.p, w.scal.p, N);
+        SPD_LAUNCH();
+    }
+}
+
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,
-              cudaStream_t s) {
+              cudaStream_t user) {
     const int64_t N = A->N;
     const auto t0 = std::chrono::steady_clock::now();
-    DBuf<double> r(N), z(N), p(N), q(N);
-    PcgState st;
+    // private non-blocking stream (graph capture is illegal on the legacy stream)
+    cudaStream_t s;
+    SPD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t ev;
+    SPD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SPD_CUDA(cudaEventRecord(ev, user));
+    SPD_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    struct Cleanup {
+        cudaStream_t s, user; cudaEvent_t ev; cudaGraphExec_t ge = nullptr; cudaGraph_t g = nullptr;
+        ProfCaptured* pc = nullptr;
+        ~Cleanup() {
+            cudaEventRecord(ev, s);
+            cudaStreamWaitEvent(user, ev, 0);
+            if (ge) cudaGraphExecDestroy(ge);
+            if (g) cudaGraphDestroy(g);
+            cudaStreamSynchronize(s);
+            prof_release(pc);
+            cudaEventDestroy(ev);
+            cudaStreamDestroy(s);
+        }
+    } cl{s, user, ev};
+    PcgWork w(N);
+    double* hs = nullptr;                       // pinned host scalars
+    SPD_CUDA(cudaMallocHost(&hs, sizeof(double) * S_NSCAL));
+    struct FreeHost { double* p; ~FreeHost() { cudaFreeHost(p); } } fh{hs};
+
     SPD_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * N, s));
-    SPD_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-    const double nb = std::sqrt(dev_dot(s, st, b, b, N));
-    rep->iters = 0; rep->converged = 0; rep->relres = 1.0;
-    if (nb == 0.0) { rep->converged = 1; rep->relres = 0.0; return; }
-    auto precond = [&](const double* in, double* out) {
-        if (M) hss_solve_tree(M, in, N, out, N, 1, s);
-        else SPD_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-    };
-    precond(r.p, z.p);
-    SPD_CUDA(cudaMemcpyAsync(p.p, z.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-    double rz = dev_dot(s, st, r.p, z.p, N);
-    for (int it = 1; it <= maxit; ++it) {
-        h2_apply_tree(A, p.p, N, q.p, N, 1, s);
-        const double pq = dev_dot(s, st, p.p, q.p, N);
-        if (!(pq > 0.0)) throw Error(SPD_ENOTPD, "PCG breakdown: p^T A p = " + std::to_string(pq));
-        double scal[2] = {rz / pq, 0.0};
-        SPD_CUDA(cudaMemcpyAsync(st.scal.p, scal, sizeof(double), cudaMemcpyHostToDevice, s));
-        update_xr_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r.p, p.p, q.p, st.scal.p, N, st.partial.p);
-        finish_kernel<<<1, RED_THREADS, 0, s>>>(st.partial.p, st.res.p);
-        SPD_LAUNCH();
-        double rr;
-        SPD_CUDA(cudaMemcpyAsync(&rr, st.res.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-        SPD_CUDA(cudaStreamSynchronize(s));
-        rep->iters = it;
-        rep->relres = std::sqrt(rr) / nb;
-        if (rep->relres <= tol) { rep->converged = 1; break; }
-        precond(r.p, z.p);
-        const double rz_new = dev_dot(s, st, r.p, z.p, N);
-        if (!(rz_new > 0.0)) throw Error(SPD_ENOTPD, "PCG breakdown: r^T M^{-1} r = " + std::to_string(rz_new));
-        scal[1] = rz_new / rz;
-        SPD_CUDA(cudaMemcpyAsync(st.scal.p, scal, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
-        update_p_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p.p, z.p, st.scal.p, N);
-        SPD_LAUNCH();
-        rz = rz_new;
-    }
+    SPD_CUDA(cudaMemcpyAsync(w.r.p, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    dot_into(s, w, b, b, N, S_RR, 0);
+    SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
     SPD_CUDA(cudaStreamSynchronize(s));
+    const double nb = std::sqrt(hs[S_RR]);
+    rep->iters = 0; rep->converged = 0; rep->relres = 1.0; rep->seconds = 0.0;
+    if (nb == 0.0) { rep->converged = 1; rep->relres = 0.0; return; }
+    // z = M r, p = z, rz = r^T z
+    if (M) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);
+    else SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    SPD_CUDA(cudaMemcpyAsync(w.p.p, w.z.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    dot_into(s, w, w.r.p, w.z.p, N, S_RZ, 0);
+    SPD_CUDA(cudaStreamSynchronize(s));
+
+    // capture one iteration as a graph (descriptors in a persistent arena)
+    h2_prepare(A, 1, s);
+    bool use_graph = maxit > 1;
+    DescArena arena((size_t)64 << 20);
+    if (use_graph) {
+        try {
+            desc_arena() = &arena;
+            const size_t mark = prof_mark();
+            SPD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+            try { iteration_body(A, M, x, w, N, s); }
+            catch (...) { cudaGraph_t g; cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g); throw; }
+            SPD_CUDA(cudaStreamEndCapture(s, &cl.g));
+            SPD_CUDA(cudaGraphInstantiate(&cl.ge, cl.g, 0));
+            cl.pc = prof_capture_take(mark);
+            desc_arena() = nullptr;
+        } catch (const Error&) {
+            desc_arena() = nullptr;
+            cudaGetLastError();
+            use_graph = false;           // fall back to direct launches (same kernels)
+        }
+    }
+    for (int it = 1; it <= maxit; ++it) {
+        if (use_graph) {
+            SPD_CUDA(cudaGraphLaunch(cl.ge, s));
+            count_launch();
+        } else {
+            iteration_body(A, M, x, w, N, s);
+        }
+        SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
+        SPD_CUDA(cudaStreamSynchronize(s));
+        if (use_graph) prof_accumulate(cl.pc);
+        if (!(hs[S_PQ] > 0.0)) throw Error(SPD_ENOTPD, "PCG breakdown: p^T A p = " + std::to_string(hs[S_PQ]));
+        rep->iters = it;
+        rep->relres = std::sqrt(hs[S_RR]) / nb;
+        if (rep->relres <= tol) { rep->converged = 1; break; }
+        if (!(hs[S_RZNEW] > 0.0)) throw Error(SPD_ENOTPD, "PCG breakdown: r^T M^{-1} r = " + std::to_string(hs[S_RZNEW]));
+    }
     rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

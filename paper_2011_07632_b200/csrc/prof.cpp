@@ -13,6 +13,9 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 struct Rec { std::string name; double flops, bytes; cudaEvent_t a, b; };
+}  // namespace
+struct ProfCaptured { std::vector<Rec> recs; };
+namespace {
 std::mutex g_mu;
 bool g_on = false;
 std::vector<Rec> g_recs;
@@ -39,19 +42,63 @@ void drain() {       // caller holds the mutex
 }
 }  // namespace
 
+DescArena*& desc_arena() {
+    static thread_local DescArena* a = nullptr;
+    return a;
+}
+
+static bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    return st == cudaStreamCaptureStatusActive;
+}
+
 ProfScope::ProfScope(cudaStream_t st, const char* name, double flops, double bytes) : s(st) {
     if (!g_on) return;
     std::lock_guard<std::mutex> lk(g_mu);
     Rec r{name, flops, bytes, get_ev(), get_ev()};
-    cudaEventRecord(r.a, s);
+    ext = capturing(s);
+    if (ext) cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal);
+    else cudaEventRecord(r.a, s);
     g_recs.push_back(r);
     slot = (int)g_recs.size() - 1;
 }
 ProfScope::~ProfScope() {
     if (slot < 0) return;
     std::lock_guard<std::mutex> lk(g_mu);
-    cudaEventRecord(g_recs[slot].b, s);
-    if (g_recs.size() > 20000) drain();
+    if (ext) cudaEventRecordWithFlags(g_recs[slot].b, s, cudaEventRecordExternal);
+    else cudaEventRecord(g_recs[slot].b, s);
+    if (!ext && g_recs.size() > 20000) drain();
+}
+
+size_t prof_mark() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return g_recs.size();
+}
+ProfCaptured* prof_capture_take(size_t first) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto* c = new ProfCaptured();
+    if (first < g_recs.size()) {
+        c->recs.assign(g_recs.begin() + first, g_recs.end());
+        g_recs.resize(first);
+    }
+    return c;
+}
+void prof_accumulate(ProfCaptured* c) {
+    if (!c) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& r : c->recs) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) { cudaGetLastError(); continue; }
+        Agg& a = g_agg[r.name];
+        a.n += 1; a.ms += ms; a.flops += r.flops; a.bytes += r.bytes;
+    }
+}
+void prof_release(ProfCaptured* c) {
+    if (!c) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& r : c->recs) { g_pool.push_back(r.a); g_pool.push_back(r.b); }
+    delete c;
 }
 
 }  // namespace spd
