@@ -153,6 +153,11 @@ void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev,
 // uplo: 'L' lower / 'U' upper storage of T; trans: false -> T^{-1} X, true -> T^{-T} X
 void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans);
 void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol);
+// unpivoted blocked Householder QR (R factor only): on exit the upper triangle of
+// A[:n, :n] holds R (n <= m); the rest of A is overwritten.  Panel width 32,
+// compact-WY trailing updates on the DMMA GEMM.
+struct QrDesc { double* A; int m, n, ld; };
+void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d);
 // form Q[:, :r] (m x r, ld ldq) from the reflectors left in A by qrcp
 struct FormQDesc { const double* A; const double* beta; const int* rank; double* Q; int m, n, lda, ldq; };
 void formq_batched(cudaStream_t s, const std::vector<FormQDesc>& d);
@@ -161,6 +166,7 @@ struct CopyDesc { const double* A; double* C; int m, n, lda, ldc; int trans; };
 void copy_batched(cudaStream_t s, const std::vector<CopyDesc>& d, double alpha, bool accumulate);
 void set_identity_plus(cudaStream_t s, const std::vector<MatDesc>& d);   // A += I, zero upper? no: A += I
 void zero_upper_batched(cudaStream_t s, const std::vector<MatDesc>& d);
+void zero_lower_batched(cudaStream_t s, const std::vector<MatDesc>& d);   // strictly lower part
 
 // Descriptor arena: while a CUDA graph is being captured, descriptor arrays
 // go to a persistent device arena (filled with a synchronous copy, legal in

@@ -98,43 +98,70 @@ __global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ 
     if (!TA) {
         const int i = wk.y * 256 + threadIdx.x;
         if (i >= d.m) return;
-        double acc[NV];
+        double acc[4][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-        for (int kk = 0; kk < d.k; ++kk) {
-            const double a = d.A[i + (size_t)kk * d.lda];
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[u][v] = 0.0;
+        const double* a = d.A + i;
+        int kk = 0;
+        for (; kk + 4 <= d.k; kk += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double av = __ldg(a + (size_t)(kk + u) * d.lda);
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                    if (v < n) acc[u][v] += av * __ldg(d.B + kk + u + (size_t)v * d.ldb);
+            }
+        }
+        for (; kk < d.k; ++kk) {
+            const double av = __ldg(a + (size_t)kk * d.lda);
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                if (v < n) acc[v] += a * d.B[kk + (size_t)v * d.ldb];
+                if (v < n) acc[0][v] += av * __ldg(d.B + kk + (size_t)v * d.ldb);
         }
 #pragma unroll
         for (int v = 0; v < NV; ++v)
             if (v < n) {
+                const double sum = (acc[0][v] + acc[1][v]) + (acc[2][v] + acc[3][v]);
                 double* c = d.C + i + (size_t)v * d.ldc;
-                *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[v];
+                *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * sum;
             }
     } else {
         const int lane = threadIdx.x & 31;
         const int i = wk.y * 8 + (threadIdx.x >> 5);
         if (i >= d.m) return;
         const double* a = d.A + (size_t)i * d.lda;
-        double acc[NV];
+        double acc[4][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-        for (int kk = lane; kk < d.k; kk += 32) {
-            const double av = a[kk];
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[u][v] = 0.0;
+        int kk = lane;
+        for (; kk + 96 < d.k; kk += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double av = __ldg(a + kk + 32 * u);
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                    if (v < n) acc[u][v] += av * __ldg(d.B + kk + 32 * u + (size_t)v * d.ldb);
+            }
+        }
+        for (; kk < d.k; kk += 32) {
+            const double av = __ldg(a + kk);
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                if (v < n) acc[v] += av * d.B[kk + (size_t)v * d.ldb];
+                if (v < n) acc[0][v] += av * __ldg(d.B + kk + (size_t)v * d.ldb);
         }
+        double sum[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = warp_sum(acc[v]);
+        for (int v = 0; v < NV; ++v) sum[v] = warp_sum((acc[0][v] + acc[1][v]) + (acc[2][v] + acc[3][v]));
         if (lane == 0)
 #pragma unroll
             for (int v = 0; v < NV; ++v)
                 if (v < n) {
                     double* c = d.C + i + (size_t)v * d.ldc;
-                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[v];
+                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * sum[v];
                 }
     }
 }
@@ -339,7 +366,63 @@ __global__ void __launch_bounds__(256) trsv_kernel(const TrsmDesc* descs) {
     for (int e = threadIdx.x; e < n * nr; e += blockDim.x) d.X[e % n + (size_t)(e / n) * d.ldx] = xs[e];
 }
 
+template <bool TRANS>
+__global__ void __launch_bounds__(256) trsv_warp_kernel(const TrsmDesc* __restrict__ descs, int ndesc, int nmax) {
+    extern __shared__ double xsh[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int item = blockIdx.x * 8 + warp;          // (desc, rhs column)
+    // items are laid out desc-major with 4 slots per desc (nrhs <= 4)
+    const int di = item >> 2, c = item & 3;
+    if (di >= ndesc) return;
+    const TrsmDesc d = descs[di];
+    if (c >= d.nrhs) return;
+    const int n = d.n;
+    double* xs = xsh + (size_t)warp * nmax;
+    double* xg = d.X + (size_t)c * d.ldx;
+    for (int i = lane; i < n; i += 32) xs[i] = xg[i];
+    __syncwarp();
+    if (!TRANS) {                                    // L x = b : x_j /= L_jj ; x_r -= L_rj x_j (r > j)
+        for (int j = 0; j < n; ++j) {
+            const double* col = d.T + (size_t)j * d.ldt;
+            const double xj = xs[j] / col[j];
+            __syncwarp();
+            if (lane == 0) xs[j] = xj;
+            for (int r = j + 1 + lane; r < n; r += 32) xs[r] -= col[r] * xj;
+            __syncwarp();
+        }
+    } else {                                         // L^T x = b : x_j = (b_j - sum_{r>j} L_rj x_r) / L_jj
+        for (int j = n - 1; j >= 0; --j) {
+            const double* col = d.T + (size_t)j * d.ldt;
+            double sacc = 0.0;
+            for (int r = j + 1 + lane; r < n; r += 32) sacc += col[r] * xs[r];
+            sacc = warp_sum(sacc);
+            if (lane == 0) xs[j] = (xs[j] - sacc) / col[j];
+            __syncwarp();
+        }
+    }
+    for (int i = lane; i < n; i += 32) xg[i] = xs[i];
+}
+
 void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans) {
+    {
+        int nrmax = 0, nmax = 0;
+        for (auto& t : d) { nrmax = std::max(nrmax, t.nrhs); nmax = std::max(nmax, t.n); }
+        const bool lower = (uplo == 'L' || uplo == 'l');
+        if (lower && nrmax <= 4 && nmax > 0 && nmax <= 768) {
+            std::vector<TrsmDesc> dv;
+            double fl = 0, by = 0;
+            for (auto& t : d) if (t.n > 0 && t.nrhs > 0) { dv.push_back(t); fl += (double)t.n * t.n * t.nrhs; by += 4.0 * t.n * t.n; }
+            if (dv.empty()) return;
+            DevArray<TrsmDesc> dd(s, dv);
+            ProfScope prof(s, "trsv", fl, by);
+            const unsigned nb = (unsigned)ceil_div((int64_t)dv.size() * 4, 8);
+            const size_t sh = (size_t)8 * nmax * sizeof(double);
+            if (!trans) trsv_warp_kernel<false><<<nb, 256, sh, s>>>(dd.p, (int)dv.size(), nmax);
+            else trsv_warp_kernel<true><<<nb, 256, sh, s>>>(dd.p, (int)dv.size(), nmax);
+            SPD_LAUNCH();
+            return;
+        }
+    }
     {
         int nrmax = 0, nmax = 0;
         for (auto& t : d) { nrmax = std::max(nrmax, t.nrhs); nmax = std::max(nmax, t.n); }
@@ -646,6 +729,134 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
     SPD_CUDA(cudaFreeAsync(bars, s));
 }
 
+// ================================================================= unpivoted blocked QR
+constexpr int QB = 32;
+struct PanelDesc {
+    double* A; int m, n, ld;     // full matrix
+    int p, jb;                   // panel columns [p, p + jb)
+    double* V; int ldv;          // (m - p) x jb explicit unit-lower reflectors
+    double* T;                   // jb x jb (ld QB) compact-WY factor, H_0..H_{jb-1} = I - V T V^T
+};
+
+// one CTA per panel: Householder column by column (warp per column for the
+// updates, so only two block barriers per column), then T from V^T V.
+__global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
+    const PanelDesc d = descs[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = 8;
+    const int L = d.m - d.p;                 // panel rows
+    double* P = d.A + d.p + (size_t)d.p * d.ld;   // panel origin
+    __shared__ double s_beta[QB], s_v0, s_mu, s_sig, s_x0;
+    __shared__ double G[QB][QB + 1];         // V^T V
+    for (int j = 0; j < d.jb; ++j) {
+        double* col = P + (size_t)j * d.ld;
+        if (warp == 0) {
+            double sg = 0.0;
+            for (int i = j + 1 + lane; i < L; i += 32) { double x = col[i]; sg += x * x; }
+            sg = warp_sum(sg);
+            if (lane == 0) {
+                const double x0 = col[j];
+                double beta, mu, v0;
+                if (sg == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
+                else {
+                    mu = sqrt(x0 * x0 + sg);
+                    v0 = (x0 <= 0.0) ? x0 - mu : -sg / (x0 + mu);
+                    beta = 2.0 * v0 * v0 / (sg + v0 * v0);
+                }
+                s_beta[j] = beta; s_v0 = v0; s_mu = mu; s_sig = sg; s_x0 = x0;
+            }
+        }
+        __syncthreads();
+        const double inv0 = (s_sig == 0.0) ? 0.0 : 1.0 / s_v0;
+        double* v = d.V + (size_t)j * d.ldv;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+            double vi = (i < j) ? 0.0 : (i == j ? 1.0 : col[i] * inv0);
+            v[i] = vi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) col[j] = s_mu;
+        const double beta = s_beta[j];
+        for (int c = j + 1 + warp; c < d.jb; c += nw) {
+            double* cc = P + (size_t)c * d.ld;
+            double w = 0.0;
+            for (int i = j + lane; i < L; i += 32) w += v[i] * cc[i];
+            w = warp_sum(w) * beta;
+            for (int i = j + lane; i < L; i += 32) cc[i] -= w * v[i];
+        }
+        __syncthreads();
+    }
+    // G = V^T V (upper part), T recurrence: T_jj = beta_j, T[:j, j] = -beta_j T[:j,:j] (V^T v_j)[:j]
+    for (int pr = warp; pr < d.jb * d.jb; pr += nw) {
+        const int a = pr % d.jb, b = pr / d.jb;
+        if (a >= b) continue;
+        const double* va = d.V + (size_t)a * d.ldv;
+        const double* vb = d.V + (size_t)b * d.ldv;
+        double s = 0.0;
+        for (int i = b + lane; i < L; i += 32) s += va[i] * vb[i];
+        s = warp_sum(s);
+        if (lane == 0) G[a][b] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double* T = d.T;
+        for (int j = 0; j < d.jb; ++j) {
+            const double beta = s_beta[j];
+            for (int a = 0; a < j; ++a) {
+                double s = 0.0;
+                for (int b = a; b < j; ++b) s += T[a + b * QB] * G[b][j];
+                T[a + j * QB] = -beta * s;
+            }
+            T[j + j * QB] = beta;
+            for (int a = j + 1; a < QB; ++a) T[a + j * QB] = 0.0;
+        }
+    }
+}
+
+void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
+    if (d.empty()) return;
+    int nmax = 0;
+    size_t vtot = 0, wtot = 0;
+    std::vector<size_t> voff(d.size()), woff(d.size());
+    for (size_t i = 0; i < d.size(); ++i) {
+        nmax = std::max(nmax, d[i].n);
+        voff[i] = vtot; vtot += (size_t)d[i].m * QB;
+        woff[i] = wtot; wtot += (size_t)QB * d[i].n;
+    }
+    DBuf<double> V(vtot), T(d.size() * QB * QB), W(wtot), W2(wtot);
+    double fl = 0;
+    for (auto& q : d) fl += 2.0 * q.m * q.n * q.n - 2.0 / 3.0 * q.n * q.n * q.n;
+    for (int p = 0; p < nmax; p += QB) {
+        std::vector<PanelDesc> pd;
+        std::vector<GemmDesc> g1, g2, g3;
+        for (size_t i = 0; i < d.size(); ++i) {
+            const QrDesc& q = d[i];
+            if (p >= q.n || p >= q.m) continue;
+            const int jb = std::min(QB, std::min(q.n, q.m) - p);
+            PanelDesc pdsc{q.A, q.m, q.n, q.ld, p, jb, V.p + voff[i], q.m, T.p + i * QB * QB};
+            pd.push_back(pdsc);
+            const int nt = q.n - p - jb, L = q.m - p;
+            if (nt > 0) {
+                double* At = q.A + p + (size_t)(p + jb) * q.ld;
+                // W = V^T A_trail ; W2 = T^T W ; A_trail -= V W2
+                g1.push_back({V.p + voff[i], At, W.p + woff[i], jb, nt, L, q.m, q.ld, QB});
+                g2.push_back({T.p + i * QB * QB, W.p + woff[i], W2.p + woff[i], jb, nt, jb, QB, QB, QB});
+                g3.push_back({V.p + voff[i], W2.p + woff[i], At, L, nt, jb, q.m, QB, q.ld});
+            }
+        }
+        {
+            DevArray<PanelDesc> dp(s, pd);
+            double pb = 0;
+            for (auto& q : pd) pb += 8.0 * (q.m - q.p) * q.jb * (q.jb + 2);
+            ProfScope prof(s, "qr_panel", 0, pb);
+            panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);
+            SPD_LAUNCH();
+        }
+        gemm_batched(s, g1, true, false, 1.0, 0.0);
+        gemm_batched(s, g2, true, false, 1.0, 0.0);
+        gemm_batched(s, g3, false, false, -1.0, 1.0);
+    }
+    SPD_CUDA(cudaStreamSynchronize(s));
+}
+
 // ================================================================= FORM Q
 __global__ void __launch_bounds__(256) formq_kernel(const FormQDesc* descs) {
     const FormQDesc d = descs[blockIdx.x];
@@ -709,6 +920,18 @@ void set_identity_plus(cudaStream_t s, const std::vector<MatDesc>& d) {
     if (d.empty()) return;
     DevArray<MatDesc> dd(s, d);
     add_identity_kernel<<<(unsigned)d.size(), 128, 0, s>>>(dd.p);
+    SPD_LAUNCH();
+}
+
+__global__ void zero_lower_kernel(const MatDesc* descs) {
+    const MatDesc d = descs[blockIdx.x];
+    for (int j = 0; j < d.n; ++j)
+        for (int i = j + 1 + threadIdx.x; i < d.m; i += blockDim.x) d.A[i + (size_t)j * d.ld] = 0.0;
+}
+void zero_lower_batched(cudaStream_t s, const std::vector<MatDesc>& d) {
+    if (d.empty()) return;
+    DevArray<MatDesc> dd(s, d);
+    zero_lower_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p);
     SPD_LAUNCH();
 }
 

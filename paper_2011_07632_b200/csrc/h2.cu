@@ -302,6 +302,22 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 proxy_matrix_kernel<<<dim3(64, (unsigned)mdesc.size()), 256, 0, s>>>(dm.p, h->kp, d, n_p);
                 SPD_LAUNCH();
             }
+            // two-stage ID: M^T = Q0 R0 (blocked, DMMA) then QRCP of R0; column norms and
+            // hence pivots and R are invariant under the left-orthogonal Q0 (reading R4)
+            {
+                std::vector<QrDesc> tall;
+                std::vector<MatDesc> tri;
+                for (size_t q = 0; q < ch.nodes.size(); ++q) {
+                    const int nc = lv.ncand[ch.nodes[q]];
+                    if (n_p >= 2 * nc && nc >= 32) {
+                        tall.push_back({qdesc[q].A, n_p, nc, n_p});
+                        tri.push_back({qdesc[q].A, nc, nc, n_p});
+                        qdesc[q].m = nc;               // QRCP on the n_c x n_c triangle
+                    }
+                }
+                qr_unpivoted_batched(s, tall);
+                zero_lower_batched(s, tri);
+            }
             qrcp_batched(s, qdesc, h->tol);
             std::vector<int> rk(lv.count + 1);
             SPD_CUDA(cudaMemcpyAsync(rk.data(), rank_d.p, sizeof(int) * (lv.count + 1), cudaMemcpyDeviceToHost, s));
