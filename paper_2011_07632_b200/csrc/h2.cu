@@ -13,6 +13,7 @@
 #include "h2.hpp"
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 
 namespace spd {
 
@@ -414,7 +415,29 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
     h->ws_k = k;
 }
 
-void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) { if (h->tree.L > 1) ensure_ws(h, k, s); }
+void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
+    if (h->tree.L > 1) ensure_ws(h, k, s);
+    if (k != 1 || h->stored_mode != -1) return;
+    // stored k=1 blocks if they need < 40% of the free device memory (env SPD_STORED=0/1 overrides)
+    const char* env = getenv("SPD_STORED");
+    if (env && env[0] == '0') { h->stored_mode = 0; return; }
+    const TreeH& t = h->tree;
+    double need = 0;
+    {
+        const int l1 = t.first(1);
+        std::vector<int64_t> rows(t.count(1));
+        for (int a = 0; a < t.count(1); ++a) rows[a] = 32LL * ceil_div(t.size(l1 + a), 32);
+        for (auto& pr : h->lists.near) need += 8.0 * rows[pr.first - l1] * t.size(pr.second);
+        for (int lk = 1; lk < t.L; ++lk) {
+            const H2Level& lv = h->lv[lk];
+            for (auto& pr : h->lists.type3[lk])
+                need += 8.0 * 32.0 * ceil_div(lv.rank[pr.first - lv.first], 32) * lv.rank[pr.second - lv.first];
+        }
+    }
+    size_t fr = 0, tot = 0;
+    SPD_CUDA(cudaMemGetInfo(&fr, &tot));
+    h->stored_mode = (env && env[0] == '1') || need < 0.4 * (double)fr ? 1 : 0;
+}
 
 // Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]
 static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
@@ -498,11 +521,13 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     const int L = t.L;
     const int64_t N = h->N;
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
+    const bool use_store = (k == 1 && h->stored_mode == 1);
+    if (use_store && h->stores.size() < (size_t)L) h->stores.resize(L);
     // near field
     {
         std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
         near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
-        kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
+        kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries, use_store ? &h->stores[0] : nullptr);
     }
     if (L == 1) return;
     ensure_ws(h, k, s);
@@ -534,7 +559,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             tg.e_end = (int)entries.size();
             targets.push_back(tg);
         }
-        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries);
+        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries, use_store ? &h->stores[lk] : nullptr);
     }
     h2_down(h, yh, L - 1, y, ldy, k, s);
 }

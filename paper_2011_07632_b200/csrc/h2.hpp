@@ -43,6 +43,9 @@ struct spd_h2_s {
     spd::DBuf<double> xt, yt;
     std::vector<spd::DBuf<double>> xh, yh;
     spd_comm_t comm = nullptr;
+    // stored blocks for k = 1 applies: [0] near field, [l] Type-3 couplings of level l
+    int stored_mode = -1;          // -1 undecided, 0 on the fly, 1 stored
+    std::vector<spd::KbStore> stores;
 };
 
 namespace spd {

@@ -145,6 +145,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
 
     // capture one iteration as a graph (descriptors in a persistent arena)
     h2_prepare(A, 1, s);
+    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);     // builds stored k=1 blocks outside the graph
     bool use_graph = maxit > 1;
     DescArena arena((size_t)64 << 20);
     if (use_graph) {

@@ -170,3 +170,26 @@ def test_full_c2_build_properties(spd):
     v = synth.multivec(cfg.n, 4, seed=5)
     sv = host(spd.hss_solve(H, cuda(v)))
     assert np.all(np.einsum("ij,ij->j", v, sv) > 0)
+
+
+@pytest.mark.parametrize("stored", ["0", "1"])
+def test_pcg_stored_and_on_the_fly_k1_paths(spd, stored, monkeypatch):
+    """Both k=1 matvec paths (on-the-fly eval-bound kernel; stored blocks, §8(f) f4)
+    give the oracle's PCG iterations and, afterwards, oracle-exact k=1 products."""
+    import torch
+    monkeypatch.setenv("SPD_STORED", stored)
+    cfg = CASES["C2s"]
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    cfg_, X_, h_, ho, H_, Ho, om = built(spd, "C2s")
+    H = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, omega=cuda(om))
+    b = synth.rhs(cfg)
+    x, rep = spd.pcg_solve(h, H, cuda(b), tol=cfg.pcg_tol, maxit=cfg.maxit)
+    _, it_o, _, _ = oracle.pcg(lambda v: oracle.h2_matvec(ho, v), lambda v: oracle.hss_solve(Ho, v),
+                               b[ho.tree.perm], cfg.pcg_tol, cfg.maxit)
+    assert rep.converged and abs(rep.iters - it_o) <= 1
+    v = synth.multivec(cfg.n, 1, seed=21)[:, 0]
+    y = host(spd.h2_matvec(h, cuda(v)))
+    yo = np.empty_like(v)
+    yo[ho.tree.perm] = oracle.h2_matvec(ho, v[ho.tree.perm])
+    assert rel(y, yo) <= 1e-9
