@@ -19,6 +19,9 @@ spd_status spd_test_trsm(char uplo, int trans, const double* T, int n, int ldt, 
  * (ld m) when Q != NULL; piv (n per matrix) and rank (1 per matrix) on the device */
 spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t stride, int max_rank,
                          double rel_tol, int* piv, int* rank, double* Q, int64_t qstride, void* stream);
+/* unpivoted blocked Householder QR (R only) of `batch` matrices A_b = A + b*stride (m x n, ld);
+ * on exit the upper triangle of each A_b[:n, :n] holds R with diag(R) >= 0 */
+spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int64_t stride, void* stream);
 /* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major */
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
 #ifdef __cplusplus

@@ -76,6 +76,7 @@ def lib():
         "spd_test_trsm": ([ctypes.c_char, c_int, vp, c_int, c_int, vp, c_int, c_int, vp], c_int),
         "spd_test_qrcp": ([c_int, vp, c_int, c_int, c_int, i64, c_int, c_double, vp, vp, vp, i64, vp], c_int),
         "spd_test_proxies": ([vp, c_int, vp, vp], c_int),
+        "spd_test_qr_unpivoted": ([c_int, vp, c_int, c_int, c_int, i64, vp], c_int),
         "spd_launch_count": ([], ctypes.c_longlong),
         "spd_prof_enable": ([c_int], None),
         "spd_prof_reset": ([], None),

@@ -295,6 +295,14 @@ spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t str
     })
 }
 
+spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int64_t stride, void* stream) {
+    SPD_TRY({
+        std::vector<QrDesc> d;
+        for (int b = 0; b < batch; ++b) d.push_back({A + b * stride, m, n, ld});
+        qr_unpivoted_batched((cudaStream_t)stream, d);
+    })
+}
+
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) {
     SPD_TRY({
         SPD_REQUIRE(h != nullptr && P_host != nullptr, "spd_test_proxies: null argument");

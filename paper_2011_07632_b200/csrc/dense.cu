@@ -811,6 +811,137 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
     }
 }
 
+// Cluster panel QR: a cluster of CL CTAs per panel; CTA g keeps rows
+// [g*rp, (g+1)*rp) of the panel in shared memory; per column two cluster
+// barriers exchange partial sums through DSMEM (summed in rank order, so
+// every CTA derives bit-identical reflectors).
+namespace cg = cooperative_groups;
+constexpr int QCL = 8;
+
+__global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int g = (int)cluster.block_rank();
+    const PanelDesc d = descs[blockIdx.x / QCL];
+    extern __shared__ double sm[];                    // rp x QB panel slice (col-major, ld rp)
+    __shared__ double part[2][QB + 2];                // [0]: sigma, x0 ; [1]: dots
+    __shared__ double Gp[QB][QB + 1];                 // partial V^T V
+    __shared__ double red[8];
+    __shared__ double s_beta[QB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int L = d.m - d.p, jb = d.jb;
+    const int r0 = g * rp, nr = max(0, min(rp, L - r0));
+    double* P = d.A + d.p + (size_t)d.p * d.ld;
+    for (int e = threadIdx.x; e < rp * jb; e += blockDim.x) {
+        const int i = e % rp, c = e / rp;
+        sm[i + c * rp] = (i < nr) ? P[r0 + i + (size_t)c * d.ld] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < jb; ++j) {
+        double* col = sm + j * rp;
+        // (1) partial sigma over rows > j, and x0 from the owner of row j
+        double sg = 0.0;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x)
+            if (r0 + i > j) sg += col[i] * col[i];
+        sg = warp_sum(sg);
+        if (lane == 0) red[warp] = sg;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < 8; ++w) t += red[w];
+            part[0][0] = t;
+            part[0][1] = (j >= r0 && j < r0 + nr) ? col[j - r0] : 0.0;
+        }
+        cluster.sync();
+        double sig = 0.0, x0 = 0.0;
+        for (int q = 0; q < QCL; ++q) {
+            const double* rp_ = cluster.map_shared_rank(&part[0][0], q);
+            sig += rp_[0];
+            x0 += rp_[1];
+        }
+        double beta, mu, v0;
+        if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
+        else {
+            mu = sqrt(x0 * x0 + sig);
+            v0 = (x0 <= 0.0) ? x0 - mu : -sig / (x0 + mu);
+            beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+        }
+        const double inv0 = (sig == 0.0) ? 0.0 : 1.0 / v0;
+        // (2) v on my rows -> global V ; R diagonal stays in the owner's slice
+        double* vg = d.V + (size_t)j * d.ldv;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+            const int gi = r0 + i;
+            const double vi = gi < j ? 0.0 : (gi == j ? 1.0 : col[i] * inv0);
+            vg[gi] = vi;
+            if (gi > j) col[i] = vi;                    // keep v in the slice (below the diagonal)
+            else if (gi == j) col[i] = mu;
+        }
+        if (threadIdx.x == 0) s_beta[j] = beta;        // identical in every CTA of the cluster
+        __syncthreads();
+        // (3) partial dots w_c = sum_{rows >= j} v_i A_ic for c > j
+        for (int c = j + 1 + warp; c < jb; c += 8) {
+            const double* cc = sm + c * rp;
+            double w = 0.0;
+            for (int i = lane; i < nr; i += 32) {
+                const int gi = r0 + i;
+                if (gi >= j) w += (gi == j ? 1.0 : col[i]) * cc[i];
+            }
+            w = warp_sum(w);
+            if (lane == 0) part[1][c] = w;
+        }
+        cluster.sync();
+        for (int c = j + 1 + warp; c < jb; c += 8) {
+            double w = 0.0;
+            for (int q = 0; q < QCL; ++q) w += cluster.map_shared_rank(&part[1][0], q)[c];
+            w *= beta;
+            double* cc = sm + c * rp;
+            for (int i = lane; i < nr; i += 32) {
+                const int gi = r0 + i;
+                if (gi >= j) cc[i] -= w * (gi == j ? 1.0 : col[i]);
+            }
+        }
+        __syncthreads();
+    }
+    // write the R part (rows <= column) back; the rest of the slice is scratch
+    for (int e = threadIdx.x; e < rp * jb; e += blockDim.x) {
+        const int i = e % rp, c = e / rp;
+        if (i < nr && r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
+    }
+    // T = compact-WY factor from V^T V (cluster-reduced) and the betas
+    for (int pr = warp; pr < jb * jb; pr += 8) {
+        const int a = pr % jb, b = pr / jb;
+        if (a >= b) continue;
+        const double* va = d.V + (size_t)a * d.ldv;
+        const double* vb = d.V + (size_t)b * d.ldv;
+        double s = 0.0;
+        for (int i = lane; i < nr; i += 32) { const int gi = r0 + i; s += va[gi] * vb[gi]; }
+        s = warp_sum(s);
+        if (lane == 0) Gp[a][b] = s;
+    }
+    cluster.sync();
+    if (g == 0 && threadIdx.x == 0) {
+        __threadfence();
+        double* T = d.T;
+        const double* bet = s_beta;
+        double G[QB][QB];
+        for (int b = 0; b < jb; ++b)
+            for (int a = 0; a < b; ++a) {
+                double s = 0.0;
+                for (int q = 0; q < QCL; ++q) s += cluster.map_shared_rank(&Gp[0][0], q)[a * (QB + 1) + b];
+                G[a][b] = s;
+            }
+        for (int j = 0; j < jb; ++j) {
+            for (int a = 0; a < j; ++a) {
+                double s = 0.0;
+                for (int b = a; b < j; ++b) s += T[a + b * QB] * G[b][j];
+                T[a + j * QB] = -bet[j] * s;
+            }
+            T[j + j * QB] = bet[j];
+            for (int a = j + 1; a < QB; ++a) T[a + j * QB] = 0.0;
+        }
+    }
+    cluster.sync();                                   // keep smem alive for remote readers
+}
+
 void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
     if (d.empty()) return;
     int nmax = 0;
@@ -845,10 +976,33 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
         {
             DevArray<PanelDesc> dp(s, pd);
             double pb = 0;
-            for (auto& q : pd) pb += 8.0 * (q.m - q.p) * q.jb * (q.jb + 2);
+            int Lmax = 0;
+            for (auto& q : pd) { pb += 8.0 * (q.m - q.p) * q.jb * (q.jb + 2); Lmax = std::max(Lmax, q.m - q.p); }
+            const int rp = ceil_div(Lmax, QCL);
+            const size_t sh = (size_t)rp * QB * sizeof(double);
             ProfScope prof(s, "qr_panel", 0, pb);
-            panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);
-            SPD_LAUNCH();
+            if (sh <= 180 * 1024) {
+                static bool attr = false;
+                if (!attr) {
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+                    attr = true;
+                }
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)pd.size() * QCL);
+                cfg.blockDim = dim3(256);
+                cfg.dynamicSmemBytes = sh;
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = QCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel, (const PanelDesc*)dp.p, rp));
+                count_launch();
+            } else {
+                panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);
+                SPD_LAUNCH();
+            }
         }
         gemm_batched(s, g1, true, false, 1.0, 0.0);
         gemm_batched(s, g2, true, false, 1.0, 0.0);

@@ -15,6 +15,8 @@ struct HssLevel {
     // factors: leaf S_i (n x n) / nonleaf F_i (m x m), lower, col-major, ld = m
     std::vector<int64_t> F_off;
     DBuf<double> F;
+    // explicit inverse factors S_i^{-1} / F_i^{-1} (lower, same layout as F) for the solve
+    DBuf<double> Finv;
     // basis: leaf V_i (n x r) / nonleaf Vbar'_i (m x r), ld = m
     std::vector<int64_t> V_off;
     DBuf<double> V;
@@ -44,7 +46,7 @@ struct spd_hss_s {
     // solve workspace
     int64_t ws_k = 0;
     spd::DBuf<double> bt, xt;
-    std::vector<spd::DBuf<double>> z, zh, res;
+    std::vector<spd::DBuf<double>> z, ub;
 };
 
 namespace spd {

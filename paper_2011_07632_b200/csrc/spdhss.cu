@@ -289,6 +289,38 @@ static void sketch_qr(spd_hss_s* H, cudaStream_t s, HssLevel& lv, const std::vec
     trsm_batched(s, td, 'L', true);
 }
 
+// ================================================================= solve factors
+__global__ void set_identity_kernel(const MatDesc* descs) {
+    const MatDesc d = descs[blockIdx.y];
+    const int64_t total = (int64_t)d.m * d.n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int i = (int)(e % d.m), j = (int)(e / d.m);
+        d.A[i + (size_t)j * d.ld] = (i == j) ? 1.0 : 0.0;
+    }
+}
+static void invert_factors(cudaStream_t s, HssLevel& lv) {
+    const int n = lv.count;
+    if (n == 0 || lv.F_off.empty()) return;
+    lv.Finv.alloc(std::max<int64_t>(1, lv.F_off[n]));
+    std::vector<MatDesc> md;
+    std::vector<TrsmDesc> td;
+    for (int a = 0; a < n; ++a) {
+        const int m = lv.m[a];
+        if (!m) continue;
+        md.push_back({lv.Finv.p + lv.F_off[a], m, m, m});
+        td.push_back({lv.F.p + lv.F_off[a], lv.Finv.p + lv.F_off[a], m, m, m, m});
+    }
+    if (md.empty()) return;
+    {
+        DevArray<MatDesc> dm(s, md);
+        for (size_t off = 0; off < md.size(); off += 65535) {
+            set_identity_kernel<<<dim3(8, (unsigned)std::min<size_t>(65535, md.size() - off)), 256, 0, s>>>(dm.p + off);
+            SPD_LAUNCH();
+        }
+    }
+    trsm_batched(s, td, 'L', false);                  // F^{-1} = F \ I (lower triangular)
+}
+
 // ================================================================= the build
 void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStream_t s) {
     spd_h2_s* h = H->h2;
@@ -307,6 +339,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         DBuf<int> info(1); DBuf<double> bad(1); info.zero(s);
         potrf_batched(s, {{r.F.p, (int)N, (int)N, (int)N}}, info.p, bad.p);
         check_info(s, info, bad, 1, 0, "leaf block A_ii");
+        invert_factors(s, r);
         return;
     }
     // ---------------- Omega (parity hook or Philox)
@@ -583,6 +616,9 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         Tprev[k].release();
         SPD_CUDA(cudaStreamSynchronize(s));
     }
+    // solve factors: explicit S_i^{-1}, F_i^{-1} (triangular inverses by blocked TRSM on I),
+    // so every step of hss_solve is an HBM-bound GEMV
+    for (int k = 1; k <= L; ++k) invert_factors(s, H->lv[k]);
     SPD_CUDA(cudaStreamSynchronize(s));
     H->timings[2] = now_s() - t2;
     H->timings[3] = now_s() - t0;
@@ -597,6 +633,9 @@ static void ensure_solve_ws(spd_hss_s* H, int k) {
     H->z.clear();
     H->z.resize(L + 1);
     for (int l = 1; l < L; ++l) H->z[l].alloc(std::max<int64_t>(1, H->lv[l].R * k));
+    H->ub.clear();
+    H->ub.resize(L + 1);
+    for (int l = 2; l <= L; ++l) H->ub[l].alloc(std::max<int64_t>(1, H->lv[l - 1].R * k));
     H->ws_k = k;
 }
 
@@ -605,96 +644,91 @@ void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64
     const TreeH& t = h->tree;
     const int L = t.L;
     const int64_t N = h->N;
-    SPD_CUDA(cudaMemcpy2DAsync(x, sizeof(double) * ldx, b, sizeof(double) * ldb, sizeof(double) * N, k,
-                               cudaMemcpyDeviceToDevice, s));
     if (L == 1) {
         const HssLevel& r = H->lv[1];
-        trsm_batched(s, {{r.F.p, x, (int)N, k, (int)N, (int)ldx}}, 'L', false);
-        trsm_batched(s, {{r.F.p, x, (int)N, k, (int)N, (int)ldx}}, 'L', true);
+        ensure_solve_ws(H, k);
+        gemm_batched(s, {{r.Finv.p, b, H->bt.p, (int)N, k, (int)N, (int)N, (int)ldb, (int)N}}, false, false, 1.0, 0.0);
+        gemm_batched(s, {{r.Finv.p, H->bt.p, x, (int)N, k, (int)N, (int)N, (int)N, (int)ldx}}, true, false, 1.0, 0.0);
         return;
     }
     ensure_solve_ws(H, k);
+    double* z = H->bt.p;                               // N x k workspace (ld N)
     const HssLevel& l1 = H->lv[1];
     // up, leaf: z = S^{-1} b ; zh = V^T z ; z <- z - V zh
     {
-        std::vector<TrsmDesc> td;
-        std::vector<GemmDesc> g1, g2;
+        std::vector<GemmDesc> g0, g1, g2;
         for (int a = 0; a < l1.count; ++a) {
-            double* xa = x + t.begin[l1.first + a];
-            td.push_back({l1.F.p + l1.F_off[a], xa, l1.m[a], k, l1.m[a], (int)ldx});
+            const int64_t off = t.begin[l1.first + a];
+            const int n = l1.m[a];
+            g0.push_back({l1.Finv.p + l1.F_off[a], b + off, z + off, n, k, n, n, (int)ldb, (int)N});
             if (l1.rank[a]) {
-                g1.push_back({l1.V.p + l1.V_off[a], xa, H->z[1].p + l1.off[a], l1.rank[a], k, l1.m[a], l1.m[a], (int)ldx,
-                              (int)l1.R});
-                g2.push_back({l1.V.p + l1.V_off[a], H->z[1].p + l1.off[a], xa, l1.m[a], k, l1.rank[a], l1.m[a], (int)l1.R,
-                              (int)ldx});
+                g1.push_back({l1.V.p + l1.V_off[a], z + off, H->z[1].p + l1.off[a], l1.rank[a], k, n, n, (int)N, (int)l1.R});
+                g2.push_back({l1.V.p + l1.V_off[a], H->z[1].p + l1.off[a], z + off, n, k, l1.rank[a], n, (int)l1.R, (int)N});
             }
         }
-        trsm_batched(s, td, 'L', false);
+        gemm_batched(s, g0, false, false, 1.0, 0.0);
         gemm_batched(s, g1, true, false, 1.0, 0.0);
         gemm_batched(s, g2, false, false, -1.0, 1.0);
     }
-    // up, levels 2..L-1: u = F^{-1} zh_children (in z[l-1]); zh = Vbar^T u; u <- u - Vbar zh
+    // up, levels 2..L-1: u = F^{-1} zh_children ; zh = Vbar^T u ; u <- u - Vbar zh   (u stored in ub[l])
     for (int l = 2; l < L; ++l) {
         const HssLevel& lv = H->lv[l];
         const HssLevel& pv = H->lv[l - 1];
-        std::vector<TrsmDesc> td;
-        std::vector<GemmDesc> g1, g2;
+        std::vector<GemmDesc> g0, g1, g2;
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
-            double* u = H->z[l - 1].p + pv.off[c1];
-            if (!lv.m[a]) continue;
-            td.push_back({lv.F.p + lv.F_off[a], u, lv.m[a], k, lv.m[a], (int)pv.R});
+            const int m = lv.m[a];
+            if (!m) continue;
+            double* u = H->ub[l].p + pv.off[c1];
+            g0.push_back({lv.Finv.p + lv.F_off[a], H->z[l - 1].p + pv.off[c1], u, m, k, m, m, (int)pv.R, (int)pv.R});
             if (lv.rank[a]) {
-                g1.push_back({lv.V.p + lv.V_off[a], u, H->z[l].p + lv.off[a], lv.rank[a], k, lv.m[a], lv.m[a], (int)pv.R,
-                              (int)lv.R});
-                g2.push_back({lv.V.p + lv.V_off[a], H->z[l].p + lv.off[a], u, lv.m[a], k, lv.rank[a], lv.m[a], (int)lv.R,
-                              (int)pv.R});
+                g1.push_back({lv.V.p + lv.V_off[a], u, H->z[l].p + lv.off[a], lv.rank[a], k, m, m, (int)pv.R, (int)lv.R});
+                g2.push_back({lv.V.p + lv.V_off[a], H->z[l].p + lv.off[a], u, m, k, lv.rank[a], m, (int)lv.R, (int)pv.R});
             }
         }
-        trsm_batched(s, td, 'L', false);
+        gemm_batched(s, g0, false, false, 1.0, 0.0);
         gemm_batched(s, g1, true, false, 1.0, 0.0);
         gemm_batched(s, g2, false, false, -1.0, 1.0);
     }
-    // root: (F F^T)^{-1} on the stacked top coefficients
+    // root: xh = F^{-T} F^{-1} zh_top   (into ub[L], then back into z[L-1])
     {
         const HssLevel& rt = H->lv[L];
         const HssLevel& pv = H->lv[L - 1];
-        if (rt.m[0]) {
-            trsm_batched(s, {{rt.F.p, H->z[L - 1].p, rt.m[0], k, rt.m[0], (int)pv.R}}, 'L', false);
-            trsm_batched(s, {{rt.F.p, H->z[L - 1].p, rt.m[0], k, rt.m[0], (int)pv.R}}, 'L', true);
+        const int m = rt.m[0];
+        if (m) {
+            gemm_batched(s, {{rt.Finv.p, H->z[L - 1].p, H->ub[L].p, m, k, m, m, (int)pv.R, (int)pv.R}}, false, false, 1.0, 0.0);
+            gemm_batched(s, {{rt.Finv.p, H->ub[L].p, H->z[L - 1].p, m, k, m, m, (int)pv.R, (int)pv.R}}, true, false, 1.0, 0.0);
         }
     }
-    // down: u <- F^{-T} (u + Vbar xh)
+    // down: children xh = F^{-T} (u + Vbar xh)
     for (int l = L - 1; l >= 2; --l) {
         const HssLevel& lv = H->lv[l];
         const HssLevel& pv = H->lv[l - 1];
-        std::vector<TrsmDesc> td;
-        std::vector<GemmDesc> g;
+        std::vector<GemmDesc> g, g3;
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
-            double* u = H->z[l - 1].p + pv.off[c1];
-            if (!lv.m[a]) continue;
+            const int m = lv.m[a];
+            if (!m) continue;
+            double* u = H->ub[l].p + pv.off[c1];
             if (lv.rank[a])
-                g.push_back({lv.V.p + lv.V_off[a], H->z[l].p + lv.off[a], u, lv.m[a], k, lv.rank[a], lv.m[a], (int)lv.R,
-                             (int)pv.R});
-            td.push_back({lv.F.p + lv.F_off[a], u, lv.m[a], k, lv.m[a], (int)pv.R});
+                g.push_back({lv.V.p + lv.V_off[a], H->z[l].p + lv.off[a], u, m, k, lv.rank[a], m, (int)lv.R, (int)pv.R});
+            g3.push_back({lv.Finv.p + lv.F_off[a], u, H->z[l - 1].p + pv.off[c1], m, k, m, m, (int)pv.R, (int)pv.R});
         }
         gemm_batched(s, g, false, false, 1.0, 1.0);
-        trsm_batched(s, td, 'L', true);
+        gemm_batched(s, g3, true, false, 1.0, 0.0);
     }
     // leaf: x = S^{-T} (z + V xh)
     {
-        std::vector<TrsmDesc> td;
-        std::vector<GemmDesc> g;
+        std::vector<GemmDesc> g, g3;
         for (int a = 0; a < l1.count; ++a) {
-            double* xa = x + t.begin[l1.first + a];
+            const int64_t off = t.begin[l1.first + a];
+            const int n = l1.m[a];
             if (l1.rank[a])
-                g.push_back({l1.V.p + l1.V_off[a], H->z[1].p + l1.off[a], xa, l1.m[a], k, l1.rank[a], l1.m[a], (int)l1.R,
-                             (int)ldx});
-            td.push_back({l1.F.p + l1.F_off[a], xa, l1.m[a], k, l1.m[a], (int)ldx});
+                g.push_back({l1.V.p + l1.V_off[a], H->z[1].p + l1.off[a], z + off, n, k, l1.rank[a], n, (int)l1.R, (int)N});
+            g3.push_back({l1.Finv.p + l1.F_off[a], z + off, x + off, n, k, n, n, (int)N, (int)ldx});
         }
         gemm_batched(s, g, false, false, 1.0, 1.0);
-        trsm_batched(s, td, 'L', true);
+        gemm_batched(s, g3, true, false, 1.0, 0.0);
     }
 }
 

@@ -104,3 +104,29 @@ def test_qrcp_matches_oracle(spd, batch, m, n, cap, tol):
         # Q columns are determined to ~eps/(R_tt/R_00): compare the well-conditioned ones
         good = min(same, int((np.abs(np.diag(Ro[:, :r])) > 1e-6 * abs(Ro[0, 0])).sum()))
         assert rel(Qg[b][:, :good], Qo[:, :good]) < 1e-9
+
+
+@pytest.mark.parametrize("batch,m,n", [(3, 6144, 300), (2, 4096, 130), (4, 700, 64), (1, 6144, 1480), (5, 100, 33)])
+def test_blocked_qr_r_factor(spd, batch, m, n):
+    """Cluster-panel blocked Householder QR: R^T R = A^T A and R matches numpy's R
+    up to row signs (diag(R) >= 0 here), including rank-deficient tails."""
+    import ctypes
+    import torch
+    rng = np.random.default_rng(m + n)
+    mats = []
+    for b in range(batch):
+        U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        mats.append((U * np.logspace(0, -15, n)) @ V.T)
+    A = np.stack(mats)
+    dA = torch.tensor(np.ascontiguousarray(A.transpose(0, 2, 1)), device="cuda")
+    st = spd.lib().spd_test_qr_unpivoted(batch, ctypes.c_void_p(dA.data_ptr()), m, n, m, m * n, spd._stream())
+    assert st == 0, spd.lib().spd_last_error()
+    torch.cuda.synchronize()
+    Rg = host(dA).reshape(batch, n, m).transpose(0, 2, 1)
+    for b in range(batch):
+        R = np.triu(Rg[b][:n, :n])
+        assert np.all(np.diag(R) >= 0)
+        Rn = np.linalg.qr(A[b], mode="r")
+        Rn = Rn * np.sign(np.diag(Rn))[:, None]
+        np.testing.assert_allclose(R, Rn, atol=1e-13 * abs(Rn[0, 0]))
