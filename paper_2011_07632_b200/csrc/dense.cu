@@ -96,37 +96,49 @@ __global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ 
     const GemmDesc d = descs[wk.x];
     const int n = d.n;
     if (!TA) {
-        const int i = wk.y * 256 + threadIdx.x;
-        if (i >= d.m) return;
+        // 32-row tile, lane = row (coalesced columns), the 8 warps split k
+        __shared__ double red[8][32][NV];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int i = wk.y * 32 + lane;
+        const bool ok = i < d.m;
         double acc[4][NV];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < NV; ++v) acc[u][v] = 0.0;
-        const double* a = d.A + i;
-        int kk = 0;
-        for (; kk + 4 <= d.k; kk += 4) {
+        const int kc = (d.k + 7) / 8, kb = warp * kc, ke = min(d.k, kb + kc);
+        if (ok) {
+            const double* a = d.A + i;
+            int kk = kb;
+            for (; kk + 4 <= ke; kk += 4) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double av = __ldg(a + (size_t)(kk + u) * d.lda);
+                for (int u = 0; u < 4; ++u) {
+                    const double av = __ldg(a + (size_t)(kk + u) * d.lda);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+                        if (v < n) acc[u][v] += av * __ldg(d.B + kk + u + (size_t)v * d.ldb);
+                }
+            }
+            for (; kk < ke; ++kk) {
+                const double av = __ldg(a + (size_t)kk * d.lda);
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
-                    if (v < n) acc[u][v] += av * __ldg(d.B + kk + u + (size_t)v * d.ldb);
+                    if (v < n) acc[0][v] += av * __ldg(d.B + kk + (size_t)v * d.ldb);
             }
         }
-        for (; kk < d.k; ++kk) {
-            const double av = __ldg(a + (size_t)kk * d.lda);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) red[warp][lane][v] = (acc[0][v] + acc[1][v]) + (acc[2][v] + acc[3][v]);
+        __syncthreads();
+        if (warp == 0 && ok) {
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                if (v < n) acc[0][v] += av * __ldg(d.B + kk + (size_t)v * d.ldb);
+                if (v < n) {
+                    double sum = 0.0;
+                    for (int w = 0; w < 8; ++w) sum += red[w][lane][v];
+                    double* c = d.C + i + (size_t)v * d.ldc;
+                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * sum;
+                }
         }
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-            if (v < n) {
-                const double sum = (acc[0][v] + acc[1][v]) + (acc[2][v] + acc[3][v]);
-                double* c = d.C + i + (size_t)v * d.ldc;
-                *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * sum;
-            }
     } else {
         const int lane = threadIdx.x & 31;
         const int i = wk.y * 8 + (threadIdx.x >> 5);
@@ -172,7 +184,7 @@ static void gemv_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool tr
     for (int i = 0; i < (int)d.size(); ++i) {
         if (d[i].m <= 0 || d[i].n <= 0) continue;
         if (d[i].k <= 0 && beta == 1.0) continue;
-        const int rows_per = transA ? 8 : 256;
+        const int rows_per = transA ? 8 : 32;
         for (int t = 0; t < ceil_div(d[i].m, rows_per); ++t) work.push_back(make_int2(i, t));
         fl += 2.0 * d[i].m * d[i].n * d[i].k;
         by += 8.0 * ((double)d[i].m * d[i].k + 2.0 * d[i].m * d[i].n);
@@ -825,6 +837,7 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
     extern __shared__ double sm[];                    // rp x QB panel slice (col-major, ld rp)
     __shared__ double part[2][QB + 2];                // [0]: sigma, x0 ; [1]: dots
     __shared__ double Gp[QB][QB + 1];                 // partial V^T V
+    __shared__ double Gs[QB][QB + 1];                 // cluster-summed V^T V (CTA 0)
     __shared__ double red[8];
     __shared__ double s_beta[QB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -906,37 +919,43 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
         const int i = e % rp, c = e / rp;
         if (i < nr && r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
     }
-    // T = compact-WY factor from V^T V (cluster-reduced) and the betas
+    // T = compact-WY factor from V^T V: partial Gram of my slice (v_a = 0 above a,
+    // 1 at a, slice value below), cluster-reduced in parallel by CTA 0
     for (int pr = warp; pr < jb * jb; pr += 8) {
         const int a = pr % jb, b = pr / jb;
         if (a >= b) continue;
-        const double* va = d.V + (size_t)a * d.ldv;
-        const double* vb = d.V + (size_t)b * d.ldv;
         double s = 0.0;
-        for (int i = lane; i < nr; i += 32) { const int gi = r0 + i; s += va[gi] * vb[gi]; }
+        for (int i = lane; i < nr; i += 32) {
+            const int gi = r0 + i;
+            if (gi < b) continue;
+            const double vb = (gi == b) ? 1.0 : sm[i + b * rp];
+            const double va = sm[i + a * rp];          // gi >= b > a: below a's diagonal
+            s += va * vb;
+        }
         s = warp_sum(s);
         if (lane == 0) Gp[a][b] = s;
     }
     cluster.sync();
-    if (g == 0 && threadIdx.x == 0) {
-        __threadfence();
-        double* T = d.T;
-        const double* bet = s_beta;
-        double G[QB][QB];
-        for (int b = 0; b < jb; ++b)
-            for (int a = 0; a < b; ++a) {
-                double s = 0.0;
-                for (int q = 0; q < QCL; ++q) s += cluster.map_shared_rank(&Gp[0][0], q)[a * (QB + 1) + b];
-                G[a][b] = s;
+    if (g == 0) {
+        for (int pr = threadIdx.x; pr < jb * jb; pr += blockDim.x) {
+            const int a = pr % jb, b = pr / jb;
+            if (a >= b) continue;
+            double s = 0.0;
+            for (int q = 0; q < QCL; ++q) s += cluster.map_shared_rank(&Gp[0][0], q)[a * (QB + 1) + b];
+            Gs[a][b] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double* T = d.T;
+            for (int j = 0; j < jb; ++j) {
+                for (int a = 0; a < j; ++a) {
+                    double s = 0.0;
+                    for (int b = a; b < j; ++b) s += T[a + b * QB] * Gs[b][j];
+                    T[a + j * QB] = -s_beta[j] * s;
+                }
+                T[j + j * QB] = s_beta[j];
+                for (int a = j + 1; a < QB; ++a) T[a + j * QB] = 0.0;
             }
-        for (int j = 0; j < jb; ++j) {
-            for (int a = 0; a < j; ++a) {
-                double s = 0.0;
-                for (int b = a; b < j; ++b) s += T[a + b * QB] * G[b][j];
-                T[a + j * QB] = -bet[j] * s;
-            }
-            T[j + j * QB] = bet[j];
-            for (int a = j + 1; a < QB; ++a) T[a + j * QB] = 0.0;
         }
     }
     cluster.sync();                                   // keep smem alive for remote readers

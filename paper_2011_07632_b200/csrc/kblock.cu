@@ -14,26 +14,43 @@
 
 namespace spd {
 
-constexpr int KB_M = 64, KB_N = 64, KB_K = 16, KB_THREADS = 128;
+constexpr int KB_M = 64, KB_K = 16;
 
 struct KbWork { int target, tm, tn; };
 
-__global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
+template <int KID>
+__device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
+    if (KID == SPD_K_GAUSSIAN) return exp(-r2 * kp.inv_l2);
+    if (KID == SPD_K_MATERN32) { const double t = sqrt(r2) * kp.sqrt3_inv_l; return (1.0 + t) * exp(-t); }
+    if (KID == SPD_K_EXPONENTIAL) return exp(-sqrt(r2) * kp.inv_l);
+    return rsqrt(r2 + kp.l2);
+}
+
+// CTA tile: KB_M target rows x NC columns, NC/32 * 2 warps (each 32 x 32 = 4x4 DMMA
+// m8n8k4 blocks).  Per source chunk of 16 points: the 64x16 kernel tile is
+// evaluated once into shared memory (shared by all column warps) and contracted
+// with the 16 x NC slice of X; the next chunk's X slice and coordinates are
+// prefetched into registers while the current chunk is evaluated/contracted.
+template <int KID, int NC>
+__global__ void __launch_bounds__(2 * NC) kblock_kernel(
     KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
     const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
     const KbWork* __restrict__ work) {
+    constexpr int NT = 2 * NC;                  // threads
+    constexpr int WN = NC / 32;                 // warps along columns
+    constexpr int XPT = KB_K * NC / NT;         // X values per thread per chunk (= 8)
+    constexpr int EPT = KB_M * KB_K / NT;       // kernel evaluations per thread per chunk
     __shared__ double Ks[KB_K][KB_M + 1];
-    __shared__ double Xs[KB_K][KB_N + 1];
+    __shared__ double Xs[KB_K][NC + 1];
     __shared__ double Sx[3][KB_K];
     const KbWork wk = work[blockIdx.x];
     const KbTarget tg = targets[wk.target];
     const KbBlock tb = blocks[tg.blk];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, q = lane & 3, wm = warp >> 1, wn = warp & 1;
-    const int r0 = wk.tm * KB_M, c0 = wk.tn * KB_N;
+    const int g = lane >> 2, q = lane & 3, wm = warp / WN, wn = warp % WN;
+    const int r0 = wk.tm * KB_M, c0 = wk.tn * NC;
     const int nrows = min(KB_M, tb.n - r0);
-    // my evaluation row and its coordinates
-    const int er = tid & (KB_M - 1), ec0 = (tid >> 6) * 8;
+    const int er = tid & (KB_M - 1), ec0 = (tid / KB_M) * EPT;
     double rx[3] = {0.0, 0.0, 0.0};
     if (er < nrows)
         for (int a = 0; a < d; ++a) rx[a] = tb.x[(size_t)a * tb.ds + r0 + er];
@@ -45,33 +62,43 @@ __global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+    double xr[XPT], sr = 0.0;
     for (int e = tg.e_begin; e < tg.e_end; ++e) {
         const KbEntry en = entries[e];
         if (c0 < en.ncols) {
             const KbBlock sb = blocks[en.src];
-            const int ncols = min(KB_N, en.ncols - c0);
+            const int ncols = min(NC, en.ncols - c0);
             const bool use_shift = (shift != 0.0) && rid >= 0 && sb.id0 >= 0;
+            auto load = [&](int k0) {
+                const int nk = min(KB_K, sb.n - k0);
+#pragma unroll
+                for (int u = 0; u < XPT; ++u) {
+                    const int idx = tid + u * NT;
+                    const int kk = idx % KB_K, j = idx / KB_K;
+                    xr[u] = (kk < nk && j < ncols) ? __ldg(en.X + k0 + kk + (size_t)(c0 + j) * en.ldx) : 0.0;
+                }
+                if (tid < KB_K * 3) {
+                    const int a = tid / KB_K, c = tid % KB_K;
+                    sr = (a < d && c < nk) ? __ldg(sb.x + (size_t)a * sb.ds + k0 + c) : 0.0;
+                }
+            };
+            load(0);
             for (int k0 = 0; k0 < sb.n; k0 += KB_K) {
                 const int nk = min(KB_K, sb.n - k0);
                 __syncthreads();
-                if (tid < KB_K * 3) {
-                    int a = tid / KB_K, c = tid % KB_K;
-                    Sx[a][c] = (a < d && c < nk) ? sb.x[(size_t)a * sb.ds + k0 + c] : 0.0;
+#pragma unroll
+                for (int u = 0; u < XPT; ++u) {
+                    const int idx = tid + u * NT;
+                    Xs[idx % KB_K][idx / KB_K] = xr[u];
                 }
-                for (int idx = tid; idx < KB_K * KB_N; idx += KB_THREADS) {
-                    int kk = idx % KB_K, j = idx / KB_K;
-                    Xs[kk][j] = (kk < nk && j < ncols) ? en.X[k0 + kk + (size_t)(c0 + j) * en.ldx] : 0.0;
-                }
+                if (tid < KB_K * 3) Sx[tid / KB_K][tid % KB_K] = sr;
                 __syncthreads();
+                if (k0 + KB_K < sb.n) load(k0 + KB_K);          // prefetch the next chunk
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < EPT; ++c) {
                     const int kc = ec0 + c;
-                    double r2 = 0.0;
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        if (a < d) { double df = rx[a] - Sx[a][kc]; r2 += df * df; }
-                    }
-                    double kv = kernel_r2(kp, r2);
+                    const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
+                    double kv = kval<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
                     if (use_shift && rid == sb.id0 + k0 + kc) kv += shift;
                     Ks[kc][er] = (er < nrows && kc < nk) ? kv : 0.0;
                 }
@@ -93,7 +120,7 @@ __global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
         const bool flush = (e + 1 == tg.e_end) || entries[e + 1].Y != en.Y;
         if (flush) {
             if (c0 < en.ncols) {
-                const int ncols = min(KB_N, en.ncols - c0);
+                const int ncols = min(NC, en.ncols - c0);
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -118,13 +145,6 @@ __global__ void __launch_bounds__(KB_THREADS) kblock_kernel(
 // source points 32 at a time, broadcasting each point's coordinates and values
 // by shuffles, so every kernel entry is evaluated exactly once; partial sums of
 // the warps are reduced in shared memory before one read-modify-write of Y.
-template <int KID>
-__device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
-    if (KID == SPD_K_GAUSSIAN) return exp(-r2 * kp.inv_l2);
-    if (KID == SPD_K_MATERN32) { const double t = sqrt(r2) * kp.sqrt3_inv_l; return (1.0 + t) * exp(-t); }
-    if (KID == SPD_K_EXPONENTIAL) return exp(-sqrt(r2) * kp.inv_l);
-    return rsqrt(r2 + kp.l2);
-}
 
 template <int KID, int NV>
 __global__ void __launch_bounds__(256) kblock_vec_kernel(
@@ -273,6 +293,9 @@ __global__ void __launch_bounds__(256) kstore_build_kernel(KernelParams kp, doub
     }
 }
 
+// The stored blocks of one (target, 32-row tile) are contiguous: (sum_e n_src) x 32.
+// The 8 warps split that column range evenly (crossing entry boundaries), lane =
+// row, so every warp streams the same number of bytes; one output group per target.
 __global__ void __launch_bounds__(256) kstore_apply_kernel(const KbBlock* __restrict__ blocks, const KbTarget* __restrict__ targets,
                                                            const KbEntry* __restrict__ entries, const int64_t* __restrict__ eoff,
                                                            const KsWork* __restrict__ work, const double* __restrict__ vals) {
@@ -282,34 +305,36 @@ __global__ void __launch_bounds__(256) kstore_apply_kernel(const KbBlock* __rest
     const KbBlock tb = blocks[tg.blk];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int row = wk.tile * 32 + lane;
-    int g0 = tg.e_begin;
-    while (g0 < tg.e_end) {
-        int g1 = g0 + 1;
-        while (g1 < tg.e_end && entries[g1].Y == entries[g0].Y) ++g1;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (int e = g0 + warp; e < g1; e += 8) {
-            const KbEntry en = entries[e];
-            const int ns = blocks[en.src].n;
-            const double* v = vals + wk.base + eoff[e] + lane;
-            const double* x = en.X;
-            int c = 0;
-            for (; c + 4 <= ns; c += 4) {
-                a0 += __ldg(v + (size_t)c * 32) * __ldg(x + c);
-                a1 += __ldg(v + (size_t)(c + 1) * 32) * __ldg(x + c + 1);
-                a2 += __ldg(v + (size_t)(c + 2) * 32) * __ldg(x + c + 2);
-                a3 += __ldg(v + (size_t)(c + 3) * 32) * __ldg(x + c + 3);
-            }
-            for (; c < ns; ++c) a0 += __ldg(v + (size_t)c * 32) * __ldg(x + c);
+    const int ne = tg.e_end - tg.e_begin;
+    const int64_t ctot = (eoff[tg.e_end - 1] + 32LL * blocks[entries[tg.e_end - 1].src].n) / 32;
+    const int64_t cb = ctot * warp / 8, ce = ctot * (warp + 1) / 8;
+    // locate the entry holding column cb
+    int e = tg.e_begin;
+    while (e + 1 < tg.e_end && eoff[e + 1] / 32 <= cb) ++e;
+    (void)ne;
+    const double* v = vals + wk.base + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t c = cb;
+    while (c < ce) {
+        const int64_t e0 = eoff[e] / 32;
+        const int ns = blocks[entries[e].src].n;
+        const int64_t cend = min(ce, e0 + ns);
+        const double* x = entries[e].X - e0;          // x[c] for global column c
+        for (; c + 4 <= cend; c += 4) {
+            a0 += __ldg(v + c * 32) * __ldg(x + c);
+            a1 += __ldg(v + (c + 1) * 32) * __ldg(x + c + 1);
+            a2 += __ldg(v + (c + 2) * 32) * __ldg(x + c + 2);
+            a3 += __ldg(v + (c + 3) * 32) * __ldg(x + c + 3);
         }
-        red[warp][lane] = (a0 + a1) + (a2 + a3);
-        __syncthreads();
-        if (warp == 0 && row < tb.n) {
-            double sum = 0.0;
-            for (int w = 0; w < 8; ++w) sum += red[w][lane];
-            entries[g0].Y[row] += sum;
-        }
-        __syncthreads();
-        g0 = g1;
+        for (; c < cend; ++c) a0 += __ldg(v + c * 32) * __ldg(x + c);
+        ++e;
+    }
+    red[warp][lane] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    if (warp == 0 && row < tb.n) {
+        double sum = 0.0;
+        for (int w = 0; w < 8; ++w) sum += red[w][lane];
+        entries[tg.e_begin].Y[row] += sum;
     }
 }
 
@@ -342,7 +367,11 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
         int maxc = 0;
         for (auto& e : entries) maxc = std::max(maxc, e.ncols);
         if (maxc == 0) return;
-        if (store && maxc == 1) {
+        bool single_group = true;
+        for (const auto& tg : targets)
+            for (int e = tg.e_begin + 1; e < tg.e_end; ++e)
+                if (entries[e].Y != entries[tg.e_begin].Y) single_group = false;
+        if (store && maxc == 1 && single_group) {
             std::vector<int64_t> eoff;
             std::vector<KsWork> work;
             const int64_t total = store_layout(blocks, targets, entries, eoff, work);
@@ -375,6 +404,9 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
         }
         if (maxc <= 4) { kblock_vec(s, kp, shift, d, blocks, targets, entries, maxc); return; }
     }
+    int maxc_all = 0;
+    for (auto& e : entries) maxc_all = std::max(maxc_all, e.ncols);
+    const int NC = maxc_all > 64 ? 128 : 64;
     std::vector<KbWork> work;
     for (int t = 0; t < (int)targets.size(); ++t) {
         const KbTarget& tg = targets[t];
@@ -382,7 +414,7 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
         int maxc = 0;
         for (int e = tg.e_begin; e < tg.e_end; ++e) maxc = std::max(maxc, entries[e].ncols);
         const int nr = blocks[tg.blk].n;
-        for (int tn = 0; tn < ceil_div(maxc, KB_N); ++tn)
+        for (int tn = 0; tn < ceil_div(maxc, NC); ++tn)
             for (int tm = 0; tm < ceil_div(nr, KB_M); ++tm) work.push_back({t, tm, tn});
     }
     if (work.empty()) return;
@@ -391,12 +423,11 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     for (int t = 0; t < (int)targets.size(); ++t)
         for (int e = targets[t].e_begin; e < targets[t].e_end; ++e) cost[t] += blocks[entries[e].src].n;
     std::stable_sort(work.begin(), work.end(), [&](const KbWork& a, const KbWork& b) { return cost[a.target] > cost[b.target]; });
-    double fl = 0, by = 0, ev = 0;
+    double fl = 0, by = 0;
     for (const auto& tg : targets)
         for (int e = tg.e_begin; e < tg.e_end; ++e) {
             const double nr = blocks[tg.blk].n, ns = blocks[entries[e].src].n, nc = entries[e].ncols;
             fl += 2.0 * nr * ns * nc;
-            ev += nr * ns;
             by += 8.0 * (ns * nc + 2.0 * nr * nc);
         }
     DevArray<KbBlock> db(s, blocks);
@@ -404,7 +435,17 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     DevArray<KbEntry> de(s, entries);
     DevArray<KbWork> dw(s, work);
     ProfScope prof(s, "kblock_dmma", fl, by);
-    kblock_kernel<<<(unsigned)work.size(), KB_THREADS, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);
+    const unsigned nb = (unsigned)work.size();
+#define SPD_KB_LAUNCH(KID)                                                                               \
+    if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);    \
+    else kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);
+    switch (kp.id) {
+    case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
+    case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
+    case SPD_K_EXPONENTIAL: SPD_KB_LAUNCH(SPD_K_EXPONENTIAL); break;
+    default: SPD_KB_LAUNCH(SPD_K_IMQ); break;
+    }
+#undef SPD_KB_LAUNCH
     SPD_LAUNCH();
 }
 
