@@ -263,6 +263,7 @@ def run_ours(args):
     lib.spd_prof_enable(1)
     l0 = lib.spd_launch_count()
     recs, step_s = [], []
+    torch.cuda.nvtx.range_push("timed")
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -273,6 +274,7 @@ def run_ours(args):
         s1.synchronize()
         step_s.append(s0.elapsed_time(s1) * 1e-3)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     launches = lib.spd_launch_count() - l0
     lib.spd_prof_enable(0)
     prof = prof_table(lib)

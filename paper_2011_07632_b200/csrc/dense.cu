@@ -32,31 +32,38 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
     const int g = lane >> 2, q = lane & 3;
     const int wm = warp >> 1, wn = warp & 1;
     const int m0 = tr.tm * GT, n0 = tr.tn * GT;
+    constexpr int PT = GT * GK / 128;                 // elements per thread per tile (8)
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-    for (int k0 = 0; k0 < d.k; k0 += GK) {
-        // load A tile (GT rows x GK k) and B tile (GK k x GT cols)
-        for (int e = tid; e < GT * GK; e += 128) {
+    double ra[PT], rb[PT];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < PT; ++u) {
+            const int e = tid + u * 128;
             int i, kk;
             if (TA) { kk = e % GK; i = e / GK; } else { i = e % GT; kk = e / GT; }
-            int gi = m0 + i, gk = k0 + kk;
-            double v = 0.0;
-            if (gi < d.m && gk < d.k) v = TA ? d.A[gk + (size_t)gi * d.lda] : d.A[gi + (size_t)gk * d.lda];
-            As[kk][i] = v;
+            const int gi = m0 + i, gk = k0 + kk;
+            ra[u] = (gi < d.m && gk < d.k) ? (TA ? __ldg(d.A + gk + (size_t)gi * d.lda) : __ldg(d.A + gi + (size_t)gk * d.lda)) : 0.0;
+            int j, kb;
+            if (TB) { j = e % GT; kb = e / GT; } else { kb = e % GK; j = e / GK; }
+            const int gj = n0 + j, gkb = k0 + kb;
+            rb[u] = (gj < d.n && gkb < d.k) ? (TB ? __ldg(d.B + gj + (size_t)gkb * d.ldb) : __ldg(d.B + gkb + (size_t)gj * d.ldb)) : 0.0;
         }
-        for (int e = tid; e < GT * GK; e += 128) {
-            int j, kk;
-            if (TB) { j = e % GT; kk = e / GT; } else { kk = e % GK; j = e / GK; }
-            int gj = n0 + j, gk = k0 + kk;
-            double v = 0.0;
-            if (gj < d.n && gk < d.k) v = TB ? d.B[gj + (size_t)gk * d.ldb] : d.B[gk + (size_t)gj * d.ldb];
-            Bs[kk][j] = v;
+    };
+    load(0);
+    for (int k0 = 0; k0 < d.k; k0 += GK) {
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PT; ++u) {
+            const int e = tid + u * 128;
+            if (TA) As[e % GK][e / GK] = ra[u]; else As[e / GT][e % GT] = ra[u];
+            if (TB) Bs[e / GT][e % GT] = rb[u]; else Bs[e % GK][e / GK] = rb[u];
         }
         __syncthreads();
+        if (k0 + GK < d.k) load(k0 + GK);                 // prefetch the next chunk
 #pragma unroll
         for (int ks = 0; ks < GK / 4; ++ks) {
             double af[4], bf[4];
@@ -69,7 +76,6 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
 #pragma unroll
                 for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
         }
-        __syncthreads();
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
