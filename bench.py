@@ -256,11 +256,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # ---------------- timed region (device events, max over ranks)
+    # ---------------- timed region (device events, max over ranks; library profiler OFF)
     sampler = ClockSampler(local)
     sampler.start()
-    lib.spd_prof_reset()
-    lib.spd_prof_enable(1)
     l0 = lib.spd_launch_count()
     recs, step_s = [], []
     torch.cuda.nvtx.range_push("timed")
@@ -276,8 +274,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     launches = lib.spd_launch_count() - l0
-    lib.spd_prof_enable(0)
-    prof = prof_table(lib)
     clocks = sampler.stop()
     t_step = max_over_ranks(statistics.mean(step_s))
     # ---------------- end-to-end: host (pinned) inputs, H2D inside, result D2H inside
@@ -297,6 +293,24 @@ def run_ours(args):
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e-3)
+    # ---------------- profiled pass (same steps, per-kernel-class CUDA events on the
+    # launching streams; kept out of the timed region because the per-launch event
+    # pairs and their host-side drains perturb the step time)
+    lib.spd_prof_reset()
+    lib.spd_prof_enable(1)
+    prof_s = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        step(pts, b)
+        s1.record(stream)
+        s1.synchronize()
+        prof_s.append(s0.elapsed_time(s1) * 1e-3)
+    torch.cuda.synchronize()
+    lib.spd_prof_enable(0)
+    prof = prof_table(lib)
     e2e_v = max_over_ranks(statistics.mean(e2e))
     if rank != 0:
         if world > 1:
@@ -324,7 +338,8 @@ def run_ours(args):
             roof = {"kernel": nm, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs", 6550.7),
                     "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6550.7), 4), "traffic": None,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        roof["share_of_step"] = round(p["ms"] * 1e-3 / sum(step_s), 4)
+        roof["share_of_step"] = round(p["ms"] * 1e-3 / sum(prof_s), 4)
+        roof["measured_in"] = "profiled pass (same steps as the timed region)"
     mv = statistics.mean(r["h2_mv_s"] for r in recs)
     mv_flops = prof.get("kblock_dmma", {}).get("flops", 0)
     line = {
@@ -348,6 +363,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_v, 4), "unit": "s", "h2d_bytes_per_step": int(8 * N * (CFG.d + 1)),
                 "d2h_bytes_per_step": int(8 * N)},
         "gpu_launches": int(launches // max(1, args.steps)),
+        "profiled_pass_s_per_step": round(statistics.mean(prof_s), 4),
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

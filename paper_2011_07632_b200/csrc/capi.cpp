@@ -39,6 +39,7 @@ void spd_comm_free(spd_comm_t c) { delete c; }
 spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf, double tol,
                     const spd_h2_opts* opts, spd_comm_t c, void* stream, spd_h2_t* out) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(out != nullptr, "h2_build: out is NULL");
         *out = nullptr;
         SPD_REQUIRE(pts != nullptr && n >= 1, "h2_build: need n >= 1 points");
@@ -59,11 +60,12 @@ spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf,
     })
 }
 
-void h2_free(spd_h2_t h) { delete h; }
+void h2_free(spd_h2_t h) { if (h) { cudaDeviceSynchronize(); delete h; } }
 
 spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t k,
                      void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(h != nullptr, "h2_matvec: null handle");
         SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "h2_matvec: bad layout");
         SPD_REQUIRE(k >= 0 && ldx >= h->N && ldy >= h->N, "h2_matvec: ld must be >= n");
@@ -78,7 +80,6 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
             permute_rows(s, h->perm.p, h->N, (int)k, X, ldx, xt.p, h->N, true);
             h2_apply_tree(h, xt.p, h->N, yt.p, h->N, (int)k, s);
             permute_rows(s, h->perm.p, h->N, (int)k, yt.p, h->N, Y, ldy, false);
-            SPD_CUDA(cudaStreamSynchronize(s));
         }
     })
 }
@@ -86,6 +87,7 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
 spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample, uint64_t seed,
                         const double* omega, void* stream, spd_hss_t* out) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(out != nullptr, "spdhss_build: out is NULL");
         *out = nullptr;
         SPD_REQUIRE(h != nullptr, "spdhss_build: null H2 handle");
@@ -100,11 +102,12 @@ spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample
     })
 }
 
-void hss_free(spd_hss_t H) { delete H; }
+void hss_free(spd_hss_t H) { if (H) { cudaDeviceSynchronize(); delete H; } }
 
 spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, double* X, int64_t ldx, int64_t nrhs,
                      void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(H != nullptr, "hss_solve: null handle");
         SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "hss_solve: bad layout");
         const int64_t N = H->h2->N;
@@ -119,7 +122,6 @@ spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, doub
             permute_rows(s, H->h2->perm.p, N, (int)nrhs, B, ldb, bt.p, N, true);
             hss_solve_tree(H, bt.p, N, xt.p, N, (int)nrhs, s);
             permute_rows(s, H->h2->perm.p, N, (int)nrhs, xt.p, N, X, ldx, false);
-            SPD_CUDA(cudaStreamSynchronize(s));
         }
     })
 }
@@ -129,6 +131,7 @@ spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, doubl
     spd_pcg_report local{};
     if (!rep) rep = &local;
     try {
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(A != nullptr && b != nullptr && x != nullptr, "pcg_solve: null argument");
         SPD_REQUIRE(M == nullptr || M->h2 == A, "pcg_solve: preconditioner built from another H2");
         SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "pcg_solve: bad layout");
@@ -142,7 +145,6 @@ spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, doubl
             permute_rows(s, A->perm.p, N, 1, b, N, bt.p, N, true);
             pcg_tree(A, M, bt.p, xt.p, tol, maxit, rep, s);
             permute_rows(s, A->perm.p, N, 1, xt.p, N, x, N, false);
-            SPD_CUDA(cudaStreamSynchronize(s));
         }
         if (!rep->converged) {
             set_last_error("pcg_solve: not converged in maxit iterations");
@@ -249,6 +251,7 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
 spd_status spd_test_gemm(int transA, int transB, int m, int n, int k, double alpha, const double* A, int lda,
                          const double* B, int ldb, double beta, double* C, int ldc, void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         std::vector<GemmDesc> d{{A, B, C, m, n, k, lda, ldb, ldc}};
         gemm_batched((cudaStream_t)stream, d, transA != 0, transB != 0, alpha, beta);
         SPD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -257,6 +260,7 @@ spd_status spd_test_gemm(int transA, int transB, int m, int n, int k, double alp
 
 spd_status spd_test_potrf(double* A, int n, int lda, int* info_host, void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         cudaStream_t s = (cudaStream_t)stream;
         DBuf<int> info(1);
         DBuf<double> bad(1);
@@ -269,6 +273,7 @@ spd_status spd_test_potrf(double* A, int n, int lda, int* info_host, void* strea
 spd_status spd_test_trsm(char uplo, int trans, const double* T, int n, int ldt, double* X, int nrhs, int ldx,
                          void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         trsm_batched((cudaStream_t)stream, {{T, X, n, nrhs, ldt, ldx}}, uplo, trans != 0);
         SPD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     })
@@ -277,6 +282,7 @@ spd_status spd_test_trsm(char uplo, int trans, const double* T, int n, int ldt, 
 spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t stride, int max_rank,
                          double rel_tol, int* piv, int* rank, double* Q, int64_t qstride, void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         cudaStream_t s = (cudaStream_t)stream;
         DBuf<double> beta((size_t)batch * std::max(1, std::min(m, n)));
         DBuf<double> norms((size_t)batch * std::max(1, n));
@@ -297,6 +303,7 @@ spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t str
 
 spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int64_t stride, void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         std::vector<QrDesc> d;
         for (int b = 0; b < batch; ++b) d.push_back({A + b * stride, m, n, ld});
         qr_unpivoted_batched((cudaStream_t)stream, d);
@@ -305,6 +312,7 @@ spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int
 
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) {
     SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(h != nullptr && P_host != nullptr, "spd_test_proxies: null argument");
         cudaStream_t s = (cudaStream_t)stream;
         DBuf<double> P((size_t)h->n_proxy * h->d);

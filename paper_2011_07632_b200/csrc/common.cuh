@@ -27,6 +27,7 @@ void set_last_error(const std::string& m);
                 std::to_string(__LINE__));                                              \
     } while (0)
 void count_launch();
+void count_launches(long long n);          // e.g. the kernel nodes of one graph replay
 #define SPD_LAUNCH() do { ::spd::count_launch(); SPD_CUDA(cudaGetLastError()); } while (0)
 #define SPD_REQUIRE(cond, msg) do { if (!(cond)) throw ::spd::Error(SPD_EINVAL, msg); } while (0)
 
@@ -40,6 +41,8 @@ struct ProfScope {
     ProfScope(cudaStream_t st, const char* name, double flops, double bytes);
     ~ProfScope();
 };
+// debug: with env SPD_STAGES set, synchronize s and print the wall time since the last mark
+void stage_mark(cudaStream_t s, const char* name, int level = 0);
 // records created while capturing a graph are moved out and re-accumulated
 // after every replay of that graph
 struct ProfCaptured;
@@ -49,6 +52,18 @@ void prof_accumulate(ProfCaptured* c);            // after a (synchronized) repl
 void prof_release(ProfCaptured* c);
 
 // ---------------------------------------------------------------- device memory
+// Device buffers are stream-ordered (cudaMallocAsync / cudaFreeAsync from the
+// device's default pool, which keeps freed memory cached up to a threshold), on
+// the stream of the current library call (AllocStreamScope; the legacy stream
+// when no call is active).  This keeps the many per-level allocations of the
+// builds off the host's critical path (cudaMalloc/cudaFree synchronize).
+cudaStream_t& alloc_stream();
+void init_mem_pool();
+struct AllocStreamScope {
+    cudaStream_t prev;
+    explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { init_mem_pool(); alloc_stream() = s; }
+    ~AllocStreamScope() { alloc_stream() = prev; }
+};
 template <class T>
 struct DBuf {                       // owning device buffer
     T* p = nullptr;
@@ -63,9 +78,9 @@ struct DBuf {                       // owning device buffer
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) SPD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (count) SPD_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), alloc_stream()));
     }
-    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    void release() { if (p) cudaFreeAsync(p, alloc_stream()); p = nullptr; n = 0; }
     void zero(cudaStream_t s) { if (n) SPD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
     void upload(const std::vector<T>& h, cudaStream_t s) {
         if (h.size() != n) alloc(h.size());

@@ -198,6 +198,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
     h->active[0] = 0;
     double t1 = now_s();
     h->timings[0] = t1 - t0;
+    stage_mark(s, nullptr);
     // --- device points (tree order, SoA)
     h->perm.upload(t.perm, s);
     DBuf<double> pts_d((size_t)N * d);
@@ -291,6 +292,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 qd.norms = norms_d.p + piv_off[a];
                 qdesc.push_back(qd);
             }
+            stage_mark(s, "h2 alloc/desc", k);
             {
                 DevArray<ProxyDesc> dp(s, pdesc);
                 ProfScope prof(s, "proxy_points", 0, 0);
@@ -303,6 +305,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 proxy_matrix_kernel<<<dim3(64, (unsigned)mdesc.size()), 256, 0, s>>>(dm.p, h->kp, d, n_p);
                 SPD_LAUNCH();
             }
+            stage_mark(s, "h2 proxies+matrix", k);
             // two-stage ID: M^T = Q0 R0 (blocked, DMMA) then QRCP of R0; column norms and
             // hence pivots and R are invariant under the left-orthogonal Q0 (reading R4)
             {
@@ -319,7 +322,9 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 qr_unpivoted_batched(s, tall);
                 zero_lower_batched(s, tri);
             }
+            stage_mark(s, "h2 blocked QR", k);
             qrcp_batched(s, qdesc, h->tol);
+            stage_mark(s, "h2 qrcp", k);
             std::vector<int> rk(lv.count + 1);
             SPD_CUDA(cudaMemcpyAsync(rk.data(), rank_d.p, sizeof(int) * (lv.count + 1), cudaMemcpyDeviceToHost, s));
             SPD_CUDA(cudaStreamSynchronize(s));
@@ -360,6 +365,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 SPD_LAUNCH();
             }
             SPD_CUDA(cudaStreamSynchronize(s));   // Mt, P freed at scope exit
+            stage_mark(s, "h2 trsm+id", k);
         }
         // pack level arrays
         for (int a = 0; a < lv.count; ++a) {
@@ -381,6 +387,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                                        sizeof(double) * sr, d, cudaMemcpyDeviceToDevice, s));
         }
         SPD_CUDA(cudaStreamSynchronize(s));
+        stage_mark(s, "h2 pack (+free)", k);
     }
     h->timings[1] = now_s() - t1;
 }
@@ -418,22 +425,10 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
 void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     if (h->tree.L > 1) ensure_ws(h, k, s);
     if (k != 1 || h->stored_mode != -1) return;
-    // stored k=1 blocks if they need < 40% of the free device memory (env SPD_STORED=0/1 overrides)
+    // stored symmetric k=1 blocks if they need < 40% of the free device memory (env SPD_STORED=0/1 overrides)
     const char* env = getenv("SPD_STORED");
     if (env && env[0] == '0') { h->stored_mode = 0; return; }
-    const TreeH& t = h->tree;
-    double need = 0;
-    {
-        const int l1 = t.first(1);
-        std::vector<int64_t> rows(t.count(1));
-        for (int a = 0; a < t.count(1); ++a) rows[a] = 32LL * ceil_div(t.size(l1 + a), 32);
-        for (auto& pr : h->lists.near) need += 8.0 * rows[pr.first - l1] * t.size(pr.second);
-        for (int lk = 1; lk < t.L; ++lk) {
-            const H2Level& lv = h->lv[lk];
-            for (auto& pr : h->lists.type3[lk])
-                need += 8.0 * 32.0 * ceil_div(lv.rank[pr.first - lv.first], 32) * lv.rank[pr.second - lv.first];
-        }
-    }
+    const double need = (double)h2sym_bytes(h);
     size_t fr = 0, tot = 0;
     SPD_CUDA(cudaMemGetInfo(&fr, &tot));
     h->stored_mode = (env && env[0] == '1') || need < 0.4 * (double)fr ? 1 : 0;
@@ -520,14 +515,25 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     const TreeH& t = h->tree;
     const int L = t.L;
     const int64_t N = h->N;
+    if (k == 1 && h->stored_mode == 1) {
+        // stored symmetric blocks: up pass, near + all coupling levels in one launch, gather, down pass
+        h2sym_build(h, s);
+        std::vector<double*> xh(L, nullptr), yh(L, nullptr);
+        if (L > 1) {
+            ensure_ws(h, 1, s);
+            for (int lk = 1; lk < L; ++lk) { xh[lk] = h->xh[lk].p; yh[lk] = h->yh[lk].p; }
+            h2_up(h, x, ldx, 1, xh, L - 1, s);
+        }
+        h2sym_apply(h, x, y, xh, yh, s);
+        if (L > 1) h2_down(h, yh, L - 1, y, ldy, 1, s);
+        return;
+    }
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
-    const bool use_store = (k == 1 && h->stored_mode == 1);
-    if (use_store && h->stores.size() < (size_t)L) h->stores.resize(L);
     // near field
     {
         std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
         near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
-        kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries, use_store ? &h->stores[0] : nullptr);
+        kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
     }
     if (L == 1) return;
     ensure_ws(h, k, s);
@@ -559,7 +565,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             tg.e_end = (int)entries.size();
             targets.push_back(tg);
         }
-        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries, use_store ? &h->stores[lk] : nullptr);
+        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries);
     }
     h2_down(h, yh, L - 1, y, ldy, k, s);
 }

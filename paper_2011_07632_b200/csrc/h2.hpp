@@ -20,6 +20,24 @@ struct H2Level {
 
 struct Timer;
 
+// symmetric stored blocks for k = 1 products (h2sym.cu)
+constexpr int SYM_MAX_SLOTS = 32;
+struct SymBuild { const double* tx; const double* sx; int64_t tds, sds, tid0, sid0; int nr, nb; int64_t vbase; };
+struct SymPiece { int64_t vbase, xa_off, xb_off, fwd, trn; int slot, nr, nb; };
+struct SymGNode { int slot, n; int64_t off; int c0, c1; };
+struct SymContrib { int64_t soff; int ro, len; };
+struct SymVecs { const double* p[SYM_MAX_SLOTS]; };
+struct SymVecsOut { double* p[SYM_MAX_SLOTS]; };
+struct H2SymStore {
+    DBuf<double> vals, scratch;
+    DBuf<SymPiece> pieces;
+    DBuf<SymGNode> gnodes;
+    DBuf<SymContrib> gcon;
+    int npieces = 0, ngnodes = 0;
+    double flops = 0, bytes = 0;
+    bool built = false;
+};
+
 }  // namespace spd
 
 struct spd_h2_s {
@@ -43,9 +61,9 @@ struct spd_h2_s {
     spd::DBuf<double> xt, yt;
     std::vector<spd::DBuf<double>> xh, yh;
     spd_comm_t comm = nullptr;
-    // stored blocks for k = 1 applies: [0] near field, [l] Type-3 couplings of level l
+    // stored symmetric blocks for k = 1 applies (near field + Type-3 couplings, h2sym.cu)
     int stored_mode = -1;          // -1 undecided, 0 on the fly, 1 stored
-    std::vector<spd::KbStore> stores;
+    spd::H2SymStore sym;
 };
 
 namespace spd {
@@ -61,6 +79,10 @@ void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::ve
            cudaStream_t s);
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
              cudaStream_t s);
+size_t h2sym_bytes(const spd_h2_s* h);
+void h2sym_build(spd_h2_s* h, cudaStream_t s);
+void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<double*>& xh,
+                 const std::vector<double*>& yh, cudaStream_t s);
 // proxy points of heap node `node` into P_dev (d x n_proxy SoA)
 void proxies_for_node(spd_h2_s* h, int node, double* P_dev, cudaStream_t s);
 }  // namespace spd

@@ -51,6 +51,9 @@ struct spd_hss_s {
 
 namespace spd {
 void hss_build_impl(spd_hss_s* H, const double* omega, uint64_t seed, cudaStream_t s);
+// k = 1 fused per-level solve (hsolve.cu); z: N workspace, zl[l] / ub[l]: level workspaces
+void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
+                   const std::vector<double*>& ub, cudaStream_t s);
 void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64_t ldx, int k, cudaStream_t s);
 void hss_query(const spd_hss_s* H, int what, void* buf, size_t bytes);
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,

@@ -260,148 +260,13 @@ static void kblock_vec(cudaStream_t s, const KernelParams& kp, double shift, int
     SPD_LAUNCH();
 }
 
-// ---------------------------------------------------------------- stored blocks
-// layout: for target t, row tile rt (32 rows), entry e of t: n_src x 32 doubles
-// (column c holds K(rows of the tile, source point c)), zero rows past the target.
-struct KsWork { int target, tile; int64_t base; };
-
-template <int KID>
-__global__ void __launch_bounds__(256) kstore_build_kernel(KernelParams kp, double shift, const KbBlock* __restrict__ blocks,
-                                                           const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
-                                                           const int64_t* __restrict__ eoff, const KsWork* __restrict__ work,
-                                                           double* __restrict__ vals, int d) {
-    const KsWork wk = work[blockIdx.x];
-    const KbTarget tg = targets[wk.target];
-    const KbBlock tb = blocks[tg.blk];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row = wk.tile * 32 + lane;
-    const bool valid = row < tb.n;
-    double rx[3] = {0.0, 0.0, 0.0};
-    if (valid) for (int a = 0; a < d; ++a) rx[a] = tb.x[(size_t)a * tb.ds + row];
-    const int64_t rid = tb.id0 >= 0 ? tb.id0 + row : -1;
-    for (int e = tg.e_begin; e < tg.e_end; ++e) {
-        const KbBlock sb = blocks[entries[e].src];
-        double* out = vals + wk.base + eoff[e];
-        const bool sh = shift != 0.0 && rid >= 0 && sb.id0 >= 0;
-        for (int c = warp; c < sb.n; c += 8) {
-            double r2 = 0.0;
-            for (int a = 0; a < d; ++a) { const double df = rx[a] - sb.x[(size_t)a * sb.ds + c]; r2 += df * df; }
-            double kv = kval<KID>(kp, r2);
-            if (sh && rid == sb.id0 + c) kv += shift;
-            out[(size_t)c * 32 + lane] = valid ? kv : 0.0;
-        }
-    }
-}
-
-// The stored blocks of one (target, 32-row tile) are contiguous: (sum_e n_src) x 32.
-// The 8 warps split that column range evenly (crossing entry boundaries), lane =
-// row, so every warp streams the same number of bytes; one output group per target.
-__global__ void __launch_bounds__(256) kstore_apply_kernel(const KbBlock* __restrict__ blocks, const KbTarget* __restrict__ targets,
-                                                           const KbEntry* __restrict__ entries, const int64_t* __restrict__ eoff,
-                                                           const KsWork* __restrict__ work, const double* __restrict__ vals) {
-    __shared__ double red[8][32];
-    const KsWork wk = work[blockIdx.x];
-    const KbTarget tg = targets[wk.target];
-    const KbBlock tb = blocks[tg.blk];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int row = wk.tile * 32 + lane;
-    const int ne = tg.e_end - tg.e_begin;
-    const int64_t ctot = (eoff[tg.e_end - 1] + 32LL * blocks[entries[tg.e_end - 1].src].n) / 32;
-    const int64_t cb = ctot * warp / 8, ce = ctot * (warp + 1) / 8;
-    // locate the entry holding column cb
-    int e = tg.e_begin;
-    while (e + 1 < tg.e_end && eoff[e + 1] / 32 <= cb) ++e;
-    (void)ne;
-    const double* v = vals + wk.base + lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t c = cb;
-    while (c < ce) {
-        const int64_t e0 = eoff[e] / 32;
-        const int ns = blocks[entries[e].src].n;
-        const int64_t cend = min(ce, e0 + ns);
-        const double* x = entries[e].X - e0;          // x[c] for global column c
-        for (; c + 4 <= cend; c += 4) {
-            a0 += __ldg(v + c * 32) * __ldg(x + c);
-            a1 += __ldg(v + (c + 1) * 32) * __ldg(x + c + 1);
-            a2 += __ldg(v + (c + 2) * 32) * __ldg(x + c + 2);
-            a3 += __ldg(v + (c + 3) * 32) * __ldg(x + c + 3);
-        }
-        for (; c < cend; ++c) a0 += __ldg(v + c * 32) * __ldg(x + c);
-        ++e;
-    }
-    red[warp][lane] = (a0 + a1) + (a2 + a3);
-    __syncthreads();
-    if (warp == 0 && row < tb.n) {
-        double sum = 0.0;
-        for (int w = 0; w < 8; ++w) sum += red[w][lane];
-        entries[tg.e_begin].Y[row] += sum;
-    }
-}
-
-static int64_t store_layout(const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
-                            const std::vector<KbEntry>& entries, std::vector<int64_t>& eoff, std::vector<KsWork>& work) {
-    eoff.assign(entries.size(), 0);
-    work.clear();
-    int64_t base = 0;
-    for (int t = 0; t < (int)targets.size(); ++t) {
-        const KbTarget& tg = targets[t];
-        if (tg.e_end <= tg.e_begin) continue;
-        int64_t per_tile = 0;
-        for (int e = tg.e_begin; e < tg.e_end; ++e) { eoff[e] = per_tile; per_tile += 32LL * blocks[entries[e].src].n; }
-        for (int rt = 0; rt < ceil_div(blocks[tg.blk].n, 32); ++rt) { work.push_back({t, rt, base}); base += per_tile; }
-    }
-    return base;
-}
-
-size_t kblock_store_bytes(const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
-                          const std::vector<KbEntry>& entries) {
-    std::vector<int64_t> eoff;
-    std::vector<KsWork> work;
-    return 8 * (size_t)store_layout(blocks, targets, entries, eoff, work);
-}
-
 void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
                   const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
-                  const std::vector<KbEntry>& entries, KbStore* store) {
+                  const std::vector<KbEntry>& entries) {
     {
         int maxc = 0;
         for (auto& e : entries) maxc = std::max(maxc, e.ncols);
         if (maxc == 0) return;
-        bool single_group = true;
-        for (const auto& tg : targets)
-            for (int e = tg.e_begin + 1; e < tg.e_end; ++e)
-                if (entries[e].Y != entries[tg.e_begin].Y) single_group = false;
-        if (store && maxc == 1 && single_group) {
-            std::vector<int64_t> eoff;
-            std::vector<KsWork> work;
-            const int64_t total = store_layout(blocks, targets, entries, eoff, work);
-            if (work.empty()) return;
-            DevArray<KbBlock> db(s, blocks);
-            DevArray<KbTarget> dt(s, targets);
-            DevArray<KbEntry> de(s, entries);
-            DevArray<int64_t> dof(s, eoff);
-            DevArray<KsWork> dw(s, work);
-            if (!store->built) {
-                store->vals.alloc(std::max<int64_t>(1, total));
-                ProfScope prof(s, "kstore_build", 0, 8.0 * total);
-                const unsigned nb = (unsigned)work.size();
-                switch (kp.id) {
-                case SPD_K_GAUSSIAN: kstore_build_kernel<SPD_K_GAUSSIAN><<<nb, 256, 0, s>>>(kp, shift, db.p, dt.p, de.p, dof.p, dw.p, store->vals.p, d); break;
-                case SPD_K_MATERN32: kstore_build_kernel<SPD_K_MATERN32><<<nb, 256, 0, s>>>(kp, shift, db.p, dt.p, de.p, dof.p, dw.p, store->vals.p, d); break;
-                case SPD_K_EXPONENTIAL: kstore_build_kernel<SPD_K_EXPONENTIAL><<<nb, 256, 0, s>>>(kp, shift, db.p, dt.p, de.p, dof.p, dw.p, store->vals.p, d); break;
-                default: kstore_build_kernel<SPD_K_IMQ><<<nb, 256, 0, s>>>(kp, shift, db.p, dt.p, de.p, dof.p, dw.p, store->vals.p, d); break;
-                }
-                SPD_LAUNCH();
-                store->built = true;
-            }
-            double fl = 0, by = 8.0 * total;
-            for (const auto& tg : targets)
-                for (int e = tg.e_begin; e < tg.e_end; ++e) fl += 2.0 * blocks[tg.blk].n * blocks[entries[e].src].n;
-            ProfScope prof(s, "kstore_gemv", fl, by);
-            kstore_apply_kernel<<<(unsigned)work.size(), 256, 0, s>>>(db.p, dt.p, de.p, dof.p, dw.p, store->vals.p);
-            SPD_LAUNCH();
-            return;
-        }
         if (maxc <= 4) { kblock_vec(s, kp, shift, d, blocks, targets, entries, maxc); return; }
     }
     int maxc_all = 0;

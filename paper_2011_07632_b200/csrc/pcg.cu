@@ -105,6 +105,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     // private non-blocking stream (graph capture is illegal on the legacy stream)
     cudaStream_t s;
     SPD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    AllocStreamScope alloc_scope(s);           // workspaces are stream-ordered on s
     cudaEvent_t ev;
     SPD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     SPD_CUDA(cudaEventRecord(ev, user));
@@ -147,6 +148,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     h2_prepare(A, 1, s);
     h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);     // builds stored k=1 blocks outside the graph
     bool use_graph = maxit > 1;
+    long long graph_kernels = 0;          // kernel nodes per replay (launch accounting)
     DescArena arena((size_t)64 << 20);
     if (use_graph) {
         try {
@@ -157,6 +159,15 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             catch (...) { cudaGraph_t g; cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g); throw; }
             SPD_CUDA(cudaStreamEndCapture(s, &cl.g));
             SPD_CUDA(cudaGraphInstantiate(&cl.ge, cl.g, 0));
+            size_t nn = 0;
+            SPD_CUDA(cudaGraphGetNodes(cl.g, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            if (nn) SPD_CUDA(cudaGraphGetNodes(cl.g, nodes.data(), &nn));
+            for (auto nd : nodes) {
+                cudaGraphNodeType ty;
+                SPD_CUDA(cudaGraphNodeGetType(nd, &ty));
+                if (ty == cudaGraphNodeTypeKernel) ++graph_kernels;
+            }
             cl.pc = prof_capture_take(mark);
             desc_arena() = nullptr;
         } catch (const Error&) {
@@ -168,7 +179,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     for (int it = 1; it <= maxit; ++it) {
         if (use_graph) {
             SPD_CUDA(cudaGraphLaunch(cl.ge, s));
-            count_launch();
+            count_launches(graph_kernels);
         } else {
             iteration_body(A, M, x, w, N, s);
         }

@@ -1,5 +1,8 @@
 // prof.cpp -- launch counter and per-kernel-class event timing (instrumentation).
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -10,6 +13,7 @@ namespace spd {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 struct Rec { std::string name; double flops, bytes; cudaEvent_t a, b; };
@@ -41,6 +45,33 @@ void drain() {       // caller holds the mutex
     g_recs.clear();
 }
 }  // namespace
+
+// stage marks (env SPD_STAGES=1): synchronize and print the wall time since the last mark
+void stage_mark(cudaStream_t s, const char* name, int level) {
+    static const bool on = getenv("SPD_STAGES") != nullptr;
+    static double last = 0.0;
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (name) fprintf(stderr, "[stage] %-24s L%-2d %9.3f ms\n", name, level, last > 0.0 ? (t - last) * 1e3 : 0.0);
+    last = t;
+}
+
+cudaStream_t& alloc_stream() {
+    static thread_local cudaStream_t st = nullptr;
+    return st;
+}
+void init_mem_pool() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) { cudaGetLastError(); return; }
+        uint64_t thr = (uint64_t)24 << 30;     // keep up to 24 GB cached between calls
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    });
+}
 
 DescArena*& desc_arena() {
     static thread_local DescArena* a = nullptr;

@@ -353,11 +353,13 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     }
     // ---------------- P:1009  all Y^(k)
     DBuf<double> Y;
+    stage_mark(s, nullptr);
     lca_bucketed_products(H, om, Y, s);
     auto Yk = [&](int k) { return Y.p + (size_t)(k - 1) * N * w; };
     SPD_CUDA(cudaStreamSynchronize(s));
     const double t1 = now_s();
     H->timings[0] = t1 - t0;
+    stage_mark(s, "hss Y products");
 
     // ---------------- leaf level
     HssLevel& l1 = H->lv[1];
@@ -448,6 +450,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     SPD_CUDA(cudaStreamSynchronize(s));
     const double t2 = now_s();
     H->timings[1] = t2 - t1;
+    stage_mark(s, "hss leaf level");
 
     // ---------------- levels k = 2..L (k = L: root factor only)
     for (int k = 2; k <= L; ++k) {
@@ -615,11 +618,13 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         for (int kp2 = k + 1; kp2 < L; ++kp2) std::swap(Tprev[kp2], Tcur[kp2]);
         Tprev[k].release();
         SPD_CUDA(cudaStreamSynchronize(s));
+        stage_mark(s, "hss level", k);
     }
     // solve factors: explicit S_i^{-1}, F_i^{-1} (triangular inverses by blocked TRSM on I),
     // so every step of hss_solve is an HBM-bound GEMV
     for (int k = 1; k <= L; ++k) invert_factors(s, H->lv[k]);
     SPD_CUDA(cudaStreamSynchronize(s));
+    stage_mark(s, "hss invert factors");
     H->timings[2] = now_s() - t2;
     H->timings[3] = now_s() - t0;
 }
@@ -653,6 +658,13 @@ void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64
     }
     ensure_solve_ws(H, k);
     double* z = H->bt.p;                               // N x k workspace (ld N)
+    if (k == 1 && !getenv("SPD_SOLVE_GEMV")) {         // fused per-level single-vector path (hsolve.cu)
+        std::vector<double*> zl(L + 1, nullptr), ubl(L + 1, nullptr);
+        for (int l = 1; l < L; ++l) zl[l] = H->z[l].p;
+        for (int l = 2; l <= L; ++l) ubl[l] = H->ub[l].p;
+        hss_solve_vec(H, b, x, z, zl, ubl, s);
+        return;
+    }
     const HssLevel& l1 = H->lv[1];
     // up, leaf: z = S^{-1} b ; zh = V^T z ; z <- z - V zh
     {
