@@ -125,6 +125,7 @@ struct IdDesc {
     const double* Mt; int ldm;   // R11 | T in the top rows (after qrcp + trsm)
     const int* piv; int s, nc;
     double* E;                   // nc x s (ld nc)
+    double* T;                   // s x (nc - s) (ld s)
     const int* cand_ids; int64_t cand_base;   // ids = cand_ids[c] or cand_base + c
     int* skel;                   // s tree positions
     double* skelX; int64_t sds;  // skeleton coords (stride sds)
@@ -143,7 +144,9 @@ __global__ void build_id_kernel(const IdDesc* descs, const double* X, int64_t N,
     }
     for (int64_t e = threadIdx.x; e < (int64_t)(nc - s) * s; e += blockDim.x) {
         int k = (int)(e % s), c = (int)(e / s);
-        id.E[id.piv[s + c] + (size_t)k * nc] = id.Mt[k + (size_t)(s + c) * id.ldm];
+        const double v = id.Mt[k + (size_t)(s + c) * id.ldm];
+        id.E[id.piv[s + c] + (size_t)k * nc] = v;
+        id.T[e] = v;
     }
 }
 
@@ -257,7 +260,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         // final outputs need ranks: keep each chunk's Mt until E is built
         std::vector<int> rank_h(lv.count, 0);
         // E, skel built per chunk into temporaries, then packed
-        struct Pending { int a; DBuf<double> E; DBuf<int> skel; DBuf<double> sx; };
+        struct Pending { int a; DBuf<double> E, T; DBuf<int> skel; DBuf<double> sx; };
         std::vector<Pending> pend;
         for (auto& ch : chunks) {
             std::vector<size_t> mt_off(ch.nodes.size() + 1, 0), p_off(ch.nodes.size() + 1, 0);
@@ -345,12 +348,14 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 pe.a = a;
                 const int sr = rank_h[a], nc = lv.ncand[a];
                 pe.E.alloc(std::max<int64_t>(1, (int64_t)nc * sr));
+                pe.T.alloc(std::max<int64_t>(1, (int64_t)(nc - sr) * sr));
                 pe.skel.alloc(std::max(1, sr));
                 pe.sx.alloc(std::max(1, sr * d));
                 IdDesc id;
                 id.Mt = Mt.p + mt_off[q]; id.ldm = n_p;
                 id.piv = piv_d.p + piv_off[a]; id.s = sr; id.nc = nc;
                 id.E = pe.E.p;
+                id.T = pe.T.p;
                 if (k == 1) { id.cand_ids = nullptr; id.cand_base = t.begin[i]; }
                 else { int c1 = 2 * i + 1 - prev->first; id.cand_ids = prev->skel.p + prev->off[c1]; id.cand_base = 0; }
                 id.skel = pe.skel.p;
@@ -376,12 +381,21 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         lv.E_off.assign(lv.count + 1, 0);
         for (int a = 0; a < lv.count; ++a) lv.E_off[a + 1] = lv.E_off[a] + (int64_t)lv.ncand[a] * lv.rank[a];
         lv.E.alloc(std::max<int64_t>(1, lv.E_off[lv.count]));
+        lv.T_off.assign(lv.count + 1, 0);
+        for (int a = 0; a < lv.count; ++a)
+            lv.T_off[a + 1] = lv.T_off[a] + (int64_t)(lv.ncand[a] - lv.rank[a]) * lv.rank[a];
+        lv.T.alloc(std::max<int64_t>(1, lv.T_off[lv.count]));
+        lv.piv_off = piv_off;
+        lv.piv = std::move(piv_d);
         lv.skel.alloc(std::max<int64_t>(1, lv.S));
         lv.skelX.alloc(std::max<int64_t>(1, lv.S * d));
         for (auto& pe : pend) {
             const int a = pe.a, sr = lv.rank[a];
             if (sr == 0) continue;
             SPD_CUDA(cudaMemcpyAsync(lv.E.p + lv.E_off[a], pe.E.p, sizeof(double) * lv.ncand[a] * sr, cudaMemcpyDeviceToDevice, s));
+            if (lv.ncand[a] > sr)
+                SPD_CUDA(cudaMemcpyAsync(lv.T.p + lv.T_off[a], pe.T.p, sizeof(double) * (lv.ncand[a] - sr) * sr,
+                                         cudaMemcpyDeviceToDevice, s));
             SPD_CUDA(cudaMemcpyAsync(lv.skel.p + lv.off[a], pe.skel.p, sizeof(int) * sr, cudaMemcpyDeviceToDevice, s));
             SPD_CUDA(cudaMemcpy2DAsync(lv.skelX.p + lv.off[a], sizeof(double) * lv.S, pe.sx.p, sizeof(double) * sr,
                                        sizeof(double) * sr, d, cudaMemcpyDeviceToDevice, s));
@@ -462,6 +476,7 @@ static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* 
 // up pass: xh[l] (S_l x k, ld S_l) = E^T [x_leaf | xh children], levels 1..top
 void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::vector<double*>& xh, int top,
            cudaStream_t s) {
+    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_up_vec(h, x, xh, top, s); return; }
     const TreeH& t = h->tree;
     for (int lk = 1; lk <= top; ++lk) {
         const H2Level& lv = h->lv[lk];
@@ -488,6 +503,7 @@ void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::ve
 // down pass: children of level-l nodes += E yh[l] for l = top..2; y_leaf += E yh[1]
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
              cudaStream_t s) {
+    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_down_vec(h, yh, top, y, s); return; }
     const TreeH& t = h->tree;
     for (int lk = top; lk >= 1; --lk) {
         const H2Level& lv = h->lv[lk];

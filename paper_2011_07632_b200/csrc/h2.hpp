@@ -16,6 +16,11 @@ struct H2Level {
     DBuf<double> skelX;           // d x S skeleton coordinates (SoA, stride S)
     std::vector<int64_t> E_off;   // offset of E_i (n_c x s_i, col-major) in E
     DBuf<double> E;               // leaf U_i / nonleaf R_i (interpolation matrices)
+    // the same interpolation matrices in ID form: E_i[piv[k], k] = 1 (k < s_i),
+    // E_i[piv[s_i + c], k] = T_i[k, c]; T_i is s_i x (n_c - s_i), col-major
+    std::vector<int64_t> T_off, piv_off;
+    DBuf<double> T;
+    DBuf<int> piv;                // n_c pivots per node (QRCP column order of the candidates)
 };
 
 struct Timer;
@@ -79,6 +84,9 @@ void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::ve
            cudaStream_t s);
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
              cudaStream_t s);
+// k = 1 basis passes in interpolative form (h2basis.cu)
+void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s);
+void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s);
 size_t h2sym_bytes(const spd_h2_s* h);
 void h2sym_build(spd_h2_s* h, cudaStream_t s);
 void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<double*>& xh,
