@@ -18,7 +18,11 @@ namespace spd {
 // ================================================================= GEMM
 constexpr int GT = 64, GK = 16;
 
-struct TileRef { int desc, tm, tn; };
+struct TileRef {
+    int desc, tm, tn;
+    int kb, ke;            // K range of this tile
+    double* P; int ldp;    // split-K: raw partial tile goes to P (ld ldp); nullptr: C = alpha acc + beta C
+};
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ descs,
@@ -39,6 +43,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     double ra[PT], rb[PT];
+    const int kend = tr.ke;
     auto load = [&](int k0) {
 #pragma unroll
         for (int u = 0; u < PT; ++u) {
@@ -46,15 +51,15 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
             int i, kk;
             if (TA) { kk = e % GK; i = e / GK; } else { i = e % GT; kk = e / GT; }
             const int gi = m0 + i, gk = k0 + kk;
-            ra[u] = (gi < d.m && gk < d.k) ? (TA ? __ldg(d.A + gk + (size_t)gi * d.lda) : __ldg(d.A + gi + (size_t)gk * d.lda)) : 0.0;
+            ra[u] = (gi < d.m && gk < kend) ? (TA ? __ldg(d.A + gk + (size_t)gi * d.lda) : __ldg(d.A + gi + (size_t)gk * d.lda)) : 0.0;
             int j, kb;
             if (TB) { j = e % GT; kb = e / GT; } else { kb = e % GK; j = e / GK; }
             const int gj = n0 + j, gkb = k0 + kb;
-            rb[u] = (gj < d.n && gkb < d.k) ? (TB ? __ldg(d.B + gj + (size_t)gkb * d.ldb) : __ldg(d.B + gkb + (size_t)gj * d.ldb)) : 0.0;
+            rb[u] = (gj < d.n && gkb < kend) ? (TB ? __ldg(d.B + gj + (size_t)gkb * d.ldb) : __ldg(d.B + gkb + (size_t)gj * d.ldb)) : 0.0;
         }
     };
-    load(0);
-    for (int k0 = 0; k0 < d.k; k0 += GK) {
+    load(tr.kb);
+    for (int k0 = tr.kb; k0 < kend; k0 += GK) {
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < PT; ++u) {
@@ -63,7 +68,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
             if (TB) Bs[e / GT][e % GT] = rb[u]; else Bs[e % GK][e / GK] = rb[u];
         }
         __syncthreads();
-        if (k0 + GK < d.k) load(k0 + GK);                 // prefetch the next chunk
+        if (k0 + GK < kend) load(k0 + GK);                 // prefetch the next chunk
 #pragma unroll
         for (int ks = 0; ks < GK / 4; ++ks) {
             double af[4], bf[4];
@@ -86,8 +91,12 @@ __global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ 
                 int i = m0 + wm * 32 + a * 8 + g;
                 int j = n0 + wn * 32 + b * 8 + 2 * q + h;
                 if (i < d.m && j < d.n) {
-                    double* c = d.C + i + (size_t)j * d.ldc;
-                    *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[a][b][h];
+                    if (tr.P) {
+                        tr.P[i + (size_t)j * tr.ldp] = acc[a][b][h];
+                    } else {
+                        double* c = d.C + i + (size_t)j * d.ldc;
+                        *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[a][b][h];
+                    }
                 }
             }
 }
@@ -184,6 +193,22 @@ __global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ 
     }
 }
 
+// split-K epilogue: C = alpha sum_s P_s + beta C, slices added in order
+struct ReduceDesc { int desc, S; int64_t off; };
+__global__ void gemm_reduce_kernel(const GemmDesc* __restrict__ descs, const ReduceDesc* __restrict__ red,
+                                   const double* __restrict__ part, double alpha, double beta) {
+    const ReduceDesc r = red[blockIdx.y];
+    const GemmDesc d = descs[r.desc];
+    const int64_t mn = (int64_t)d.m * d.n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int q = 0; q < r.S; ++q) acc += part[r.off + q * mn + e];
+        const int i = (int)(e % d.m), j = (int)(e / d.m);
+        double* c = d.C + i + (size_t)j * d.ldc;
+        *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc;
+    }
+}
+
 static void gemv_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, double alpha, double beta) {
     std::vector<int2> work;
     double fl = 0, by = 0;
@@ -219,14 +244,47 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         for (auto& g : d) nmax = std::max(nmax, g.n);
         if (nmax <= 4) { gemv_batched(s, d, transA, alpha, beta); return; }
     }
+    // output tiles; when they are too few to fill the GPU and K is long (the tall
+    // skinny V^T A of the blocked QR), K is split into S slices whose raw partial
+    // tiles are summed in slice order by gemm_reduce_kernel (deterministic)
+    long long ntiles = 0;
+    int kmax = 0;
+    for (const auto& g : d) {
+        if (g.m <= 0 || g.n <= 0) continue;
+        ntiles += (long long)ceil_div(g.m, GT) * ceil_div(g.n, GT);
+        kmax = std::max(kmax, g.k);
+    }
+    int S = 1;
+    if (ntiles > 0 && ntiles < 2 * 148 && kmax >= 8 * 64)
+        S = (int)std::max<long long>(1, std::min<long long>(kmax / 256, (4 * 148 + ntiles - 1) / ntiles));
     std::vector<TileRef> tiles;
+    std::vector<ReduceDesc> red;
+    size_t poff = 0;
     for (int i = 0; i < (int)d.size(); ++i) {
         if (d[i].m <= 0 || d[i].n <= 0) continue;
         if (d[i].k <= 0 && beta == 1.0) continue;
-        for (int tn = 0; tn < ceil_div(d[i].n, GT); ++tn)
-            for (int tm = 0; tm < ceil_div(d[i].m, GT); ++tm) tiles.push_back({i, tm, tn});
+        const int Si = (S > 1 && d[i].k >= 8 * 64) ? std::min(S, ceil_div(d[i].k, 128)) : 1;
+        const int kc = Si > 1 ? ceil_div(ceil_div(d[i].k, Si), GK) * GK : std::max(d[i].k, 0);
+        const int Seff = Si > 1 ? ceil_div(d[i].k, kc) : 1;
+        for (int ks = 0; ks < Seff; ++ks)
+            for (int tn = 0; tn < ceil_div(d[i].n, GT); ++tn)
+                for (int tm = 0; tm < ceil_div(d[i].m, GT); ++tm) {
+                    TileRef tr{i, tm, tn, ks * kc, std::min(d[i].k, (ks + 1) * kc), nullptr, d[i].m};
+                    if (Seff > 1) tr.P = (double*)(uintptr_t)(poff + (size_t)ks * d[i].m * d[i].n + 1);  // offset+1, patched below
+                    tiles.push_back(tr);
+                }
+        if (Seff > 1) {
+            red.push_back({i, Seff, (int64_t)poff});
+            poff += (size_t)Seff * d[i].m * d[i].n;
+        }
     }
     if (tiles.empty()) return;
+    DBuf<double> part;
+    if (poff) {
+        part.alloc(poff);
+        for (auto& tr : tiles)
+            if (tr.P) tr.P = part.p + ((size_t)(uintptr_t)tr.P - 1);
+    }
     double fl = 0, by = 0;
     for (auto& g : d) if (g.m > 0 && g.n > 0 && g.k > 0) {
         fl += 2.0 * g.m * g.n * g.k;
@@ -234,13 +292,21 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     }
     DevArray<GemmDesc> dd(s, d);
     DevArray<TileRef> dt(s, tiles);
-    ProfScope prof(s, "gemm_dmma", fl, by);
-    for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
-        unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
-        if (!transA && !transB) gemm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-        else if (transA && !transB) gemm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-        else if (!transA && transB) gemm_kernel<false, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-        else gemm_kernel<true, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+    {
+        ProfScope prof(s, "gemm_dmma", fl, by);
+        for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
+            unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
+            if (!transA && !transB) gemm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+            else if (transA && !transB) gemm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+            else if (!transA && transB) gemm_kernel<false, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+            else gemm_kernel<true, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
+            SPD_LAUNCH();
+        }
+    }
+    if (!red.empty()) {
+        DevArray<ReduceDesc> dr(s, red);
+        ProfScope prof(s, "gemm_reduce", 0, 8.0 * poff);
+        gemm_reduce_kernel<<<dim3(16, (unsigned)red.size()), 256, 0, s>>>(dd.p, dr.p, part.p, alpha, beta);
         SPD_LAUNCH();
     }
 }
@@ -834,8 +900,8 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
 // barriers exchange partial sums through DSMEM (summed in rank order, so
 // every CTA derives bit-identical reflectors).
 namespace cg = cooperative_groups;
-constexpr int QCL = 8;
 
+template <int QCL>
 __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
     cg::cluster_group cluster = cg::this_cluster();
     const int g = (int)cluster.block_rank();
@@ -871,12 +937,16 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
             part[0][1] = (j >= r0 && j < r0 + nr) ? col[j - r0] : 0.0;
         }
         cluster.sync();
+        // lane q reads CTA q's partials; the xor-butterfly sum is bitwise identical in
+        // every lane, warp and CTA (commutative pairwise adds), so all CTAs agree
         double sig = 0.0, x0 = 0.0;
-        for (int q = 0; q < QCL; ++q) {
-            const double* rp_ = cluster.map_shared_rank(&part[0][0], q);
-            sig += rp_[0];
-            x0 += rp_[1];
+        if (lane < QCL) {
+            const double* rp_ = cluster.map_shared_rank(&part[0][0], lane);
+            sig = rp_[0];
+            x0 = rp_[1];
         }
+        sig = warp_sum(sig);
+        x0 = warp_sum(x0);
         double beta, mu, v0;
         if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
         else {
@@ -909,9 +979,8 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
         }
         cluster.sync();
         for (int c = j + 1 + warp; c < jb; c += 8) {
-            double w = 0.0;
-            for (int q = 0; q < QCL; ++q) w += cluster.map_shared_rank(&part[1][0], q)[c];
-            w *= beta;
+            double w = lane < QCL ? cluster.map_shared_rank(&part[1][0], lane)[c] : 0.0;
+            w = warp_sum(w) * beta;
             double* cc = sm + c * rp;
             for (int i = lane; i < nr; i += 32) {
                 const int gi = r0 + i;
@@ -1003,26 +1072,31 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
             double pb = 0;
             int Lmax = 0;
             for (auto& q : pd) { pb += 8.0 * (q.m - q.p) * q.jb * (q.jb + 2); Lmax = std::max(Lmax, q.m - q.p); }
-            const int rp = ceil_div(Lmax, QCL);
+            // cluster of 8 CTAs (portable) when the panel slice fits 180 KB, else 16 (non-portable)
+            const int qcl = ceil_div(Lmax, 8) * QB * (int)sizeof(double) <= 180 * 1024 ? 8 : 16;
+            const int rp = ceil_div(Lmax, qcl);
             const size_t sh = (size_t)rp * QB * sizeof(double);
             ProfScope prof(s, "qr_panel", 0, pb);
             if (sh <= 180 * 1024) {
                 static bool attr = false;
                 if (!attr) {
-                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                     attr = true;
                 }
                 cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3((unsigned)pd.size() * QCL);
+                cfg.gridDim = dim3((unsigned)pd.size() * qcl);
                 cfg.blockDim = dim3(256);
                 cfg.dynamicSmemBytes = sh;
                 cfg.stream = s;
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
-                at[0].val.clusterDim.x = QCL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                at[0].val.clusterDim.x = qcl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel, (const PanelDesc*)dp.p, rp));
+                if (qcl == 8) SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<8>, (const PanelDesc*)dp.p, rp));
+                else SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<16>, (const PanelDesc*)dp.p, rp));
                 count_launch();
             } else {
                 panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);

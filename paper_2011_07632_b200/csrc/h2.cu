@@ -439,13 +439,16 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
 void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     if (h->tree.L > 1) ensure_ws(h, k, s);
     if (k != 1 || h->stored_mode != -1) return;
-    // stored symmetric k=1 blocks if they need < 40% of the free device memory (env SPD_STORED=0/1 overrides)
+    // symmetric k=1 product; blocks stored up to 40% of the free device memory, the rest
+    // evaluated on the fly (env SPD_STORED=0: legacy per-level on-the-fly path; =1: store all)
     const char* env = getenv("SPD_STORED");
     if (env && env[0] == '0') { h->stored_mode = 0; return; }
     const double need = (double)h2sym_bytes(h);
     size_t fr = 0, tot = 0;
     SPD_CUDA(cudaMemGetInfo(&fr, &tot));
-    h->stored_mode = (env && env[0] == '1') || need < 0.4 * (double)fr ? 1 : 0;
+    h->stored_mode = 1;
+    h->sym_budget = (env && env[0] == '1') ? need : std::min(need, 0.4 * (double)fr);
+    if (const char* b = getenv("SPD_SYM_BUDGET")) h->sym_budget = std::min(need, atof(b));   // bytes (tests)
 }
 
 // Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]
@@ -533,7 +536,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     const int64_t N = h->N;
     if (k == 1 && h->stored_mode == 1) {
         // stored symmetric blocks: up pass, near + all coupling levels in one launch, gather, down pass
-        h2sym_build(h, s);
+        h2sym_build(h, h->sym_budget, s);
         std::vector<double*> xh(L, nullptr), yh(L, nullptr);
         if (L > 1) {
             ensure_ws(h, 1, s);

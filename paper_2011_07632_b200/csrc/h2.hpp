@@ -28,7 +28,11 @@ struct Timer;
 // symmetric stored blocks for k = 1 products (h2sym.cu)
 constexpr int SYM_MAX_SLOTS = 32;
 struct SymBuild { const double* tx; const double* sx; int64_t tds, sds, tid0, sid0; int nr, nb; int64_t vbase; };
-struct SymPiece { int64_t vbase, xa_off, xb_off, fwd, trn; int slot, nr, nb; };
+struct SymPiece {
+    int64_t vbase, xa_off, xb_off, fwd, trn;   // vbase < 0: evaluated on the fly
+    int slot, nr, nb;
+    const double* tx; const double* sx; int64_t tds, sds, tid0, sid0;   // row / column points, ids (shift)
+};
 struct SymGNode { int slot, n; int64_t off; int c0, c1; };
 struct SymContrib { int64_t soff; int ro, len; };
 struct SymVecs { const double* p[SYM_MAX_SLOTS]; };
@@ -39,7 +43,7 @@ struct H2SymStore {
     DBuf<SymGNode> gnodes;
     DBuf<SymContrib> gcon;
     int npieces = 0, ngnodes = 0;
-    double flops = 0, bytes = 0;
+    double flops = 0, bytes = 0, stored_frac = 1.0;
     bool built = false;
 };
 
@@ -66,8 +70,10 @@ struct spd_h2_s {
     spd::DBuf<double> xt, yt;
     std::vector<spd::DBuf<double>> xh, yh;
     spd_comm_t comm = nullptr;
-    // stored symmetric blocks for k = 1 applies (near field + Type-3 couplings, h2sym.cu)
-    int stored_mode = -1;          // -1 undecided, 0 on the fly, 1 stored
+    // symmetric k = 1 product (near field + Type-3 couplings, h2sym.cu): blocks stored
+    // up to sym_budget bytes, the rest evaluated on the fly
+    int stored_mode = -1;          // -1 undecided, 0 old per-level path (tests), 1 symmetric
+    double sym_budget = 0.0;
     spd::H2SymStore sym;
 };
 
@@ -88,7 +94,7 @@ void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double*
 void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s);
 void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s);
 size_t h2sym_bytes(const spd_h2_s* h);
-void h2sym_build(spd_h2_s* h, cudaStream_t s);
+void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s);
 void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<double*>& xh,
                  const std::vector<double*>& yh, cudaStream_t s);
 // proxy points of heap node `node` into P_dev (d x n_proxy SoA)

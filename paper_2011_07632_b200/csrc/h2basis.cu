@@ -20,66 +20,90 @@ struct BasisItem {
     int s, nc, tile;      // tile: 32-row tile of xh (up) / 32-column tile of T (down)
 };
 
-// up: xh[k] = x[piv[k]] + sum_c T[k, c] x[piv[s + c]] for k in the tile; the 8 warps
-// split the columns c, partial sums reduced in warp order (deterministic)
-__global__ void __launch_bounds__(256) basis_up_kernel(const BasisItem* __restrict__ items) {
+constexpr int BV_T = 512, BV_W = BV_T / 32;
+
+// up: xh[k] = x[piv[k]] + sum_c T[k, c] x[piv[s + c]] for k in the tile (lane = k);
+// warp w takes columns c = w (mod 16), 8 loads in flight per lane; the warp sums
+// are added in warp order (deterministic)
+__global__ void __launch_bounds__(BV_T) basis_up_kernel(const BasisItem* __restrict__ items) {
     extern __shared__ double xg[];                // gathered x[piv[s + c]], c < n_c - s
-    __shared__ double red[8][32];
+    __shared__ double red[BV_W][32];
     const BasisItem it = items[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int s = it.s, nr = it.nc - it.s;
-    for (int c = threadIdx.x; c < nr; c += 256) xg[c] = it.in[it.piv[s + c]];
+    for (int c = threadIdx.x; c < nr; c += BV_T) xg[c] = it.in[it.piv[s + c]];
     __syncthreads();
     const int k = it.tile * 32 + lane;
-    const int cw = (nr + 7) / 8, cb = warp * cw, ce = min(nr, cb + cw);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
     if (k < s) {
         const double* p = it.T + k;
-        int c = cb;
-        for (; c + 4 <= ce; c += 4) {
-            a0 += __ldg(p + (size_t)c * s) * xg[c];
-            a1 += __ldg(p + (size_t)(c + 1) * s) * xg[c + 1];
-            a2 += __ldg(p + (size_t)(c + 2) * s) * xg[c + 2];
-            a3 += __ldg(p + (size_t)(c + 3) * s) * xg[c + 3];
+        int c = warp;
+        for (; c + 7 * BV_W < nr; c += 8 * BV_W) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (size_t)(c + u * BV_W) * s);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] += v[u] * xg[c + u * BV_W];
         }
-        for (; c < ce; ++c) a0 += __ldg(p + (size_t)c * s) * xg[c];
+        for (; c < nr; c += BV_W) acc[0] += __ldg(p + (size_t)c * s) * xg[c];
     }
-    red[warp][lane] = (a0 + a1) + (a2 + a3);
+    red[warp][lane] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     __syncthreads();
     if (warp == 0 && k < s) {
         double sum = it.in[it.piv[k]];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) sum += red[w][lane];
+        for (int w = 0; w < BV_W; ++w) sum += red[w][lane];
         it.out[k] = sum;
     }
 }
 
-// down: y[piv[s + c]] += sum_k T[k, c] yh[k] for the tile's 32 columns c (one warp per
-// column, lanes over k), and y[piv[k]] += yh[k] for k in [32 tile, 32 tile + 32)
-__global__ void __launch_bounds__(256) basis_down_kernel(const BasisItem* __restrict__ items) {
+// down: y[piv[s + c]] += sum_k T[k, c] yh[k] for the tile's 32 columns c, and
+// y[piv[k]] += yh[k] for k in [32 tile, 32 tile + 32).  Warp w takes the 32-row
+// chunks q = w (mod 16) of T's tile: 32 coalesced loads (lane = row), scaled by
+// yh, then a butterfly transpose-reduction leaves column c's partial in lane c.
+__global__ void __launch_bounds__(BV_T) basis_down_kernel(const BasisItem* __restrict__ items) {
     extern __shared__ double yh[];
+    __shared__ double red[BV_W][32];
     const BasisItem it = items[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int s = it.s, nr = it.nc - it.s;
-    for (int k = threadIdx.x; k < s; k += 256) yh[k] = it.in[k];
+    for (int k = threadIdx.x; k < s; k += BV_T) yh[k] = it.in[k];
     __syncthreads();
     const int k0 = it.tile * 32;
     if (warp == 0 && k0 + lane < s) it.out[it.piv[k0 + lane]] += yh[k0 + lane];
-    for (int cc = warp; cc < 32; cc += 8) {
-        const int c = k0 + cc;
-        if (c >= nr) break;
-        const double* p = it.T + (size_t)c * s;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int k = lane;
-        for (; k + 96 < s; k += 128) {
-            a0 += __ldg(p + k) * yh[k];
-            a1 += __ldg(p + k + 32) * yh[k + 32];
-            a2 += __ldg(p + k + 64) * yh[k + 64];
-            a3 += __ldg(p + k + 96) * yh[k + 96];
+    const int c0 = k0, cn = min(32, nr - c0);
+    if (cn <= 0) return;                         // whole CTA: no T columns in this tile
+    double acc = 0.0;
+    for (int q = warp; q * 32 < s; q += BV_W) {
+        const int k = q * 32 + lane;
+        const double y = k < s ? yh[k] : 0.0;
+        const double* p = it.T + k + (size_t)c0 * s;
+        double v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = (k < s && c < cn) ? __ldg(p + (size_t)c * s) : 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] *= y;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int j = 0; j < o; ++j) {
+                const double send = up ? v[j] : v[j + o];
+                const double keep = up ? v[j + o] : v[j];
+                v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
         }
-        for (; k < s; k += 32) a0 += __ldg(p + k) * yh[k];
-        const double v = warp_sum((a0 + a1) + (a2 + a3));
-        if (lane == 0) it.out[it.piv[s + c]] += v;
+        acc += v[0];
+    }
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && lane < cn) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < BV_W; ++w) sum += red[w][lane];
+        it.out[it.piv[s + c0 + lane]] += sum;
     }
 }
 
@@ -113,7 +137,7 @@ void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& x
         if (smem > 48 * 1024)
             SPD_CUDA(cudaFuncSetAttribute(basis_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         ProfScope prof(s, "basis_vec", 0, by);
-        basis_up_kernel<<<(unsigned)items.size(), 256, smem, s>>>(di.p);
+        basis_up_kernel<<<(unsigned)items.size(), BV_T, smem, s>>>(di.p);
         SPD_LAUNCH();
     }
 }
@@ -149,7 +173,7 @@ void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, dou
         if (smem > 48 * 1024)
             SPD_CUDA(cudaFuncSetAttribute(basis_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         ProfScope prof(s, "basis_vec", 0, by);
-        basis_down_kernel<<<(unsigned)items.size(), 256, smem, s>>>(di.p);
+        basis_down_kernel<<<(unsigned)items.size(), BV_T, smem, s>>>(di.p);
         SPD_LAUNCH();
     }
 }

@@ -3,10 +3,12 @@
 //
 // At k = 1 evaluating K on the fly is FP64-ALU bound (exp/sqrt per entry for two
 // useful flops), while a stored block is read once per product: HBM bound.  K is
-// symmetric, so only the blocks (a, b) with a <= b are stored: the near-field leaf
+// symmetric, so only the blocks (a, b) with a <= b are visited: the near-field leaf
 // blocks K(X_a, X_b) + sigma I and, per level, the Type-3 couplings
-// B^{H2}_ab = K(X_{J_a}, X_{J_b}) (eqn:uniformbasis_h2).  One stored block serves
-// y_a += K_ab x_b and y_b += K_ab^T x_a, which halves the bytes per product.
+// B^{H2}_ab = K(X_{J_a}, X_{J_b}) (eqn:uniformbasis_h2).  One block serves
+// y_a += K_ab x_b and y_b += K_ab^T x_a, which halves the bytes (stored) or the
+// kernel evaluations (on the fly) per product.  Blocks are stored while they fit
+// the memory budget; the rest are evaluated on the fly by the same kernel.
 //
 // Layout: a block is cut into 32-row tiles ("pieces"); a piece is 32 x n_b
 // doubles, column c holding K(rows of the tile, source point c) (rows past the
@@ -53,16 +55,26 @@ __global__ void __launch_bounds__(256) sym_build_kernel(KernelParams kp, double 
     }
 }
 
+template <int KID>
 __global__ void __launch_bounds__(SY_NW * 32) sym_apply_kernel(const SymPiece* __restrict__ pieces, SymVecs xin,
                                                                const double* __restrict__ vals,
-                                                               double* __restrict__ scratch) {
+                                                               double* __restrict__ scratch, KernelParams kp,
+                                                               double shift, int d) {
     __shared__ double red[SY_NW][32];
     const SymPiece pc = pieces[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* xs = xin.p[pc.slot];
     const bool trn = pc.trn >= 0;
     const double xa = (trn && lane < pc.nr) ? xs[pc.xa_off + lane] : 0.0;
-    const double* v = vals + pc.vbase + lane;
+    const bool stored = pc.vbase >= 0;
+    const double* v = vals + (stored ? pc.vbase : 0) + lane;
+    double rx0 = 0.0, rx1 = 0.0, rx2 = 0.0;     // on the fly: this lane's row point
+    if (!stored && lane < pc.nr) {
+        rx0 = pc.tx[lane];
+        if (d > 1) rx1 = pc.tx[pc.tds + lane];
+        if (d > 2) rx2 = pc.tx[2 * pc.tds + lane];
+    }
+    const bool sh = !stored && shift != 0.0 && pc.tid0 >= 0;
     double acc = 0.0;
     const int nch = (pc.nb + 31) >> 5;
     for (int ch = warp; ch < nch; ch += SY_NW) {
@@ -70,12 +82,31 @@ __global__ void __launch_bounds__(SY_NW * 32) sym_apply_kernel(const SymPiece* _
         const int cn = min(32, pc.nb - c0);
         const double xbv = lane < cn ? xs[pc.xb_off + c0 + lane] : 0.0;
         double kv[32];
-        if (cn == 32) {
+        if (stored) {
+            if (cn == 32) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) kv[c] = __ldg(v + (size_t)(c0 + c) * 32);
+                for (int c = 0; c < 32; ++c) kv[c] = __ldg(v + (size_t)(c0 + c) * 32);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) kv[c] = c < cn ? __ldg(v + (size_t)(c0 + c) * 32) : 0.0;
+            }
         } else {
+            // source point c0 + lane, broadcast by shuffles; rows past nr give 0
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            if (lane < cn) {
+                s0 = pc.sx[c0 + lane];
+                if (d > 1) s1 = pc.sx[pc.sds + c0 + lane];
+                if (d > 2) s2 = pc.sx[2 * pc.sds + c0 + lane];
+            }
 #pragma unroll
-            for (int c = 0; c < 32; ++c) kv[c] = c < cn ? __ldg(v + (size_t)(c0 + c) * 32) : 0.0;
+            for (int c = 0; c < 32; ++c) {
+                const double d0 = rx0 - __shfl_sync(0xffffffffu, s0, c);
+                const double d1 = rx1 - __shfl_sync(0xffffffffu, s1, c);
+                const double d2 = rx2 - __shfl_sync(0xffffffffu, s2, c);
+                double k = kval_sym<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
+                if (sh && pc.tid0 + lane == pc.sid0 + c0 + c) k += shift;
+                kv[c] = (c < cn && lane < pc.nr) ? k : 0.0;
+            }
         }
         double f0 = 0.0, f1 = 0.0;
 #pragma unroll
@@ -141,17 +172,18 @@ __global__ void __launch_bounds__(256) sym_gather_kernel(const SymGNode* __restr
 
 // ----------------------------------------------------------------- host side
 namespace {
-struct PlanBlock { int slot, a, b; };   // stored block (a <= b) of slot 0 (near, leaves) or level slot
+struct PlanBlock { int slot, a, b; };   // block (a <= b) of slot 0 (near, leaves) or level slot
 }
 
-static void sym_plan(const spd_h2_s* h, std::vector<SymBuild>* builds, std::vector<SymPiece>* pieces,
+// budget: doubles of stored blocks allowed (pieces past it are evaluated on the fly)
+static void sym_plan(const spd_h2_s* h, int64_t budget, std::vector<SymBuild>* builds, std::vector<SymPiece>* pieces,
                      std::vector<SymGNode>* gnodes, std::vector<SymContrib>* gcon, int64_t* nvals, int64_t* nscratch,
-                     double* flops) {
+                     double* flops, int64_t* nall) {
     const TreeH& t = h->tree;
     const int L = t.L, d = h->d;
     const int64_t N = h->N;
     (void)d;
-    int64_t vb = 0, sc = 0;
+    int64_t vb = 0, sc = 0, all = 0;
     double fl = 0.0;
     // per output node (slot, local index) and 32-row tile: list of contributions
     std::vector<std::vector<std::vector<std::vector<SymContrib>>>> con(L);
@@ -183,19 +215,23 @@ static void sym_plan(const spd_h2_s* h, std::vector<SymBuild>* builds, std::vect
         fl += 2.0 * na * nb * (diag ? 1.0 : 2.0);
         for (int r0 = 0; r0 < na; r0 += 32) {
             const int nr = std::min(32, na - r0);
-            if (builds)
+            const bool store = vb + 32LL * nb <= budget;
+            all += 32LL * nb;
+            if (builds && store)
                 builds->push_back({tx + r0, sx, ds, ds, slot == 0 ? tid0 + r0 : -1, slot == 0 ? sid0 : -1, nr, nb, vb});
             SymPiece pc;
-            pc.vbase = vb; pc.slot = slot; pc.nr = nr; pc.nb = nb;
+            pc.vbase = store ? vb : -1; pc.slot = slot; pc.nr = nr; pc.nb = nb;
+            pc.tx = tx + r0; pc.sx = sx; pc.tds = ds; pc.sds = ds;
+            pc.tid0 = slot == 0 ? tid0 + r0 : -1; pc.sid0 = slot == 0 ? sid0 : -1;
             pc.xa_off = xa0 + r0; pc.xb_off = xb0;
             pc.fwd = sc; sc += 32;
             pc.trn = diag ? -1 : sc;
             if (!diag) sc += nb;
             if (pieces) pieces->push_back(pc);
+            if (store) vb += 32LL * nb;
             con[slot][a][r0 / 32].push_back({pc.fwd, 0, nr});
             if (!diag)
                 for (int tb = 0; tb * 32 < nb; ++tb) con[slot][b][tb].push_back({pc.trn + 32 * tb, 0, std::min(32, nb - 32 * tb)});
-            vb += 32LL * nb;
         }
     };
     for (const auto& pr : h->lists.near)
@@ -226,24 +262,25 @@ static void sym_plan(const spd_h2_s* h, std::vector<SymBuild>* builds, std::vect
     *nvals = vb;
     *nscratch = sc;
     *flops = fl;
+    *nall = all;
 }
 
 size_t h2sym_bytes(const spd_h2_s* h) {
-    int64_t nv = 0, ns = 0;
+    int64_t nv = 0, ns = 0, na = 0;
     double fl = 0;
-    sym_plan(h, nullptr, nullptr, nullptr, nullptr, &nv, &ns, &fl);
-    return 8 * (size_t)(nv + ns);
+    sym_plan(h, 0, nullptr, nullptr, nullptr, nullptr, &nv, &ns, &fl, &na);
+    return 8 * (size_t)(na + ns);
 }
 
-void h2sym_build(spd_h2_s* h, cudaStream_t s) {
+void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
     H2SymStore& st = h->sym;
     if (st.built) return;
     std::vector<SymBuild> builds;
     std::vector<SymPiece> pieces;
     std::vector<SymGNode> gnodes;
     std::vector<SymContrib> gcon;
-    int64_t nv = 0, ns = 0;
-    sym_plan(h, &builds, &pieces, &gnodes, &gcon, &nv, &ns, &st.flops);
+    int64_t nv = 0, ns = 0, na = 0;
+    sym_plan(h, (int64_t)(budget_bytes / 8), &builds, &pieces, &gnodes, &gcon, &nv, &ns, &st.flops, &na);
     st.vals.alloc(std::max<int64_t>(1, nv));
     st.scratch.alloc(std::max<int64_t>(1, ns));
     st.pieces.upload(pieces, s);
@@ -252,6 +289,7 @@ void h2sym_build(spd_h2_s* h, cudaStream_t s) {
     st.npieces = (int)pieces.size();
     st.ngnodes = (int)gnodes.size();
     st.bytes = 8.0 * nv;
+    st.stored_frac = na ? (double)nv / (double)na : 1.0;
     if (!builds.empty()) {
         DevArray<SymBuild> db(s, builds);
         ProfScope prof(s, "sym_build", 0, 8.0 * nv);
@@ -284,8 +322,16 @@ void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<doub
     yout.p[0] = y;
     for (int l = 1; l < L; ++l) { xin.p[l] = xh[l]; yout.p[l] = yh[l]; }
     if (st.npieces) {
-        ProfScope prof(s, "sym_gemv", st.flops, st.bytes);
-        sym_apply_kernel<<<(unsigned)st.npieces, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p);
+        ProfScope prof(s, st.stored_frac >= 1.0 ? "sym_gemv" : "sym_gemv_eval", st.flops, st.bytes);
+        const unsigned nb = (unsigned)st.npieces;
+        const KernelParams& kp = h->kp;
+        const double sh = h->kern.shift;
+        switch (kp.id) {
+        case SPD_K_GAUSSIAN: sym_apply_kernel<SPD_K_GAUSSIAN><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
+        case SPD_K_MATERN32: sym_apply_kernel<SPD_K_MATERN32><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
+        case SPD_K_EXPONENTIAL: sym_apply_kernel<SPD_K_EXPONENTIAL><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
+        default: sym_apply_kernel<SPD_K_IMQ><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
+        }
         SPD_LAUNCH();
     }
     if (st.ngnodes) {

@@ -2,12 +2,13 @@
 //
 // The recursive solve of reading R12 ("ULV-style"):
 //   H^{-1} = S^{-T} [ (I - V V^T) + V (I + H_2)^{-1} V^T ] S^{-1},  recursively,
-// ending in (I + B_root)^{-1} = F_root^{-T} F_root^{-1}.  Per node and level the
-// three dependent products of the up sweep (u = F^{-1} w, zh = V^T u, u -= V zh)
-// and the two of the down sweep (t = u + V xh, out = F^{-T} t) run inside ONE CTA
-// with the vectors in shared memory, so one level is one launch (2L launches per
-// solve instead of 5L dependent GEMV launches).  The factors are read once per
-// product, lower triangles only (F^{-1} is lower triangular), coalesced.
+// ending in (I + B_root)^{-1} = F_root^{-T} F_root^{-1}.  With P = S^{-T} V (the
+// build's Phi^T; F^{-T} Vbar' above the leaves) the per-node work splits into two
+// products that do not depend on each other:
+//   up:    u0 = S^{-1} w,  zh = V^T S^{-1} w = P^T w
+//   down:  x  = S^{-T} (u0 - V zh + V xh) = S^{-T} u0 + P (xh - zh)
+// so each level is ONE launch with ONE round of independent loads per CTA (one CTA
+// per node, 16 warps; F^{-1} is read as a lower triangle), 2L launches per solve.
 // Summation order is fixed (no atomics): partial sums per (32-row tile, 32-column
 // chunk) are reduced in chunk order.
 #include "hss.hpp"
@@ -15,26 +16,26 @@
 
 namespace spd {
 
-constexpr int HS_T = 256, HS_W = HS_T / 32, HS_CC = 32, HS_MT = 10;   // m <= 32 * HS_MT
+constexpr int HS_T = 512, HS_W = HS_T / 32, HS_CC = 32, HS_MT = 10;   // m <= 32 * HS_MT
 
 struct HsNode {
     const double* F;   // m x m lower triangular (ld m): S_i^{-1} (leaf) / F_i^{-1}
-    const double* V;   // m x r (ld m): V_i / Vbar'_i
+    const double* P;   // m x r (ld m): S_i^{-T} V_i / F_i^{-T} Vbar'_i
     int m, r;
-    const double* in;  // up/root: w (m) ; down: u (m)
+    const double* in;  // up/root: w (m) ; down: u0 (m)
     const double* xh;  // down: coarse solution (r)
-    double* u;         // up: u (m)
-    double* zh;        // up: V^T u (r)
+    const double* zhi; // down: zh of the up sweep (r)
+    double* u;         // up: u0 (m)
+    double* zh;        // up: P^T w (r), input of the next level
+    double* zh2;       // up: copy of zh kept for the down sweep
     double* out;       // down/root: result (m)
 };
 
-// y[i] = s_i (mode 0) / y[i] - s_i (mode 1) / y[i] + s_i (mode 2),
-// s_i = sum_j A[i + j ld] x[j] over j < n (j <= i if lower).  Work items are
-// (32-row tile, 32-column chunk); a warp issues the chunk's 32 loads at once
-// (lane = row, coalesced 256-byte lines), partial sums per chunk go to `part`
-// and are added in chunk order.
-__device__ void cta_gemv_n(const double* __restrict__ A, int ld, int m, int n, bool lower, const double* x,
-                           double* y, double* part, int mode) {
+// Partial products of y = A x (y[i] = sum_j A[i + j ld] x[j], j < n, j <= i if lower).
+// Work items are (32-row tile, 32-column chunk); a warp issues the chunk's 32 loads
+// at once (lane = row, coalesced 256-byte lines) and writes part[cc * m + i].
+__device__ void cta_gemv_n_items(const double* __restrict__ A, int ld, int m, int n, bool lower, const double* x,
+                                 double* part) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nrt = (m + 31) >> 5, ncc = (n + HS_CC - 1) / HS_CC;
     for (int item = warp; item < nrt * ncc; item += HS_W) {
@@ -61,14 +62,14 @@ __device__ void cta_gemv_n(const double* __restrict__ A, int ld, int m, int n, b
         }
         if (i < m) part[cc * m + i] = a0 + a1;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < m; i += HS_T) {
-        const int ccmax = lower ? min(ncc, ((i | 31) / HS_CC) + 1) : ncc;
-        double s = 0.0;
-        for (int cc = 0; cc < ccmax; ++cc) s += part[cc * m + i];
-        y[i] = mode == 0 ? s : (mode == 1 ? y[i] - s : y[i] + s);
-    }
-    __syncthreads();
+}
+// (after a barrier) the row sums of the partials, in chunk order
+__device__ __forceinline__ double cta_gemv_n_row(const double* part, int m, int n, bool lower, int i) {
+    const int ncc = (n + HS_CC - 1) / HS_CC;
+    const int ccmax = lower ? min(ncc, ((i | 31) / HS_CC) + 1) : ncc;
+    double s = 0.0;
+    for (int cc = 0; cc < ccmax; ++cc) s += part[cc * m + i];
+    return s;
 }
 
 // y[j] = sum_i A[i + j ld] x[i] over i < m (i >= j if lower), j < n.  A warp takes
@@ -103,14 +104,13 @@ __device__ void cta_gemv_t(const double* __restrict__ A, int ld, int m, int n, b
             if (two) y[j + 1] = s1;
         }
     }
-    __syncthreads();
 }
 
-// mode 0: up    u = F w ; zh = V^T u ; u -= V zh     (writes u, zh)
-// mode 1: down  t = u + V xh ; out = F^T t
+// mode 0: up    u0 = F w ; zh = P^T w                      (writes u0, zh, zh2)
+// mode 1: down  out = F^T u0 + P (xh - zh)
 // mode 2: root  out = F^T (F w)
 template <int MODE>
-__global__ void __launch_bounds__(HS_T, 2) hss_level_kernel(const HsNode* __restrict__ nodes, int mmax) {
+__global__ void __launch_bounds__(HS_T, 1) hss_level_kernel(const HsNode* __restrict__ nodes, int mmax) {
     extern __shared__ double sm[];
     const HsNode nd = nodes[blockIdx.x];
     const int m = nd.m, r = nd.r;
@@ -120,21 +120,25 @@ __global__ void __launch_bounds__(HS_T, 2) hss_level_kernel(const HsNode* __rest
     double* part = zh + mmax;              // ceil(mmax/32) * mmax
     for (int i = threadIdx.x; i < m; i += HS_T) w[i] = nd.in[i];
     if (MODE == 1)
-        for (int i = threadIdx.x; i < r; i += HS_T) zh[i] = nd.xh[i];
+        for (int i = threadIdx.x; i < r; i += HS_T) zh[i] = nd.xh[i] - nd.zhi[i];
     __syncthreads();
     if (MODE == 0) {
-        cta_gemv_n(nd.F, m, m, m, true, w, u, part, 0);
-        if (r > 0) {
-            cta_gemv_t(nd.V, m, m, r, false, u, zh);
-            cta_gemv_n(nd.V, m, m, r, false, zh, u, part, 1);
-            for (int i = threadIdx.x; i < r; i += HS_T) nd.zh[i] = zh[i];
-        }
-        for (int i = threadIdx.x; i < m; i += HS_T) nd.u[i] = u[i];
+        cta_gemv_n_items(nd.F, m, m, m, true, w, part);
+        if (r > 0) cta_gemv_t(nd.P, m, m, r, false, w, zh);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += HS_T) nd.u[i] = cta_gemv_n_row(part, m, m, true, i);
+        for (int i = threadIdx.x; i < r; i += HS_T) { nd.zh[i] = zh[i]; nd.zh2[i] = zh[i]; }
     } else if (MODE == 1) {
-        if (r > 0) cta_gemv_n(nd.V, m, m, r, false, zh, w, part, 2);
-        cta_gemv_t(nd.F, m, m, m, true, w, nd.out);
+        if (r > 0) cta_gemv_n_items(nd.P, m, m, r, false, zh, part);
+        cta_gemv_t(nd.F, m, m, m, true, w, u);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += HS_T)
+            nd.out[i] = u[i] + (r > 0 ? cta_gemv_n_row(part, m, r, false, i) : 0.0);
     } else {
-        cta_gemv_n(nd.F, m, m, m, true, w, u, part, 0);
+        cta_gemv_n_items(nd.F, m, m, m, true, w, part);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += HS_T) u[i] = cta_gemv_n_row(part, m, m, true, i);
+        __syncthreads();
         cta_gemv_t(nd.F, m, m, m, true, u, nd.out);
     }
 }
@@ -150,7 +154,7 @@ static void launch_level(cudaStream_t s, const std::vector<HsNode>& nodes) {
     double by = 0;
     for (auto& n : nodes) {
         mmax = std::max(mmax, n.m);
-        by += 8.0 * (0.5 * n.m * (n.m + 1) * (MODE == 2 ? 2 : 1) + (double)n.m * n.r * (MODE == 0 ? 2 : 1) + 2.0 * n.m);
+        by += 8.0 * (0.5 * n.m * (n.m + 1) * (MODE == 2 ? 2 : 1) + (double)n.m * n.r + 2.0 * n.m + 2.0 * n.r);
     }
     const size_t smem = level_smem(mmax);
     SPD_REQUIRE(mmax <= 32 * HS_MT, "hss_solve: node too large for the fused k=1 solve");
@@ -162,20 +166,21 @@ static void launch_level(cudaStream_t s, const std::vector<HsNode>& nodes) {
     SPD_LAUNCH();
 }
 
-// x = H^{-1} b for one vector (tree order, contiguous), L >= 2
+// x = H^{-1} b for one vector (tree order, contiguous), L >= 2.  zl[l]: level-l
+// coefficients (zh up, xh down), zs[l]: zh kept for the down sweep, ub[l]: u0 of the
+// level-l nodes at their children's offsets (leaves: u0 in z).
 void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
-                   const std::vector<double*>& ub, cudaStream_t s) {
+                   const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s) {
     const spd_h2_s* h = H->h2;
     const TreeH& t = h->tree;
     const int L = t.L;
     const HssLevel& l1 = H->lv[1];
     std::vector<HsNode> nodes;
-    // up, leaves: u -> z, zh -> zl[1]
     for (int a = 0; a < l1.count; ++a) {
         const int64_t off = t.begin[l1.first + a];
         if (!l1.m[a]) continue;
-        nodes.push_back({l1.Finv.p + l1.F_off[a], l1.V.p + l1.V_off[a], l1.m[a], l1.rank[a], b + off, nullptr,
-                         z + off, zl[1] + l1.off[a], nullptr});
+        nodes.push_back({l1.Finv.p + l1.F_off[a], l1.P.p + l1.V_off[a], l1.m[a], l1.rank[a], b + off, nullptr, nullptr,
+                         z + off, zl[1] + l1.off[a], zs[1] + l1.off[a], nullptr});
     }
     launch_level<0>(s, nodes);
     for (int l = 2; l < L; ++l) {
@@ -185,15 +190,16 @@ void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const st
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
             if (!lv.m[a]) continue;
-            nodes.push_back({lv.Finv.p + lv.F_off[a], lv.V.p + lv.V_off[a], lv.m[a], lv.rank[a], zl[l - 1] + pv.off[c1],
-                             nullptr, ub[l] + pv.off[c1], zl[l] + lv.off[a], nullptr});
+            nodes.push_back({lv.Finv.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a], zl[l - 1] + pv.off[c1],
+                             nullptr, nullptr, ub[l] + pv.off[c1], zl[l] + lv.off[a], zs[l] + lv.off[a], nullptr});
         }
         launch_level<0>(s, nodes);
     }
     {
         const HssLevel& rt = H->lv[L];
         if (rt.m[0]) {
-            nodes.assign(1, {rt.Finv.p, nullptr, rt.m[0], 0, zl[L - 1], nullptr, nullptr, nullptr, zl[L - 1]});
+            nodes.assign(1, {rt.Finv.p, nullptr, rt.m[0], 0, zl[L - 1], nullptr, nullptr, nullptr, nullptr, nullptr,
+                             zl[L - 1]});
             launch_level<2>(s, nodes);
         }
     }
@@ -204,8 +210,8 @@ void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const st
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
             if (!lv.m[a]) continue;
-            nodes.push_back({lv.Finv.p + lv.F_off[a], lv.V.p + lv.V_off[a], lv.m[a], lv.rank[a], ub[l] + pv.off[c1],
-                             zl[l] + lv.off[a], nullptr, nullptr, zl[l - 1] + pv.off[c1]});
+            nodes.push_back({lv.Finv.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a], ub[l] + pv.off[c1],
+                             zl[l] + lv.off[a], zs[l] + lv.off[a], nullptr, nullptr, nullptr, zl[l - 1] + pv.off[c1]});
         }
         launch_level<1>(s, nodes);
     }
@@ -213,8 +219,8 @@ void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const st
     for (int a = 0; a < l1.count; ++a) {
         const int64_t off = t.begin[l1.first + a];
         if (!l1.m[a]) continue;
-        nodes.push_back({l1.Finv.p + l1.F_off[a], l1.V.p + l1.V_off[a], l1.m[a], l1.rank[a], z + off,
-                         zl[1] + l1.off[a], nullptr, nullptr, x + off});
+        nodes.push_back({l1.Finv.p + l1.F_off[a], l1.P.p + l1.V_off[a], l1.m[a], l1.rank[a], z + off,
+                         zl[1] + l1.off[a], zs[1] + l1.off[a], nullptr, nullptr, nullptr, x + off});
     }
     launch_level<1>(s, nodes);
 }

@@ -46,14 +46,14 @@ struct spd_hss_s {
     // solve workspace
     int64_t ws_k = 0;
     spd::DBuf<double> bt, xt;
-    std::vector<spd::DBuf<double>> z, ub;
+    std::vector<spd::DBuf<double>> z, ub, zs;
 };
 
 namespace spd {
 void hss_build_impl(spd_hss_s* H, const double* omega, uint64_t seed, cudaStream_t s);
 // k = 1 fused per-level solve (hsolve.cu); z: N workspace, zl[l] / ub[l]: level workspaces
 void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
-                   const std::vector<double*>& ub, cudaStream_t s);
+                   const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s);
 void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64_t ldx, int k, cudaStream_t s);
 void hss_query(const spd_hss_s* H, int what, void* buf, size_t bytes);
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,

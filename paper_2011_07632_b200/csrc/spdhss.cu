@@ -641,6 +641,9 @@ static void ensure_solve_ws(spd_hss_s* H, int k) {
     H->ub.clear();
     H->ub.resize(L + 1);
     for (int l = 2; l <= L; ++l) H->ub[l].alloc(std::max<int64_t>(1, H->lv[l - 1].R * k));
+    H->zs.clear();
+    H->zs.resize(L + 1);
+    for (int l = 1; l < L; ++l) H->zs[l].alloc(std::max<int64_t>(1, H->lv[l].R));
     H->ws_k = k;
 }
 
@@ -659,10 +662,10 @@ void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64
     ensure_solve_ws(H, k);
     double* z = H->bt.p;                               // N x k workspace (ld N)
     if (k == 1 && !getenv("SPD_SOLVE_GEMV")) {         // fused per-level single-vector path (hsolve.cu)
-        std::vector<double*> zl(L + 1, nullptr), ubl(L + 1, nullptr);
-        for (int l = 1; l < L; ++l) zl[l] = H->z[l].p;
+        std::vector<double*> zl(L + 1, nullptr), zsl(L + 1, nullptr), ubl(L + 1, nullptr);
+        for (int l = 1; l < L; ++l) { zl[l] = H->z[l].p; zsl[l] = H->zs[l].p; }
         for (int l = 2; l <= L; ++l) ubl[l] = H->ub[l].p;
-        hss_solve_vec(H, b, x, z, zl, ubl, s);
+        hss_solve_vec(H, b, x, z, zl, zsl, ubl, s);
         return;
     }
     const HssLevel& l1 = H->lv[1];

@@ -16,7 +16,9 @@ def spd():
 
 
 @pytest.mark.parametrize("ta,tb,m,n,k", [(0, 0, 64, 64, 16), (0, 0, 130, 77, 45), (1, 0, 50, 200, 300),
-                                         (0, 1, 7, 9, 3), (1, 1, 129, 65, 257), (0, 0, 1, 1, 1)])
+                                         (0, 1, 7, 9, 3), (1, 1, 129, 65, 257), (0, 0, 1, 1, 1),
+                                         # few output tiles, long K: split-K path (ragged last slice)
+                                         (1, 0, 32, 96, 6144), (0, 0, 70, 40, 5000), (1, 0, 32, 1, 4100)])
 def test_gemm(spd, ta, tb, m, n, k):
     import ctypes
     rng = np.random.default_rng(m * n + k)

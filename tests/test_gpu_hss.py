@@ -172,12 +172,16 @@ def test_full_c2_build_properties(spd):
     assert np.all(np.einsum("ij,ij->j", v, sv) > 0)
 
 
-@pytest.mark.parametrize("stored", ["0", "1"])
+@pytest.mark.parametrize("stored", ["0", "1", "partial"])
 def test_pcg_stored_and_on_the_fly_k1_paths(spd, stored, monkeypatch):
-    """Both k=1 matvec paths (on-the-fly eval-bound kernel; stored blocks, §8(f) f4)
-    give the oracle's PCG iterations and, afterwards, oracle-exact k=1 products."""
+    """All k=1 matvec paths (legacy per-level on-the-fly kernels; symmetric stored
+    blocks, §8(f) f4; symmetric with half the blocks evaluated on the fly) give the
+    oracle's PCG iterations and, afterwards, oracle-exact k=1 products."""
     import torch
-    monkeypatch.setenv("SPD_STORED", stored)
+    if stored == "partial":
+        monkeypatch.setenv("SPD_SYM_BUDGET", str(4 << 20))    # ~half of the C2s blocks
+    else:
+        monkeypatch.setenv("SPD_STORED", stored)
     cfg = CASES["C2s"]
     X = synth.points(cfg)
     h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
