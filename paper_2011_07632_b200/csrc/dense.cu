@@ -10,96 +10,15 @@
 //                  matrices use many SMs; small matrices get one CTA.  [P:827]
 //   formq_batched  explicit Q[:, :r] from the stored reflectors
 #include "common.cuh"
+#include "gemm.cuh"
 #include <algorithm>
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace spd {
 
-// ================================================================= GEMM
-constexpr int GT = 64, GK = 16;
-
-struct TileRef {
-    int desc, tm, tn;
-    int kb, ke;            // K range of this tile
-    double* P; int ldp;    // split-K: raw partial tile goes to P (ld ldp); nullptr: C = alpha acc + beta C
-};
-
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(128) gemm_kernel(const GemmDesc* __restrict__ descs,
-                                                   const TileRef* __restrict__ tiles,
-                                                   double alpha, double beta) {
-    __shared__ double As[GK][GT + 1];
-    __shared__ double Bs[GK][GT + 1];
-    const TileRef tr = tiles[blockIdx.x];
-    const GemmDesc d = descs[tr.desc];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, q = lane & 3;
-    const int wm = warp >> 1, wn = warp & 1;
-    const int m0 = tr.tm * GT, n0 = tr.tn * GT;
-    constexpr int PT = GT * GK / 128;                 // elements per thread per tile (8)
-    double acc[4][4][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    double ra[PT], rb[PT];
-    const int kend = tr.ke;
-    auto load = [&](int k0) {
-#pragma unroll
-        for (int u = 0; u < PT; ++u) {
-            const int e = tid + u * 128;
-            int i, kk;
-            if (TA) { kk = e % GK; i = e / GK; } else { i = e % GT; kk = e / GT; }
-            const int gi = m0 + i, gk = k0 + kk;
-            ra[u] = (gi < d.m && gk < kend) ? (TA ? __ldg(d.A + gk + (size_t)gi * d.lda) : __ldg(d.A + gi + (size_t)gk * d.lda)) : 0.0;
-            int j, kb;
-            if (TB) { j = e % GT; kb = e / GT; } else { kb = e % GK; j = e / GK; }
-            const int gj = n0 + j, gkb = k0 + kb;
-            rb[u] = (gj < d.n && gkb < kend) ? (TB ? __ldg(d.B + gj + (size_t)gkb * d.ldb) : __ldg(d.B + gkb + (size_t)gj * d.ldb)) : 0.0;
-        }
-    };
-    load(tr.kb);
-    for (int k0 = tr.kb; k0 < kend; k0 += GK) {
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < PT; ++u) {
-            const int e = tid + u * 128;
-            if (TA) As[e % GK][e / GK] = ra[u]; else As[e / GT][e % GT] = ra[u];
-            if (TB) Bs[e / GT][e % GT] = rb[u]; else Bs[e % GK][e / GK] = rb[u];
-        }
-        __syncthreads();
-        if (k0 + GK < kend) load(k0 + GK);                 // prefetch the next chunk
-#pragma unroll
-        for (int ks = 0; ks < GK / 4; ++ks) {
-            double af[4], bf[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) af[a] = As[ks * 4 + q][wm * 32 + a * 8 + g];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) bf[b] = Bs[ks * 4 + q][wn * 32 + b * 8 + g];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-        }
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                int i = m0 + wm * 32 + a * 8 + g;
-                int j = n0 + wn * 32 + b * 8 + 2 * q + h;
-                if (i < d.m && j < d.n) {
-                    if (tr.P) {
-                        tr.P[i + (size_t)j * tr.ldp] = acc[a][b][h];
-                    } else {
-                        double* c = d.C + i + (size_t)j * d.ldc;
-                        *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[a][b][h];
-                    }
-                }
-            }
-}
+// ================================================================= GEMM (pipelined DMMA tiles: gemm.cuh)
+constexpr int GK = 16;
 
 // ---------------------------------------------------------------- narrow GEMM (n <= 4): GEMV-like
 // notrans A: one thread per output row (coalesced column reads of A);
@@ -193,6 +112,27 @@ __global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ 
     }
 }
 
+template <int BM, int BN, int WM, int WN, int ST, bool TA, bool TB>
+static void launch_gemm_pipe1(cudaStream_t s, unsigned nb, const GemmDesc* d, const TileRef* t, double alpha, double beta) {
+    constexpr size_t sh = gemm_pipe_smem<BM, BN, WM, WN, ST, TA, TB>();
+    static bool attr = false;
+    if (!attr) {
+        SPD_CUDA(cudaFuncSetAttribute(gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        attr = true;
+    }
+    gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB><<<nb, (BM / WM) * (BN / WN) * 32, sh, s>>>(d, t, alpha, beta);
+    SPD_LAUNCH();
+}
+template <int BM, int BN, int WM, int WN, int ST>
+static void launch_gemm_pipe(cudaStream_t s, unsigned nb, const GemmDesc* d, const TileRef* t, double alpha,
+                             double beta, bool ta, bool tb) {
+    if (!ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, false>(s, nb, d, t, alpha, beta);
+    else if (ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, true, false>(s, nb, d, t, alpha, beta);
+    else if (!ta && tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, true>(s, nb, d, t, alpha, beta);
+    else launch_gemm_pipe1<BM, BN, WM, WN, ST, true, true>(s, nb, d, t, alpha, beta);
+}
+
 // split-K epilogue: C = alpha sum_s P_s + beta C, slices added in order
 struct ReduceDesc { int desc, S; int64_t off; };
 __global__ void gemm_reduce_kernel(const GemmDesc* __restrict__ descs, const ReduceDesc* __restrict__ red,
@@ -244,6 +184,10 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         for (auto& g : d) nmax = std::max(nmax, g.n);
         if (nmax <= 4) { gemv_batched(s, d, transA, alpha, beta); return; }
     }
+    // tile size: 64 x 64 (4 warps of 32 x 32; measured 31-32 TF/s at 4096^3, 88-91 % of
+    // cuBLAS DGEMM, against 28-30 TF/s for 128 x 128); env SPD_GEMM_TILE=128 overrides
+    int T = 64;
+    if (const char* e = getenv("SPD_GEMM_TILE")) T = atoi(e) == 128 ? 128 : 64;
     // output tiles; when they are too few to fill the GPU and K is long (the tall
     // skinny V^T A of the blocked QR), K is split into S slices whose raw partial
     // tiles are summed in slice order by gemm_reduce_kernel (deterministic)
@@ -251,7 +195,7 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     int kmax = 0;
     for (const auto& g : d) {
         if (g.m <= 0 || g.n <= 0) continue;
-        ntiles += (long long)ceil_div(g.m, GT) * ceil_div(g.n, GT);
+        ntiles += (long long)ceil_div(g.m, T) * ceil_div(g.n, T);
         kmax = std::max(kmax, g.k);
     }
     int S = 1;
@@ -267,8 +211,8 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         const int kc = Si > 1 ? ceil_div(ceil_div(d[i].k, Si), GK) * GK : std::max(d[i].k, 0);
         const int Seff = Si > 1 ? ceil_div(d[i].k, kc) : 1;
         for (int ks = 0; ks < Seff; ++ks)
-            for (int tn = 0; tn < ceil_div(d[i].n, GT); ++tn)
-                for (int tm = 0; tm < ceil_div(d[i].m, GT); ++tm) {
+            for (int tn = 0; tn < ceil_div(d[i].n, T); ++tn)
+                for (int tm = 0; tm < ceil_div(d[i].m, T); ++tm) {
                     TileRef tr{i, tm, tn, ks * kc, std::min(d[i].k, (ks + 1) * kc), nullptr, d[i].m};
                     if (Seff > 1) tr.P = (double*)(uintptr_t)(poff + (size_t)ks * d[i].m * d[i].n + 1);  // offset+1, patched below
                     tiles.push_back(tr);
@@ -296,11 +240,8 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         ProfScope prof(s, "gemm_dmma", fl, by);
         for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
             unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
-            if (!transA && !transB) gemm_kernel<false, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-            else if (transA && !transB) gemm_kernel<true, false><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-            else if (!transA && transB) gemm_kernel<false, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-            else gemm_kernel<true, true><<<nb, 128, 0, s>>>(dd.p, dt.p + off, alpha, beta);
-            SPD_LAUNCH();
+            if (T == 128) launch_gemm_pipe<128, 128, 64, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
+            else launch_gemm_pipe<64, 64, 32, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
         }
     }
     if (!red.empty()) {
@@ -829,7 +770,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = 8;
     const int L = d.m - d.p;                 // panel rows
     double* P = d.A + d.p + (size_t)d.p * d.ld;   // panel origin
-    __shared__ double s_beta[QB], s_v0, s_mu, s_sig, s_x0;
+    __shared__ double s_beta[QB], s_v0, s_mu, s_sig;
     __shared__ double G[QB][QB + 1];         // V^T V
     for (int j = 0; j < d.jb; ++j) {
         double* col = P + (size_t)j * d.ld;
@@ -846,7 +787,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
                     v0 = (x0 <= 0.0) ? x0 - mu : -sg / (x0 + mu);
                     beta = 2.0 * v0 * v0 / (sg + v0 * v0);
                 }
-                s_beta[j] = beta; s_v0 = v0; s_mu = mu; s_sig = sg; s_x0 = x0;
+                s_beta[j] = beta; s_v0 = v0; s_mu = mu; s_sig = sg;
             }
         }
         __syncthreads();
