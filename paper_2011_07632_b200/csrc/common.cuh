@@ -48,6 +48,7 @@ void stage_mark(cudaStream_t s, const char* name, int level = 0);
 struct ProfCaptured;
 ProfCaptured* prof_capture_take(size_t first);   // records [first, end) of the list
 size_t prof_mark();
+void prof_update_last(const char* name, double flops, double bytes);   // latest record of that name
 void prof_accumulate(ProfCaptured* c);            // after a (synchronized) replay
 void prof_release(ProfCaptured* c);
 

@@ -449,6 +449,11 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     h->stored_mode = 1;
     h->sym_budget = (env && env[0] == '1') ? need : std::min(need, 0.4 * (double)fr);
     if (const char* b = getenv("SPD_SYM_BUDGET")) h->sym_budget = std::min(need, atof(b));   // bytes (tests)
+    // Blocks past the memory budget are evaluated on the fly.  (Measured on C2: the
+    // evaluation path runs at ~1e11 entries/s inside the sym kernel against ~8e11
+    // streamed, so nothing is evaluated while memory allows.)  SPD_SYM_FRAC: test hook.
+    h->sym_frac = 1.0;
+    if (const char* f = getenv("SPD_SYM_FRAC")) h->sym_frac = atof(f);
 }
 
 // Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]

@@ -28,12 +28,13 @@ struct Timer;
 // symmetric stored blocks for k = 1 products (h2sym.cu)
 constexpr int SYM_MAX_SLOTS = 32;
 struct SymBuild { const double* tx; const double* sx; int64_t tds, sds, tid0, sid0; int nr, nb; int64_t vbase; };
-struct SymPiece {
+struct SymPiece {            // a band of up to 4 row tiles of a block (rows nr <= 128)
     int64_t vbase, xa_off, xb_off, fwd, trn;   // vbase < 0: evaluated on the fly
     int slot, nr, nb;
     const double* tx; const double* sx; int64_t tds, sds, tid0, sid0;   // row / column points, ids (shift)
 };
-struct SymGNode { int slot, n; int64_t off; int c0, c1; };
+struct SymGNode { int slot, n; int64_t off; int c0, c1; };   // lists >= SYM_BIG: one CTA
+constexpr int SYM_BIG = 48;
 struct SymContrib { int64_t soff; int ro, len; };
 struct SymVecs { const double* p[SYM_MAX_SLOTS]; };
 struct SymVecsOut { double* p[SYM_MAX_SLOTS]; };
@@ -42,7 +43,8 @@ struct H2SymStore {
     DBuf<SymPiece> pieces;
     DBuf<SymGNode> gnodes;
     DBuf<SymContrib> gcon;
-    int npieces = 0, ngnodes = 0;
+    int npieces = 0, ngnodes = 0, nbig = 0;      // gnodes[0, nbig): long lists
+    int nbmax = 1;
     double flops = 0, bytes = 0, stored_frac = 1.0;
     bool built = false;
 };
@@ -74,6 +76,7 @@ struct spd_h2_s {
     // up to sym_budget bytes, the rest evaluated on the fly
     int stored_mode = -1;          // -1 undecided, 0 old per-level path (tests), 1 symmetric
     double sym_budget = 0.0;
+    double sym_frac = 1.0;         // fraction of the blocks to store (rest: evaluated, overlapping HBM and FP64)
     spd::H2SymStore sym;
 };
 

@@ -19,19 +19,11 @@
 // and a gather kernel sums each output node's partials in a fixed order (no
 // atomics: the product is bitwise reproducible) and overwrites y / yh.
 #include "h2.hpp"
+#include "phases.cuh"
 #include <algorithm>
 
 namespace spd {
 
-constexpr int SY_NW = 4;               // warps per apply CTA
-
-template <int KID>
-__device__ __forceinline__ double kval_sym(const KernelParams& kp, double r2) {
-    if (KID == SPD_K_GAUSSIAN) return exp(-r2 * kp.inv_l2);
-    if (KID == SPD_K_MATERN32) { const double t = sqrt(r2) * kp.sqrt3_inv_l; return (1.0 + t) * exp(-t); }
-    if (KID == SPD_K_EXPONENTIAL) return exp(-sqrt(r2) * kp.inv_l);
-    return rsqrt(r2 + kp.l2);
-}
 
 template <int KID>
 __global__ void __launch_bounds__(256) sym_build_kernel(KernelParams kp, double shift, int d,
@@ -55,119 +47,27 @@ __global__ void __launch_bounds__(256) sym_build_kernel(KernelParams kp, double 
     }
 }
 
-template <int KID>
+template <int KID, bool EVAL>
 __global__ void __launch_bounds__(SY_NW * 32) sym_apply_kernel(const SymPiece* __restrict__ pieces, SymVecs xin,
                                                                const double* __restrict__ vals,
                                                                double* __restrict__ scratch, KernelParams kp,
                                                                double shift, int d) {
-    __shared__ double red[SY_NW][32];
-    const SymPiece pc = pieces[blockIdx.x];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* xs = xin.p[pc.slot];
-    const bool trn = pc.trn >= 0;
-    const double xa = (trn && lane < pc.nr) ? xs[pc.xa_off + lane] : 0.0;
-    const bool stored = pc.vbase >= 0;
-    const double* v = vals + (stored ? pc.vbase : 0) + lane;
-    double rx0 = 0.0, rx1 = 0.0, rx2 = 0.0;     // on the fly: this lane's row point
-    if (!stored && lane < pc.nr) {
-        rx0 = pc.tx[lane];
-        if (d > 1) rx1 = pc.tx[pc.tds + lane];
-        if (d > 2) rx2 = pc.tx[2 * pc.tds + lane];
-    }
-    const bool sh = !stored && shift != 0.0 && pc.tid0 >= 0;
-    double acc = 0.0;
-    const int nch = (pc.nb + 31) >> 5;
-    for (int ch = warp; ch < nch; ch += SY_NW) {
-        const int c0 = ch * 32;
-        const int cn = min(32, pc.nb - c0);
-        const double xbv = lane < cn ? xs[pc.xb_off + c0 + lane] : 0.0;
-        double kv[32];
-        if (stored) {
-            if (cn == 32) {
-#pragma unroll
-                for (int c = 0; c < 32; ++c) kv[c] = __ldg(v + (size_t)(c0 + c) * 32);
-            } else {
-#pragma unroll
-                for (int c = 0; c < 32; ++c) kv[c] = c < cn ? __ldg(v + (size_t)(c0 + c) * 32) : 0.0;
-            }
-        } else {
-            // source point c0 + lane, broadcast by shuffles; rows past nr give 0
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            if (lane < cn) {
-                s0 = pc.sx[c0 + lane];
-                if (d > 1) s1 = pc.sx[pc.sds + c0 + lane];
-                if (d > 2) s2 = pc.sx[2 * pc.sds + c0 + lane];
-            }
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const double d0 = rx0 - __shfl_sync(0xffffffffu, s0, c);
-                const double d1 = rx1 - __shfl_sync(0xffffffffu, s1, c);
-                const double d2 = rx2 - __shfl_sync(0xffffffffu, s2, c);
-                double k = kval_sym<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
-                if (sh && pc.tid0 + lane == pc.sid0 + c0 + c) k += shift;
-                kv[c] = (c < cn && lane < pc.nr) ? k : 0.0;
-            }
-        }
-        double f0 = 0.0, f1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-            f0 += kv[c] * __shfl_sync(0xffffffffu, xbv, c);
-            f1 += kv[c + 1] * __shfl_sync(0xffffffffu, xbv, c + 1);
-        }
-        acc += f0 + f1;
-        if (trn) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) kv[c] *= xa;
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                const bool up = (lane & o) != 0;
-#pragma unroll
-                for (int j = 0; j < o; ++j) {
-                    const double send = up ? kv[j] : kv[j + o];
-                    const double keep = up ? kv[j + o] : kv[j];
-                    kv[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                }
-            }
-            if (lane < cn) scratch[pc.trn + c0 + lane] = kv[0];
-        }
-    }
-    red[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0 && lane < pc.nr) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < SY_NW; ++w) s += red[w][lane];
-        scratch[pc.fwd + lane] = s;
-    }
+    extern __shared__ double tp[];
+    sym_piece<KID, EVAL>(pieces[blockIdx.x], xin, vals, scratch, kp, shift, d, 0, tp);
 }
 
-// one CTA per (output node, 32-row tile): y[tile] = sum of the tile's partials in list order
-// (warp w takes partials w, w+8, ...; the 8 warp sums are added in warp order)
-__global__ void __launch_bounds__(256) sym_gather_kernel(const SymGNode* __restrict__ nodes,
+// long lists: one CTA per (output node, 32-row tile); short lists: one warp each
+__global__ void __launch_bounds__(PH_T) sym_gather_big_kernel(const SymGNode* __restrict__ nodes,
+                                                              const SymContrib* __restrict__ con, SymVecsOut yout,
+                                                              const double* __restrict__ scratch) {
+    __shared__ double red[PH_W * 32];
+    gather_item_cta(nodes[blockIdx.x], con, yout, scratch, red);
+}
+__global__ void __launch_bounds__(256) sym_gather_kernel(const SymGNode* __restrict__ nodes, int n,
                                                          const SymContrib* __restrict__ con, SymVecsOut yout,
                                                          const double* __restrict__ scratch) {
-    __shared__ double red[8][32];
-    const SymGNode g = nodes[blockIdx.x];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double a0 = 0.0, a1 = 0.0;
-    int c = g.c0 + warp;
-    for (; c + 8 < g.c1; c += 16) {
-        const SymContrib q0 = con[c], q1 = con[c + 8];
-        if (lane < q0.len) a0 += scratch[q0.soff + lane];
-        if (lane < q1.len) a1 += scratch[q1.soff + lane];
-    }
-    if (c < g.c1) {
-        const SymContrib q0 = con[c];
-        if (lane < q0.len) a0 += scratch[q0.soff + lane];
-    }
-    red[warp][lane] = a0 + a1;
-    __syncthreads();
-    if (warp == 0 && lane < g.n) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) sum += red[w][lane];
-        yout.p[g.slot][g.off + lane] = sum;
-    }
+    const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (w < n) gather_item_warp(nodes[w], con, yout, scratch);
 }
 
 // ----------------------------------------------------------------- host side
@@ -176,9 +76,12 @@ struct PlanBlock { int slot, a, b; };   // block (a <= b) of slot 0 (near, leave
 }
 
 // budget: doubles of stored blocks allowed (pieces past it are evaluated on the fly)
-static void sym_plan(const spd_h2_s* h, int64_t budget, std::vector<SymBuild>* builds, std::vector<SymPiece>* pieces,
-                     std::vector<SymGNode>* gnodes, std::vector<SymContrib>* gcon, int64_t* nvals, int64_t* nscratch,
-                     double* flops, int64_t* nall) {
+static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector<SymBuild>* builds,
+                     std::vector<SymPiece>* pieces, std::vector<SymGNode>* gnodes, std::vector<SymContrib>* gcon,
+                     int64_t* nvals, int64_t* nscratch, double* flops, int64_t* nall, int* nbig_out = nullptr,
+                     int* nbmax_out = nullptr) {
+    int64_t npiece = 0;
+    int nbmax = 1;
     const TreeH& t = h->tree;
     const int L = t.L, d = h->d;
     const int64_t N = h->N;
@@ -213,23 +116,33 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, std::vector<SymBuild>* b
         if (na == 0 || nb == 0) return;
         const bool diag = (a == b);
         fl += 2.0 * na * nb * (diag ? 1.0 : 2.0);
-        for (int r0 = 0; r0 < na; r0 += 32) {
-            const int nr = std::min(32, na - r0);
-            const bool store = vb + 32LL * nb <= budget;
-            all += 32LL * nb;
+        for (int r0 = 0; r0 < na; r0 += 32 * SY_NW) {
+            const int nr = std::min(32 * SY_NW, na - r0);          // band of up to 4 row tiles
+            const int nt = ceil_div(nr, 32);
+            // stored if within the budget and, when only a fraction should be stored,
+            // on the evenly spread pattern (stored and evaluated bands interleave, so
+            // every SM streams and evaluates at the same time)
+            const int64_t ip = npiece++;
+            const bool pat = frac >= 1.0 || (int64_t)((ip + 1) * frac) > (int64_t)(ip * frac);
+            const bool store = pat && vb + 32LL * nb * nt <= budget;
+            all += 32LL * nb * nt;
             if (builds && store)
-                builds->push_back({tx + r0, sx, ds, ds, slot == 0 ? tid0 + r0 : -1, slot == 0 ? sid0 : -1, nr, nb, vb});
+                for (int w = 0; w < nt; ++w)
+                    builds->push_back({tx + r0 + 32 * w, sx, ds, ds, slot == 0 ? tid0 + r0 + 32 * w : -1,
+                                       slot == 0 ? sid0 : -1, std::min(32, nr - 32 * w), nb, vb + 32LL * nb * w});
             SymPiece pc;
             pc.vbase = store ? vb : -1; pc.slot = slot; pc.nr = nr; pc.nb = nb;
             pc.tx = tx + r0; pc.sx = sx; pc.tds = ds; pc.sds = ds;
             pc.tid0 = slot == 0 ? tid0 + r0 : -1; pc.sid0 = slot == 0 ? sid0 : -1;
             pc.xa_off = xa0 + r0; pc.xb_off = xb0;
-            pc.fwd = sc; sc += 32;
+            pc.fwd = sc; sc += 32 * nt;
             pc.trn = diag ? -1 : sc;
             if (!diag) sc += nb;
             if (pieces) pieces->push_back(pc);
-            if (store) vb += 32LL * nb;
-            con[slot][a][r0 / 32].push_back({pc.fwd, 0, nr});
+            if (store) vb += 32LL * nb * nt;
+            nbmax = std::max(nbmax, nb);
+            for (int w = 0; w < nt; ++w)
+                con[slot][a][r0 / 32 + w].push_back({pc.fwd + 32 * w, 0, std::min(32, nr - 32 * w)});
             if (!diag)
                 for (int tb = 0; tb * 32 < nb; ++tb) con[slot][b][tb].push_back({pc.trn + 32 * tb, 0, std::min(32, nb - 32 * tb)});
         }
@@ -242,23 +155,30 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, std::vector<SymBuild>* b
             if (pr.first < pr.second) add_block(lk, pr.first - f, pr.second - f);
     }
     if (gnodes) {
-        for (int slot = 0; slot < L; ++slot) {
-            const int cnt = slot == 0 ? nl : h->lv[slot].count;
-            for (int a = 0; a < cnt; ++a) {
-                const int n = slot == 0 ? (int)t.size(l1 + a) : h->lv[slot].rank[a];
-                const int64_t off = slot == 0 ? t.begin[l1 + a] : h->lv[slot].off[a];
-                for (int tt = 0; tt * 32 < n; ++tt) {
-                    SymGNode g;
-                    g.slot = slot; g.n = std::min(32, n - 32 * tt);
-                    g.off = off + 32 * tt;
-                    g.c0 = (int)gcon->size();
-                    for (auto& q : con[slot][a][tt]) gcon->push_back(q);
-                    g.c1 = (int)gcon->size();
-                    gnodes->push_back(g);
+        // long lists (>= SYM_BIG partials) first: those are reduced by a whole CTA
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int slot = 0; slot < L; ++slot) {
+                const int cnt = slot == 0 ? nl : h->lv[slot].count;
+                for (int a = 0; a < cnt; ++a) {
+                    const int n = slot == 0 ? (int)t.size(l1 + a) : h->lv[slot].rank[a];
+                    const int64_t off = slot == 0 ? t.begin[l1 + a] : h->lv[slot].off[a];
+                    for (int tt = 0; tt * 32 < n; ++tt) {
+                        const auto& L_ = con[slot][a][tt];
+                        if ((pass == 0) != ((int)L_.size() >= SYM_BIG)) continue;
+                        SymGNode g;
+                        g.slot = slot; g.n = std::min(32, n - 32 * tt);
+                        g.off = off + 32 * tt;
+                        g.c0 = (int)gcon->size();
+                        for (auto& q : L_) gcon->push_back(q);
+                        g.c1 = (int)gcon->size();
+                        gnodes->push_back(g);
+                    }
                 }
             }
+            if (pass == 0 && nbig_out) *nbig_out = (int)gnodes->size();
         }
     }
+    if (nbmax_out) *nbmax_out = nbmax;
     *nvals = vb;
     *nscratch = sc;
     *flops = fl;
@@ -268,7 +188,7 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, std::vector<SymBuild>* b
 size_t h2sym_bytes(const spd_h2_s* h) {
     int64_t nv = 0, ns = 0, na = 0;
     double fl = 0;
-    sym_plan(h, 0, nullptr, nullptr, nullptr, nullptr, &nv, &ns, &fl, &na);
+    sym_plan(h, 0, 1.0, nullptr, nullptr, nullptr, nullptr, &nv, &ns, &fl, &na);
     return 8 * (size_t)(na + ns);
 }
 
@@ -280,7 +200,8 @@ void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
     std::vector<SymGNode> gnodes;
     std::vector<SymContrib> gcon;
     int64_t nv = 0, ns = 0, na = 0;
-    sym_plan(h, (int64_t)(budget_bytes / 8), &builds, &pieces, &gnodes, &gcon, &nv, &ns, &st.flops, &na);
+    sym_plan(h, (int64_t)(budget_bytes / 8), h->sym_frac, &builds, &pieces, &gnodes, &gcon, &nv, &ns, &st.flops, &na,
+             &st.nbig, &st.nbmax);
     st.vals.alloc(std::max<int64_t>(1, nv));
     st.scratch.alloc(std::max<int64_t>(1, ns));
     st.pieces.upload(pieces, s);
@@ -309,6 +230,21 @@ void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
     st.built = true;
 }
 
+template <int KID>
+static void launch_sym(cudaStream_t s, unsigned nb, size_t smem, const H2SymStore& st, const SymVecs& xin,
+                       const KernelParams& kp, double sh, int d) {
+    if (st.stored_frac >= 1.0) {
+        if (smem > 48 * 1024)
+            SPD_CUDA(cudaFuncSetAttribute(sym_apply_kernel<KID, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        sym_apply_kernel<KID, false><<<nb, SY_NW * 32, smem, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, d);
+    } else {
+        if (smem > 48 * 1024)
+            SPD_CUDA(cudaFuncSetAttribute(sym_apply_kernel<KID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        sym_apply_kernel<KID, true><<<nb, SY_NW * 32, smem, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, d);
+    }
+    SPD_LAUNCH();
+}
+
 // y (leaf slot) and yh[l] are OVERWRITTEN with the near / coupling products of
 // x and xh[l]; the caller runs the up pass before and the down pass after.
 void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<double*>& xh,
@@ -326,18 +262,26 @@ void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<doub
         const unsigned nb = (unsigned)st.npieces;
         const KernelParams& kp = h->kp;
         const double sh = h->kern.shift;
+        const size_t smem = sizeof(double) * SY_NW * st.nbmax;
         switch (kp.id) {
-        case SPD_K_GAUSSIAN: sym_apply_kernel<SPD_K_GAUSSIAN><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
-        case SPD_K_MATERN32: sym_apply_kernel<SPD_K_MATERN32><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
-        case SPD_K_EXPONENTIAL: sym_apply_kernel<SPD_K_EXPONENTIAL><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
-        default: sym_apply_kernel<SPD_K_IMQ><<<nb, SY_NW * 32, 0, s>>>(st.pieces.p, xin, st.vals.p, st.scratch.p, kp, sh, h->d); break;
+        case SPD_K_GAUSSIAN: launch_sym<SPD_K_GAUSSIAN>(s, nb, smem, st, xin, kp, sh, h->d); break;
+        case SPD_K_MATERN32: launch_sym<SPD_K_MATERN32>(s, nb, smem, st, xin, kp, sh, h->d); break;
+        case SPD_K_EXPONENTIAL: launch_sym<SPD_K_EXPONENTIAL>(s, nb, smem, st, xin, kp, sh, h->d); break;
+        default: launch_sym<SPD_K_IMQ>(s, nb, smem, st, xin, kp, sh, h->d); break;
         }
-        SPD_LAUNCH();
     }
     if (st.ngnodes) {
         ProfScope prof(s, "sym_gather", 0, 0);
-        sym_gather_kernel<<<(unsigned)st.ngnodes, 256, 0, s>>>(st.gnodes.p, st.gcon.p, yout, st.scratch.p);
-        SPD_LAUNCH();
+        if (st.nbig) {
+            sym_gather_big_kernel<<<(unsigned)st.nbig, PH_T, 0, s>>>(st.gnodes.p, st.gcon.p, yout, st.scratch.p);
+            SPD_LAUNCH();
+        }
+        const int ns = st.ngnodes - st.nbig;
+        if (ns > 0) {
+            sym_gather_kernel<<<(unsigned)ceil_div(ns, 8), 256, 0, s>>>(st.gnodes.p + st.nbig, ns, st.gcon.p, yout,
+                                                                       st.scratch.p);
+            SPD_LAUNCH();
+        }
     }
 }
 

@@ -58,6 +58,16 @@ void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64
 void hss_query(const spd_hss_s* H, int what, void* buf, size_t bytes);
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,
               cudaStream_t s);
+// persistent (cooperative) PCG kernel, pcgk.cu
+struct PcgPersistent {
+    struct Impl;
+    Impl* impl = nullptr;
+    ~PcgPersistent();
+};
+bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double* x, double* r, double* p, double* q,
+                            double* z, cudaStream_t s);
+// out: ||r||^2, iterations, converged, error (1: p^T A p <= 0, 2: r^T M r <= 0)
+void pcg_persistent_run(PcgPersistent& pk, double rz, double nb, double tol, int maxit, double out[4], cudaStream_t s);
 const spd_hss_s* hss_if_hss(const void* handle);      // nullptr when handle is not an HSS
 const double* hss_timings(const spd_hss_s* H);
 inline uint64_t pair_key(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uint32_t)j; }

@@ -8,6 +8,7 @@
 #include "hss.hpp"
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 
 namespace spd {
 
@@ -142,10 +143,27 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     else SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
     SPD_CUDA(cudaMemcpyAsync(w.p.p, w.z.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
     dot_into(s, w, w.r.p, w.z.p, N, S_RZ, 0);
+    SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
     SPD_CUDA(cudaStreamSynchronize(s));
 
-    // capture one iteration as a graph (descriptors in a persistent arena)
     h2_prepare(A, 1, s);
+    // persistent cooperative kernel for the whole loop (pcgk.cu); env SPD_PCG_GRAPH=1
+    // selects the per-iteration CUDA graph below instead (per-kernel profiling)
+    if (!getenv("SPD_PCG_GRAPH")) {
+        PcgPersistent pk;
+        if (pcg_persistent_prepare(pk, A, M, x, w.r.p, w.p.p, w.q.p, w.z.p, s)) {
+            double out[4];
+            pcg_persistent_run(pk, hs[S_RZ], nb, tol, maxit, out, s);
+            rep->iters = (int)out[1];
+            rep->relres = std::sqrt(out[0]) / nb;
+            rep->converged = out[2] != 0.0;
+            if (out[3] == 1.0) throw Error(SPD_ENOTPD, "PCG breakdown: p^T A p <= 0");
+            if (out[3] == 2.0) throw Error(SPD_ENOTPD, "PCG breakdown: r^T M^{-1} r <= 0");
+            rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return;
+        }
+    }
+    // capture one iteration as a graph (descriptors in a persistent arena)
     h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);     // builds stored k=1 blocks outside the graph
     bool use_graph = maxit > 1;
     long long graph_kernels = 0;          // kernel nodes per replay (launch accounting)

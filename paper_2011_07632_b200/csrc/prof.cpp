@@ -102,6 +102,12 @@ ProfScope::~ProfScope() {
     if (!ext && g_recs.size() > 20000) drain();
 }
 
+void prof_update_last(const char* name, double flops, double bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = g_recs.size(); i-- > 0;)
+        if (g_recs[i].name == name) { g_recs[i].flops = flops; g_recs[i].bytes = bytes; return; }
+}
+
 size_t prof_mark() {
     std::lock_guard<std::mutex> lk(g_mu);
     return g_recs.size();
