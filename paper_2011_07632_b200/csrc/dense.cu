@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <cstdio>
 
 namespace spd {
 
@@ -836,11 +837,25 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
     }
 }
 
-// Cluster panel QR: a cluster of CL CTAs per panel; CTA g keeps rows
-// [g*rp, (g+1)*rp) of the panel in shared memory; per column two cluster
-// barriers exchange partial sums through DSMEM (summed in rank order, so
-// every CTA derives bit-identical reflectors).
+// Cluster panel QR: a cluster of QCL CTAs per panel; CTA g keeps rows
+// [g*rp, (g+1)*rp) of the panel in shared memory.  ONE cluster barrier per column:
+// before the reflector of column j is known, every CTA forms the partial sums over
+// its rows i > j of  A_ij^2 (sigma),  A_ij A_ic (c > j)  and  V_ia A_ij (a < j)  and
+// publishes them with the row-j values it owns; after the barrier every CTA adds
+// the QCL partials (lane q reads CTA q, xor-butterfly: bitwise identical everywhere)
+// and derives the Householder scalars, w_c = A_jc + d_c / v0 for the update and
+// V^T v_j = V_j. + g / v0 for the next column of the compact-WY T (T_jj = beta_j,
+// T[:j, j] = -beta_j T[:j, :j] V^T v_j; Golub-Van Loan 5.1.2), without a second pass.
 namespace cg = cooperative_groups;
+
+__device__ unsigned long long g_qr_trace[64];      // debug (SPD_QR_TRACE): CTA 0 phase timestamps
+__device__ __forceinline__ void qr_tr(int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_qr_trace[k] = t;
+    }
+}
 
 template <int QCL>
 __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
@@ -848,46 +863,71 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
     const int g = (int)cluster.block_rank();
     const PanelDesc d = descs[blockIdx.x / QCL];
     extern __shared__ double sm[];                    // rp x QB panel slice (col-major, ld rp)
-    __shared__ double part[2][QB + 2];                // [0]: sigma, x0 ; [1]: dots
-    __shared__ double Gp[QB][QB + 1];                 // partial V^T V
-    __shared__ double Gs[QB][QB + 1];                 // cluster-summed V^T V (CTA 0)
-    __shared__ double red[8];
-    __shared__ double s_beta[QB];
+    constexpr int NP = 2 * QB + 2;                    // partials per column
+    __shared__ double part[2][NP];                    // [0..QB): A_ij A_ic (c = j: sigma), [QB..2QB): V_ia A_ij,
+                                                      // [2QB]: x0 (row-j owner), row-j values in rowv
+    __shared__ double rowv[2][2 * QB];                // row j: A_jc (c > j) and V_ja (a < j), owner CTA only
+    __shared__ double T[QB][QB + 1];
+    __shared__ double vtv[QB];
+    __shared__ double wc[QB];
+    __shared__ double tot[NP + 2 * QB];               // their sums
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int L = d.m - d.p, jb = d.jb;
     const int r0 = g * rp, nr = max(0, min(rp, L - r0));
     double* P = d.A + d.p + (size_t)d.p * d.ld;
-    for (int e = threadIdx.x; e < rp * jb; e += blockDim.x) {
-        const int i = e % rp, c = e / rp;
-        sm[i + c * rp] = (i < nr) ? P[r0 + i + (size_t)c * d.ld] : 0.0;
-    }
+    qr_tr(0);
+    // panel slice -> smem with asynchronous copies (all in flight at once)
+    for (int c = 0; c < jb; ++c)
+        for (int i = threadIdx.x; i < rp; i += blockDim.x)
+            cp_async8(sm + i + c * rp, i < nr ? P + r0 + i + (size_t)c * d.ld : P, i < nr);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
+    qr_tr(1);
     for (int j = 0; j < jb; ++j) {
-        double* col = sm + j * rp;
-        // (1) partial sigma over rows > j, and x0 from the owner of row j
-        double sg = 0.0;
-        for (int i = threadIdx.x; i < nr; i += blockDim.x)
-            if (r0 + i > j) sg += col[i] * col[i];
-        sg = warp_sum(sg);
-        if (lane == 0) red[warp] = sg;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < 8; ++w) t += red[w];
-            part[0][0] = t;
-            part[0][1] = (j >= r0 && j < r0 + nr) ? col[j - r0] : 0.0;
+        if (j == 1) qr_tr(2);
+        if (j == 16) qr_tr(3);
+        const int buf = j & 1;
+        const double* colj = sm + j * rp;
+        // ---- partial sums over my rows i > j (warp w: entries e = w, w + 8, ...)
+        //      e < QB: column c = j + e (c == j: sigma);  QB <= e < QB + j: reflector a = e - QB
+        for (int e = warp; e < QB + j; e += 8) {
+            double acc = 0.0;
+            const double* other = e < QB ? (j + e < jb ? sm + (j + e) * rp : nullptr) : sm + (e - QB) * rp;
+            if (other)
+                for (int i = lane; i < nr; i += 32)
+                    if (r0 + i > j) acc += colj[i] * other[i];
+            acc = warp_sum(acc);
+            if (lane == 0) part[buf][e] = acc;
+        }
+        // row-j values (owner of row j)
+        const bool own = j >= r0 && j < r0 + nr;
+        if (own) {
+            const int lj = j - r0;
+            for (int c = threadIdx.x; c < jb; c += blockDim.x) rowv[buf][c] = sm[lj + c * rp];          // A_jc
+            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][QB + a] = sm[lj + a * rp];      // V_ja
+        } else {
+            for (int c = threadIdx.x; c < jb; c += blockDim.x) rowv[buf][c] = 0.0;
+            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][QB + a] = 0.0;
         }
         cluster.sync();
-        // lane q reads CTA q's partials; the xor-butterfly sum is bitwise identical in
-        // every lane, warp and CTA (commutative pairwise adds), so all CTAs agree
-        double sig = 0.0, x0 = 0.0;
-        if (lane < QCL) {
-            const double* rp_ = cluster.map_shared_rank(&part[0][0], lane);
-            sig = rp_[0];
-            x0 = rp_[1];
+        // ---- sum every entry over the CTAs in rank order (same bits in every CTA):
+        //      thread e issues its QCL remote (DSMEM) loads at once
+        {
+            constexpr int NE = NP + 2 * QB;
+            for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+                const double* base = e < NP ? &part[buf][e] : &rowv[buf][e - NP];
+                double v[QCL];
+#pragma unroll
+                for (int q = 0; q < QCL; ++q) v[q] = *cluster.map_shared_rank(base, q);
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < QCL; ++q) t += v[q];
+                tot[e] = t;
+            }
+            __syncthreads();
         }
-        sig = warp_sum(sig);
-        x0 = warp_sum(x0);
+        const double sig = tot[0], x0 = tot[NP + j];
         double beta, mu, v0;
         if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
         else {
@@ -896,84 +936,41 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
             beta = 2.0 * v0 * v0 / (sig + v0 * v0);
         }
         const double inv0 = (sig == 0.0) ? 0.0 : 1.0 / v0;
-        // (2) v on my rows -> global V ; R diagonal stays in the owner's slice
-        double* vg = d.V + (size_t)j * d.ldv;
+        // w_c = A_jc + d_c / v0 (c > j);  V^T v_j [a] = V_ja + g_a / v0 (a < j)
+        for (int c = j + 1 + threadIdx.x; c < jb; c += blockDim.x) wc[c] = tot[NP + c] + tot[c - j] * inv0;
+        for (int a = threadIdx.x; a < j; a += blockDim.x) vtv[a] = tot[NP + QB + a] + tot[QB + a] * inv0;
+        __syncthreads();
+        // ---- T column j (warp 0; identical in every CTA, CTA 0 stores it)
+        if (warp == 0) {
+            double t = 0.0;
+            if (lane < j)
+                for (int b = lane; b < j; ++b) t += T[lane][b] * vtv[b];
+            __syncwarp();
+            if (lane < j) T[lane][j] = -beta * t;
+            if (lane == j) T[j][j] = beta;
+            if (lane > j) T[lane][j] = 0.0;
+        }
+        // ---- update my rows: column j -> v (mu at row j), columns c > j -= beta w_c v
+        double* colw = sm + j * rp;
         for (int i = threadIdx.x; i < nr; i += blockDim.x) {
             const int gi = r0 + i;
-            const double vi = gi < j ? 0.0 : (gi == j ? 1.0 : col[i] * inv0);
-            vg[gi] = vi;
-            if (gi > j) col[i] = vi;                    // keep v in the slice (below the diagonal)
-            else if (gi == j) col[i] = mu;
-        }
-        if (threadIdx.x == 0) s_beta[j] = beta;        // identical in every CTA of the cluster
-        __syncthreads();
-        // (3) partial dots w_c = sum_{rows >= j} v_i A_ic for c > j
-        for (int c = j + 1 + warp; c < jb; c += 8) {
-            const double* cc = sm + c * rp;
-            double w = 0.0;
-            for (int i = lane; i < nr; i += 32) {
-                const int gi = r0 + i;
-                if (gi >= j) w += (gi == j ? 1.0 : col[i]) * cc[i];
-            }
-            w = warp_sum(w);
-            if (lane == 0) part[1][c] = w;
-        }
-        cluster.sync();
-        for (int c = j + 1 + warp; c < jb; c += 8) {
-            double w = lane < QCL ? cluster.map_shared_rank(&part[1][0], lane)[c] : 0.0;
-            w = warp_sum(w) * beta;
-            double* cc = sm + c * rp;
-            for (int i = lane; i < nr; i += 32) {
-                const int gi = r0 + i;
-                if (gi >= j) cc[i] -= w * (gi == j ? 1.0 : col[i]);
-            }
+            const double vi = gi < j ? 0.0 : (gi == j ? 1.0 : colw[i] * inv0);
+            for (int c = j + 1; c < jb; ++c) sm[i + c * rp] -= beta * wc[c] * vi;
+            if (gi > j) colw[i] = vi;
+            else if (gi == j) colw[i] = mu;
+            d.V[(size_t)j * d.ldv + gi] = vi;
         }
         __syncthreads();
     }
+    qr_tr(4);
     // write the R part (rows <= column) back; the rest of the slice is scratch
-    for (int e = threadIdx.x; e < rp * jb; e += blockDim.x) {
-        const int i = e % rp, c = e / rp;
-        if (i < nr && r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
-    }
-    // T = compact-WY factor from V^T V: partial Gram of my slice (v_a = 0 above a,
-    // 1 at a, slice value below), cluster-reduced in parallel by CTA 0
-    for (int pr = warp; pr < jb * jb; pr += 8) {
-        const int a = pr % jb, b = pr / jb;
-        if (a >= b) continue;
-        double s = 0.0;
-        for (int i = lane; i < nr; i += 32) {
-            const int gi = r0 + i;
-            if (gi < b) continue;
-            const double vb = (gi == b) ? 1.0 : sm[i + b * rp];
-            const double va = sm[i + a * rp];          // gi >= b > a: below a's diagonal
-            s += va * vb;
-        }
-        s = warp_sum(s);
-        if (lane == 0) Gp[a][b] = s;
-    }
-    cluster.sync();
-    if (g == 0) {
-        for (int pr = threadIdx.x; pr < jb * jb; pr += blockDim.x) {
-            const int a = pr % jb, b = pr / jb;
-            if (a >= b) continue;
-            double s = 0.0;
-            for (int q = 0; q < QCL; ++q) s += cluster.map_shared_rank(&Gp[0][0], q)[a * (QB + 1) + b];
-            Gs[a][b] = s;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double* T = d.T;
-            for (int j = 0; j < jb; ++j) {
-                for (int a = 0; a < j; ++a) {
-                    double s = 0.0;
-                    for (int b = a; b < j; ++b) s += T[a + b * QB] * Gs[b][j];
-                    T[a + j * QB] = -s_beta[j] * s;
-                }
-                T[j + j * QB] = s_beta[j];
-                for (int a = j + 1; a < QB; ++a) T[a + j * QB] = 0.0;
-            }
-        }
-    }
+    for (int c = 0; c < jb; ++c)
+        for (int i = threadIdx.x; i < nr; i += blockDim.x)
+            if (r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
+    if (g == 0)
+        for (int e = threadIdx.x; e < QB * QB; e += blockDim.x) d.T[e] = T[e % QB][e / QB];
+    qr_tr(5);
+    qr_tr(6);
     cluster.sync();                                   // keep smem alive for remote readers
 }
 
@@ -1039,6 +1036,15 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
                 if (qcl == 8) SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<8>, (const PanelDesc*)dp.p, rp));
                 else SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<16>, (const PanelDesc*)dp.p, rp));
                 count_launch();
+                static const bool trace = getenv("SPD_QR_TRACE") != nullptr;
+                if (trace && p == 0) {
+                    unsigned long long tr[8];
+                    SPD_CUDA(cudaStreamSynchronize(s));
+                    SPD_CUDA(cudaMemcpyFromSymbol(tr, g_qr_trace, sizeof(tr)));
+                    fprintf(stderr, "[qr trace] panels %zu qcl %d rp %d: load %.1f col0 %.1f cols1-15 %.1f cols16-31 %.1f "
+                            "gram %.1f T %.1f us\n", pd.size(), qcl, rp, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3,
+                            (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3, (tr[5] - tr[4]) * 1e-3, (tr[6] - tr[5]) * 1e-3);
+                }
             } else {
                 panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);
                 SPD_LAUNCH();
