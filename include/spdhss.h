@@ -71,8 +71,22 @@ typedef struct {
     double seconds;          /* wall time of the solve (host clock)       */
 } spd_pcg_report;
 
-/* Communicator for multi-GPU runs.  Round 1: nranks must be 1 (the data-path
- * collectives of SURVEY.md §8(e) are not built yet); pass NULL id. */
+/* Communicator for multi-GPU runs (NCCL over NVLink/NVSwitch,
+ * loaded at run time from libnccl.so.2).  One process per GPU; every rank calls
+ * with identical global arguments and the points replicated.
+ *   spd_comm_unique_id: rank 0 creates the 128-byte NCCL id (host buffer) and
+ *                       shares it (e.g. torch.distributed.broadcast_object_list).
+ *   spd_comm_init:      nranks a power of 2; id NULL with nranks == 1 (single
+ *                       GPU) or nranks > 1 (a "virtual" communicator: the sharded
+ *                       code path emulated in one process on one GPU -- tests).
+ * Sharding (h2_build): rank p computes the nodes of subtree p at every level with
+ * >= nranks nodes (p count/P .. (p+1) count/P - 1), levels with fewer nodes are
+ * computed redundantly; after each sharded level the owners' contiguous ranges of
+ * the level arrays are broadcast (ncclBroadcast group = an all-gather of variable
+ * size) and the ranks all-reduced, so every rank ends with the full H2.  The
+ * caller owns the communicator; handles keep a reference (free them first).
+ * Errors: SPD_EINVAL (bad nranks / rank), SPD_ENCCL (library or NCCL failure). */
+spd_status spd_comm_unique_id(void* nccl_unique_id_out);
 spd_status spd_comm_init(const void* nccl_unique_id, int nranks, int rank, spd_comm_t* out);
 void spd_comm_free(spd_comm_t c);
 

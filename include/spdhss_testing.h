@@ -24,6 +24,9 @@ spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t str
 spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int64_t stride, void* stream);
 /* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major */
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
+/* subtree-sharding plan (host logic only, no GPU): owner rank of node a of a level
+ * with `count` nodes for nranks ranks, -1 when the level is computed redundantly */
+int spd_test_shard_owner(int nranks, int count, int a);
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,8 @@ def lib():
     sigs = {
         "spd_last_error": ([], ctypes.c_char_p),
         "spd_comm_init": ([vp, c_int, c_int, P(vp)], c_int),
+        "spd_comm_unique_id": ([vp], c_int),
+        "spd_test_shard_owner": ([c_int, c_int, c_int], c_int),
         "spd_comm_free": ([vp], None),
         "h2_build": ([vp, i64, c_int, _Kernel, c_int, c_double, P(_H2Opts), vp, vp, P(vp)], c_int),
         "h2_matvec": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
@@ -91,7 +93,7 @@ def lib():
     return L
 
 
-EXPORTED = ["spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
+EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
             "pcg_solve", "spd_query", "h2_free", "hss_free", "spd_last_error"]
 
 
@@ -214,16 +216,49 @@ def _proxies(h, node, n_proxy=None):
     return out
 
 
-def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0):
-    """points: CUDA float64 (n, d) row-major, original order."""
+class Comm:
+    """Communicator (spd_comm_init).  Caller-owned; keep it alive while handles use it."""
+
+    def __init__(self, nranks=1, rank=0, unique_id=None):
+        self.ptr = ctypes.c_void_p()
+        uid = None
+        if unique_id is not None:
+            uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().spd_comm_init(uid, int(nranks), int(rank), ctypes.byref(self.ptr)))
+        self.nranks, self.rank = nranks, rank
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.spd_comm_free(self.ptr)
+            self.ptr = None
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (rank 0), to be shared with the other ranks."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().spd_comm_unique_id(buf))
+    return buf.raw
+
+
+def shard_owner(nranks, count, a):
+    """Owner rank of node a of a level with `count` nodes (-1: computed by every rank)."""
+    return int(lib().spd_test_shard_owner(int(nranks), int(count), int(a)))
+
+
+def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0, comm=None):
+    """points: CUDA float64 (n, d) row-major, original order.  comm: optional Comm
+    (subtree-sharded build; every rank ends with the full H2)."""
     if points.dim() != 2 or not points.is_contiguous():
         raise ValueError("points must be a contiguous (n, d) tensor")
     n, d = points.shape
     out = ctypes.c_void_p()
     opts = _H2Opts(int(n_proxy), 0)
     _check(lib().h2_build(_dptr(points, "points"), n, d, _Kernel(int(kernel_id), float(ell), float(shift)),
-                          int(leaf), float(tol), ctypes.byref(opts), None, _stream(), ctypes.byref(out)))
-    return H2(out, n, d)
+                          int(leaf), float(tol), ctypes.byref(opts), comm.ptr if comm is not None else None,
+                          _stream(), ctypes.byref(out)))
+    h = H2(out, n, d)
+    h._comm = comm            # keep the communicator alive as long as the handle
+    return h
 
 
 def h2_matvec(h2, X, layout=LAYOUT_ORIGINAL, out=None):

@@ -5,6 +5,7 @@
 #include <string>
 #include "h2.hpp"
 #include "hss.hpp"
+#include "comm.hpp"
 #include "../../include/spdhss_testing.h"
 
 namespace spd {
@@ -12,7 +13,6 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
 }  // namespace spd
 
-struct spd_comm_s { int nranks, rank; };
 
 using namespace spd;
 
@@ -26,15 +26,26 @@ extern "C" {
 
 const char* spd_last_error(void) { return g_last_error.c_str(); }
 
+spd_status spd_comm_unique_id(void* out128) {
+    SPD_TRY({
+        SPD_REQUIRE(out128 != nullptr, "spd_comm_unique_id: out is NULL");
+        comm_unique_id(out128);
+    })
+}
+
 spd_status spd_comm_init(const void* id, int nranks, int rank, spd_comm_t* out) {
     SPD_TRY({
         SPD_REQUIRE(out != nullptr, "spd_comm_init: out is NULL");
-        SPD_REQUIRE(nranks == 1 && rank == 0 && id == nullptr,
-                    "spd_comm_init: only nranks == 1 is supported in this build (subtree sharding not built)");
-        *out = new spd_comm_s{nranks, rank};
+        *out = comm_create(id, nranks, rank);
     })
 }
-void spd_comm_free(spd_comm_t c) { delete c; }
+void spd_comm_free(spd_comm_t c) { comm_destroy(c); }
+
+int spd_test_shard_owner(int nranks, int count, int a) {
+    spd_comm_s c;
+    c.nranks = nranks;
+    return shard_owner(&c, count, a);
+}
 
 spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf, double tol,
                     const spd_h2_opts* opts, spd_comm_t c, void* stream, spd_h2_t* out) {

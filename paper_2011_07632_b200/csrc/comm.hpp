@@ -1,0 +1,27 @@
+// comm.hpp -- communicator of libspdhss (NCCL, loaded at run time; comm.cpp).
+#pragma once
+#include <vector>
+#include "common.cuh"
+
+struct spd_comm_s {
+    int nranks = 1, rank = 0;
+    bool virt = false;          // single-process emulation of nranks ranks (tests)
+    void* nccl = nullptr;       // ncclComm_t
+};
+
+namespace spd {
+
+struct Nccl128 { char b[128]; };   // ncclUniqueId
+
+void comm_unique_id(void* out128);
+spd_comm_s* comm_create(const void* id, int nranks, int rank);
+void comm_destroy(spd_comm_s* c);
+// owner rank of node a (0 <= a < count) of a level, -1 when the level is redundant
+int shard_owner(const spd_comm_s* c, int count, int a);
+// every rank q broadcasts elements [begin[q], end[q]) of buf (elem bytes each), in one group
+void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::vector<int64_t>& begin,
+                       const std::vector<int64_t>& end, cudaStream_t s);
+void comm_allreduce_sum(const spd_comm_s* c, double* buf, size_t n, cudaStream_t s);
+void comm_allreduce_sum(const spd_comm_s* c, int* buf, size_t n, cudaStream_t s);
+
+}  // namespace spd

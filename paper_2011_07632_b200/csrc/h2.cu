@@ -11,6 +11,7 @@
 // xh_i = E_i^T [x_i | xh_children] (batched DMMA GEMM), Type-3 coupling on the
 // fly (kblock over skeleton points), down pass, leaf accumulation.
 #include "h2.hpp"
+#include "comm.hpp"
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -243,13 +244,21 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         rank_d.zero(s);
         DBuf<double> beta_d(std::max<int64_t>(1, piv_off[lv.count]));
         DBuf<double> norms_d(std::max<int64_t>(1, piv_off[lv.count]));
-        // process in chunks bounded by the proxy-matrix budget
+        // subtree sharding (comm.cpp): a rank computes the nodes of its subtree at levels
+        // with >= P nodes (all nodes at the redundant top levels); a virtual communicator
+        // computes every virtual rank's share in turn in this process
+        const spd_comm_s* cm = h->comm;
+        const int P = cm ? cm->nranks : 1;
+        const bool sharded = P > 1 && lv.count >= P;
+        // process in chunks bounded by the proxy-matrix budget, one rank's nodes per chunk
         struct Chunk { std::vector<int> nodes; };
         std::vector<Chunk> chunks;
-        {
+        for (int q = 0; q < (sharded && cm->virt ? P : 1); ++q) {
+            const int me = !sharded ? -1 : (cm->virt ? q : cm->rank);
             Chunk cur;
             size_t bytes = 0;
             for (int a : nodes) {
+                if (me >= 0 && shard_owner(cm, lv.count, a) != me) continue;
                 size_t b = (size_t)n_p * lv.ncand[a] * 8 + (size_t)n_p * d * 8;
                 if (!cur.nodes.empty() && bytes + b > budget) { chunks.push_back(cur); cur = Chunk(); bytes = 0; }
                 cur.nodes.push_back(a);
@@ -372,6 +381,14 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             SPD_CUDA(cudaStreamSynchronize(s));   // Mt, P freed at scope exit
             stage_mark(s, "h2 trsm+id", k);
         }
+        // sharded level: every rank learns all ranks (the owners' entries, the others 0)
+        if (sharded && !cm->virt) {
+            comm_allreduce_sum(cm, rank_d.p, (size_t)lv.count, s);
+            std::vector<int> rk(lv.count + 1);
+            SPD_CUDA(cudaMemcpyAsync(rk.data(), rank_d.p, sizeof(int) * (lv.count + 1), cudaMemcpyDeviceToHost, s));
+            SPD_CUDA(cudaStreamSynchronize(s));
+            for (int a = 0; a < lv.count; ++a) rank_h[a] = rk[a];
+        }
         // pack level arrays
         for (int a = 0; a < lv.count; ++a) {
             lv.rank[a] = rank_h[a];
@@ -399,6 +416,28 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             SPD_CUDA(cudaMemcpyAsync(lv.skel.p + lv.off[a], pe.skel.p, sizeof(int) * sr, cudaMemcpyDeviceToDevice, s));
             SPD_CUDA(cudaMemcpy2DAsync(lv.skelX.p + lv.off[a], sizeof(double) * lv.S, pe.sx.p, sizeof(double) * sr,
                                        sizeof(double) * sr, d, cudaMemcpyDeviceToDevice, s));
+        }
+        // sharded level: the owners' contiguous node ranges of every level array are
+        // broadcast (one NCCL group = an all-gather of variable-size ranges)
+        if (sharded && !cm->virt) {
+            std::vector<int64_t> eb(P), ee(P), tb(P), te(P), sb(P), se(P), pb(P), pe_(P);
+            const int per = lv.count / P;
+            for (int q = 0; q < P; ++q) {
+                const int a0 = q * per, a1 = (q + 1) * per;
+                eb[q] = lv.E_off[a0]; ee[q] = lv.E_off[a1];
+                tb[q] = lv.T_off[a0]; te[q] = lv.T_off[a1];
+                sb[q] = lv.off[a0]; se[q] = lv.off[a1];
+                pb[q] = lv.piv_off[a0]; pe_[q] = lv.piv_off[a1];
+            }
+            comm_bcast_ranges(cm, lv.E.p, sizeof(double), eb, ee, s);
+            comm_bcast_ranges(cm, lv.T.p, sizeof(double), tb, te, s);
+            comm_bcast_ranges(cm, lv.skel.p, sizeof(int), sb, se, s);
+            comm_bcast_ranges(cm, lv.piv.p, sizeof(int), pb, pe_, s);
+            for (int a = 0; a < d; ++a) {
+                std::vector<int64_t> xb(P), xe(P);
+                for (int q = 0; q < P; ++q) { xb[q] = a * lv.S + sb[q]; xe[q] = a * lv.S + se[q]; }
+                comm_bcast_ranges(cm, lv.skelX.p, sizeof(double), xb, xe, s);
+            }
         }
         SPD_CUDA(cudaStreamSynchronize(s));
         stage_mark(s, "h2 pack (+free)", k);
