@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: ONE problem, H2 build sharded by subtrees over NCCL (strong scaling); "
+                         "default: independent replicas (weak scaling)")
     return ap.parse_args()
 
 
@@ -215,6 +218,11 @@ def run_ours(args):
         dist.init_process_group("nccl", rank=rank, world_size=world)
     torch.cuda.set_device(local)
     lib = spd.lib()
+    comm = None
+    if args.shard and world > 1:
+        uid = [spd.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = spd.Comm(world, rank, uid[0])
     cfg = replica_config(rank) if not args.n else CFG.scaled(args.n)
     N = cfg.n
     X_h = synth.points(cfg)
@@ -231,7 +239,7 @@ def run_ours(args):
     def step(points, rhs, record=None):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
-        h = spd.h2_build(points, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+        h = spd.h2_build(points, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol, comm=comm)
         ev[1].record(stream)
         H = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, seed=1234)
         ev[2].record(stream)
@@ -345,9 +353,11 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 2), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if comm is not None else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": WORKLOAD, "l2_flush": "256 MB write between steps",
-                   "parallelism": "replicas" if world > 1 else "single GPU", "N": N},
+                   "parallelism": ("h2_build sharded by subtrees over NCCL, HSS build + PCG replicated"
+                                   if comm is not None else "replicas") if world > 1 else "single GPU", "N": N},
         "breakdown": {k: round(statistics.mean(r[k] for r in recs), 4)
                       for k in ("h2_build_s", "spdhss_build_s", "pcg_s", "h2_mv_s")},
         "full_build_s": round(statistics.mean(r["h2_build_s"] + r["spdhss_build_s"] for r in recs), 4),
