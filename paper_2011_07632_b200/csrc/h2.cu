@@ -592,13 +592,12 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         return;
     }
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
-    // near field
-    {
-        std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
-        near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
+    std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
+    near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
+    if (L == 1) {
         kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
+        return;
     }
-    if (L == 1) return;
     ensure_ws(h, k, s);
     std::vector<double*> xh(L, nullptr), yh(L, nullptr);
     for (int lk = 1; lk < L; ++lk) {
@@ -607,29 +606,30 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].S * k, s));
     }
     h2_up(h, x, ldx, k, xh, L - 1, s);
-    // Type-3 coupling per level
+    // near field and the Type-3 couplings of every level in ONE launch (one balanced
+    // work list; skeleton blocks carry no ids, so the shift only reaches near blocks)
     for (int lk = 1; lk < L; ++lk) {
         const H2Level& lv = h->lv[lk];
         if (h->lists.type3[lk].empty()) continue;
-        std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
+        const int b0 = (int)blocks.size();
         for (int a = 0; a < lv.count; ++a)
             blocks.push_back({lv.skelX.p + lv.off[a], lv.S, lv.rank[a], -1});
         const auto& T3 = h->lists.type3[lk];
         size_t e = 0;
         while (e < T3.size()) {
             const int i = T3[e].first, a = i - lv.first;
-            KbTarget tg{a, (int)entries.size(), 0};
+            KbTarget tg{b0 + a, (int)entries.size(), 0};
             while (e < T3.size() && T3[e].first == i) {
                 const int bj = T3[e].second - lv.first;
                 if (lv.rank[bj] > 0 && lv.rank[a] > 0)
-                    entries.push_back({bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
+                    entries.push_back({b0 + bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
                 ++e;
             }
             tg.e_end = (int)entries.size();
             targets.push_back(tg);
         }
-        kblock_apply(s, h->kp, 0.0, h->d, blocks, targets, entries);
     }
+    kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
     h2_down(h, yh, L - 1, y, ldy, k, s);
 }
 

@@ -11,12 +11,16 @@
 #include "common.cuh"
 #include "kblock.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace spd {
 
-constexpr int KB_M = 64, KB_K = 16;
+constexpr int KB_M = 64, KB_K = 16;   // simple kernel: 64-row tiles, 16-source chunks
 
-struct KbWork { int target, tm, tn; };
+// work item: target row tile tm, column tile tn, entries [eb, ee) of the target;
+// pslot >= 0: the tile is a segment of a split target, its sum goes to partial slot
+// pslot (64 x NC, ld 64) and kb_reduce_kernel adds the segments in order into Y
+struct KbWork { int target, tm, tn, eb, ee, pslot; };
 
 template <int KID>
 __device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
@@ -32,22 +36,23 @@ __device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
 // with the 16 x NC slice of X; the next chunk's X slice and coordinates are
 // prefetched into registers while the current chunk is evaluated/contracted.
 template <int KID, int NC>
-__global__ void __launch_bounds__(2 * NC) kblock_kernel(
+__global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
     KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
     const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
-    const KbWork* __restrict__ work) {
+    const KbWork* __restrict__ work, double* __restrict__ partial) {
     constexpr int NT = 2 * NC;                  // threads
     constexpr int WN = NC / 32;                 // warps along columns
     constexpr int XPT = KB_K * NC / NT;         // X values per thread per chunk (= 8)
     constexpr int EPT = KB_M * KB_K / NT;       // kernel evaluations per thread per chunk
-    __shared__ double Ks[KB_K][KB_M + 1];
-    __shared__ double Xs[KB_K][NC + 1];
+    __shared__ double Ks[KB_K][KB_M + 8];            // row stride = 8 (mod 16) doubles: fragment reads in 2 wavefronts
+    __shared__ double Xs[NC][KB_K + 4];              // kc contiguous: conflict-free writes and reads
     __shared__ double Sx[3][KB_K];
     const KbWork wk = work[blockIdx.x];
     const KbTarget tg = targets[wk.target];
     const KbBlock tb = blocks[tg.blk];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, q = lane & 3, wm = warp / WN, wn = warp % WN;
+    double* part = wk.pslot >= 0 ? partial + (size_t)wk.pslot * KB_M * NC : nullptr;
     const int r0 = wk.tm * KB_M, c0 = wk.tn * NC;
     const int nrows = min(KB_M, tb.n - r0);
     const int er = tid & (KB_M - 1), ec0 = (tid / KB_M) * EPT;
@@ -63,7 +68,7 @@ __global__ void __launch_bounds__(2 * NC) kblock_kernel(
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
     double xr[XPT], sr = 0.0;
-    for (int e = tg.e_begin; e < tg.e_end; ++e) {
+    for (int e = wk.eb; e < wk.ee; ++e) {
         const KbEntry en = entries[e];
         if (c0 < en.ncols) {
             const KbBlock sb = blocks[en.src];
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(2 * NC) kblock_kernel(
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
                     const int idx = tid + u * NT;
-                    Xs[idx % KB_K][idx / KB_K] = xr[u];
+                    Xs[idx / KB_K][idx % KB_K] = xr[u];
                 }
                 if (tid < KB_K * 3) Sx[tid / KB_K][tid % KB_K] = sr;
                 __syncthreads();
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(2 * NC) kblock_kernel(
 #pragma unroll
                     for (int a = 0; a < 4; ++a) af[a] = Ks[ks * 4 + q][wm * 32 + a * 8 + g];
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) bf[b] = Xs[ks * 4 + q][wn * 32 + b * 8 + g];
+                    for (int b = 0; b < 4; ++b) bf[b] = Xs[wn * 32 + b * 8 + g][ks * 4 + q];
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -117,9 +122,19 @@ __global__ void __launch_bounds__(2 * NC) kblock_kernel(
                 }
             }
         }
-        const bool flush = (e + 1 == tg.e_end) || entries[e + 1].Y != en.Y;
+        const bool flush = (e + 1 == wk.ee) || entries[e + 1].Y != en.Y;
         if (flush) {
-            if (c0 < en.ncols) {
+            if (part) {                       // segment of a split target: raw tile to its slot
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            int i = wm * 32 + a * 8 + g, j = wn * 32 + b * 8 + 2 * q + h;
+                            part[i + (size_t)j * KB_M] = acc[a][b][h];
+                        }
+            } else if (c0 < en.ncols) {
                 const int ncols = min(NC, en.ncols - c0);
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
@@ -136,6 +151,20 @@ __global__ void __launch_bounds__(2 * NC) kblock_kernel(
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         }
+    }
+}
+
+// split targets: Y[tile] += sum of its segments' partial tiles, in segment order
+struct KbRed { double* Y; int ldy, nrows, ncols, p0, np; };
+template <int NC>
+__global__ void kb_reduce_kernel(const KbRed* __restrict__ red, const double* __restrict__ partial) {
+    const KbRed r = red[blockIdx.x];
+    for (int e = threadIdx.x; e < KB_M * NC; e += blockDim.x) {
+        const int i = e % KB_M, j = e / KB_M;
+        if (i >= r.nrows || j >= r.ncols) continue;
+        double s = 0.0;
+        for (int p = 0; p < r.np; ++p) s += partial[(size_t)(r.p0 + p) * KB_M * NC + e];
+        r.Y[i + (size_t)j * r.ldy] += s;
     }
 }
 
@@ -272,22 +301,67 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     int maxc_all = 0;
     for (auto& e : entries) maxc_all = std::max(maxc_all, e.ncols);
     const int NC = maxc_all > 64 ? 128 : 64;
+    // work items; a target whose entries (one output group) hold many more source
+    // points than the average item is cut into segments at entry boundaries, so the
+    // long top-level coupling lists spread over many CTAs (ordered reduction after)
+    std::vector<long long> cost(targets.size(), 0);
+    long long total_cost = 0, ntile_all = 0;
+    for (int t = 0; t < (int)targets.size(); ++t) {
+        for (int e = targets[t].e_begin; e < targets[t].e_end; ++e) cost[t] += blocks[entries[e].src].n;
+        const long long tiles = (long long)ceil_div(blocks[targets[t].blk].n, KB_M);
+        total_cost += cost[t] * tiles;
+        ntile_all += tiles;
+    }
+    const long long seg = std::max<long long>(1024, total_cost / std::max<long long>(1, 148LL * 8));
     std::vector<KbWork> work;
+    std::vector<KbRed> red;
+    int nslot = 0;
     for (int t = 0; t < (int)targets.size(); ++t) {
         const KbTarget& tg = targets[t];
         if (tg.e_end <= tg.e_begin) continue;
         int maxc = 0;
-        for (int e = tg.e_begin; e < tg.e_end; ++e) maxc = std::max(maxc, entries[e].ncols);
+        bool one_group = true;
+        for (int e = tg.e_begin; e < tg.e_end; ++e) {
+            maxc = std::max(maxc, entries[e].ncols);
+            if (entries[e].Y != entries[tg.e_begin].Y || entries[e].ncols != entries[tg.e_begin].ncols) one_group = false;
+        }
         const int nr = blocks[tg.blk].n;
+        // segment boundaries
+        std::vector<int> cuts{tg.e_begin};
+        if (one_group && cost[t] > 2 * seg) {
+            long long acc = 0;
+            for (int e = tg.e_begin; e < tg.e_end; ++e) {
+                acc += blocks[entries[e].src].n;
+                if (acc >= seg && e + 1 < tg.e_end) { cuts.push_back(e + 1); acc = 0; }
+            }
+        }
+        cuts.push_back(tg.e_end);
+        const int nseg = (int)cuts.size() - 1;
         for (int tn = 0; tn < ceil_div(maxc, NC); ++tn)
-            for (int tm = 0; tm < ceil_div(nr, KB_M); ++tm) work.push_back({t, tm, tn});
+            for (int tm = 0; tm < ceil_div(nr, KB_M); ++tm) {
+                if (nseg == 1) { work.push_back({t, tm, tn, tg.e_begin, tg.e_end, -1}); continue; }
+                const KbEntry& e0 = entries[tg.e_begin];
+                red.push_back({e0.Y + tm * KB_M + (size_t)tn * NC * e0.ldy, e0.ldy, std::min(KB_M, nr - tm * KB_M),
+                               std::min(NC, e0.ncols - tn * NC), nslot, nseg});
+                for (int sg = 0; sg < nseg; ++sg) work.push_back({t, tm, tn, cuts[sg], cuts[sg + 1], nslot++});
+            }
     }
     if (work.empty()) return;
-    // heaviest tiles first (crude LPT over the launch order)
-    std::vector<long long> cost(targets.size(), 0);
-    for (int t = 0; t < (int)targets.size(); ++t)
-        for (int e = targets[t].e_begin; e < targets[t].e_end; ++e) cost[t] += blocks[entries[e].src].n;
-    std::stable_sort(work.begin(), work.end(), [&](const KbWork& a, const KbWork& b) { return cost[a.target] > cost[b.target]; });
+    // heaviest items first (crude LPT over the launch order)
+    auto wcost = [&](const KbWork& w) {
+        long long c = 0;
+        for (int e = w.eb; e < w.ee; ++e) c += blocks[entries[e].src].n;
+        return c;
+    };
+    std::vector<std::pair<long long, int>> order;
+    for (int i = 0; i < (int)work.size(); ++i) order.push_back({-wcost(work[i]), i});
+    std::stable_sort(order.begin(), order.end());
+    {
+        std::vector<KbWork> sorted;
+        for (auto& o : order) sorted.push_back(work[o.second]);
+        work.swap(sorted);
+    }
+    DBuf<double> partial(std::max<size_t>(1, (size_t)nslot * KB_M * NC));
     double fl = 0, by = 0;
     for (const auto& tg : targets)
         for (int e = tg.e_begin; e < tg.e_end; ++e) {
@@ -301,9 +375,9 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     DevArray<KbWork> dw(s, work);
     ProfScope prof(s, "kblock_dmma", fl, by);
     const unsigned nb = (unsigned)work.size();
-#define SPD_KB_LAUNCH(KID)                                                                               \
-    if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);    \
-    else kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p);
+#define SPD_KB_LAUNCH(KID)                                                                                    \
+    if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
+    else kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
     switch (kp.id) {
     case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
     case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
@@ -312,6 +386,12 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     }
 #undef SPD_KB_LAUNCH
     SPD_LAUNCH();
+    if (!red.empty()) {
+        DevArray<KbRed> dr(s, red);
+        if (NC == 128) kb_reduce_kernel<128><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        else kb_reduce_kernel<64><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        SPD_LAUNCH();
+    }
 }
 
 }  // namespace spd
