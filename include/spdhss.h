@@ -130,6 +130,13 @@ spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, doub
 spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x,
                      double tol, int maxit, spd_pcg_report* rep, void* stream);
 
+/* pcg_solve_bj: the same PCG with the block-Jacobi preconditioner built from M's leaf
+ * Cholesky factors, x_i = A_ii^{-1} b_i (the paper's BJ baseline, P:1216,
+ * SPD-HSS "combines a BJ preconditioner with off-diagonal
+ * approximations").  M must not be NULL (SPD_EINVAL). */
+spd_status pcg_solve_bj(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x, double tol, int maxit,
+                        spd_pcg_report* rep, void* stream);
+
 /* Introspection (host buffers).  `what` selects:                            */
 enum {
     SPD_Q_N = 1,            /* int64: n                                       */

@@ -16,6 +16,8 @@ hss_matvec        HSS apply: leaf D_i, U_i; transfers R_i; sibling B_ij
 hss_solve         recursive solve of reading R12:
                   H^{-1} = S^{-T}[(I - V V^T) + V (I+H_2)^{-1} V^T] S^{-1}.
 pcg               textbook PCG, x0 = 0, stop on ||r_k|| <= tol ||b|| (R15).
+block_jacobi_solve  the BJ baseline preconditioner:
+                  x_i = A_ii^{-1} b_i over the leaves, A_ii = K(X_i, X_i) + sigma I.
 hss_error         Fig. 5 metric: mean over probes of
                   ||H_hss x - H_h2 x|| / ||H_h2 x||.
 """
@@ -263,6 +265,20 @@ def hss_solve(hss: HSS, b):
         v = res[i] + hss.V[i] @ xh[i]
         x[t.begin[i]:t.end[i]] = solve_triangular(hss.S[i].T, v, lower=False) if v.shape[0] else v
     return x[:, 0] if vec else x
+
+
+def block_jacobi_solve(h2: H2, b):
+    """Block-Jacobi preconditioner: x_i = A_ii^{-1} b_i for every leaf i, by the
+    Cholesky factor of A_ii (SPD-HSS = BJ's diagonal blocks + off-diagonal
+    approximations).  b, x in tree order."""
+    t = h2.tree
+    b = np.asarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    for i in t.nodes_at(1):
+        rows = np.arange(t.begin[i], t.end[i])
+        S = cholesky(h2.K(rows, rows), where=f"leaf {i}")
+        x[rows] = solve_triangular(S, solve_triangular(S, b[rows], lower=True), lower=True, trans="T")
+    return x
 
 
 def pcg(apply_A, apply_M, b, tol, maxit):

@@ -69,6 +69,7 @@ def lib():
         "spdhss_build": ([vp, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp)], c_int),
         "hss_solve": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
         "pcg_solve": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
+        "pcg_solve_bj": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
         "spd_query": ([vp, c_int, vp, ctypes.c_size_t], c_int),
         "h2_free": ([vp], None),
         "hss_free": ([vp], None),
@@ -94,7 +95,7 @@ def lib():
 
 
 EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
-            "pcg_solve", "spd_query", "h2_free", "hss_free", "spd_last_error"]
+            "pcg_solve", "pcg_solve_bj", "spd_query", "h2_free", "hss_free", "spd_last_error"]
 
 
 def _check(status):
@@ -319,11 +320,13 @@ def hss_solve(hss, B, layout=LAYOUT_ORIGINAL, out=None):
     return out
 
 
-def pcg_solve(h2, hss, b, tol=1e-8, maxit=3000, layout=LAYOUT_ORIGINAL, x=None):
-    """Returns (x, PcgReport).  hss=None: unpreconditioned CG."""
+def pcg_solve(h2, hss, b, tol=1e-8, maxit=3000, layout=LAYOUT_ORIGINAL, x=None, precond="hss"):
+    """Returns (x, PcgReport).  hss=None: unpreconditioned CG.  precond="bj": block
+    Jacobi from the SPD-HSS leaf factors (the paper's BJ baseline)."""
     if x is None:
         x = b.new_zeros(b.shape)
     rep = PcgReport()
-    _check(lib().pcg_solve(h2.ptr, hss.ptr if hss is not None else None, layout, _dptr(b, "b"),
-                           _dptr(x, "x"), float(tol), int(maxit), ctypes.byref(rep), _stream()))
+    fn = lib().pcg_solve_bj if precond == "bj" else lib().pcg_solve
+    _check(fn(h2.ptr, hss.ptr if hss is not None else None, layout, _dptr(b, "b"),
+              _dptr(x, "x"), float(tol), int(maxit), ctypes.byref(rep), _stream()))
     return x, rep

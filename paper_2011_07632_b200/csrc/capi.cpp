@@ -137,8 +137,8 @@ spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, doub
     })
 }
 
-spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x, double tol, int maxit,
-                     spd_pcg_report* rep, void* stream) {
+static spd_status pcg_common(spd_h2_t A, spd_hss_t M, int precond, int layout, const double* b, double* x,
+                             double tol, int maxit, spd_pcg_report* rep, void* stream) {
     spd_pcg_report local{};
     if (!rep) rep = &local;
     try {
@@ -150,11 +150,11 @@ spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, doubl
         cudaStream_t s = (cudaStream_t)stream;
         const int64_t N = A->N;
         if (layout == SPD_LAYOUT_TREE) {
-            pcg_tree(A, M, b, x, tol, maxit, rep, s);
+            pcg_tree(A, M, b, x, tol, maxit, rep, s, precond);
         } else {
             DBuf<double> bt(N), xt(N);
             permute_rows(s, A->perm.p, N, 1, b, N, bt.p, N, true);
-            pcg_tree(A, M, bt.p, xt.p, tol, maxit, rep, s);
+            pcg_tree(A, M, bt.p, xt.p, tol, maxit, rep, s, precond);
             permute_rows(s, A->perm.p, N, 1, xt.p, N, x, N, false);
         }
         if (!rep->converged) {
@@ -164,6 +164,17 @@ spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, doubl
         return SPD_OK;
     } catch (const spd::Error& e) { set_last_error(e.what()); return e.code; }
     catch (const std::exception& e) { set_last_error(e.what()); return SPD_ECUDA; }
+}
+
+spd_status pcg_solve(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x, double tol, int maxit,
+                     spd_pcg_report* rep, void* stream) {
+    return pcg_common(A, M, PC_HSS, layout, b, x, tol, maxit, rep, stream);
+}
+
+spd_status pcg_solve_bj(spd_h2_t A, spd_hss_t M, int layout, const double* b, double* x, double tol, int maxit,
+                        spd_pcg_report* rep, void* stream) {
+    if (!M) { set_last_error("pcg_solve_bj: needs the SPD-HSS handle (its leaf factors)"); return SPD_EINVAL; }
+    return pcg_common(A, M, PC_BJ, layout, b, x, tol, maxit, rep, stream);
 }
 
 static size_t need(size_t have, size_t want) {

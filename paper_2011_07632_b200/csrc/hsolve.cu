@@ -134,6 +134,37 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
     return out;
 }
 
+// Block-Jacobi preconditioner (the paper's BJ baseline): x_i =
+// A_ii^{-1} b_i = S_i^{-T} S_i^{-1} b_i with the leaf Cholesky factors of the SPD-HSS
+// build -- its diagonal blocks without the off-diagonal approximation.  Two phases:
+// u0 = S^{-1} b (kind 0), x = S^{-T} u0 (kind 2 without coarse term).
+std::vector<HsPhase> bj_solve_plan(const spd_hss_s* H, const double* b, double* x, double* z) {
+    const spd_h2_s* h = H->h2;
+    const TreeH& t = h->tree;
+    const HssLevel& l1 = H->lv[1];
+    std::vector<HsPhase> out(2);
+    out[0].mode = 0;
+    out[1].mode = 1;
+    for (int a = 0; a < l1.count; ++a) {
+        const int64_t off = t.begin[l1.first + a];
+        const int m = l1.m[a];
+        if (!m) continue;
+        const double* F = l1.Finv.p + l1.F_off[a];
+        out[0].nodes.push_back({F, nullptr, m, 0, b + off, nullptr, nullptr, z + off, nullptr, nullptr, nullptr});
+        out[1].nodes.push_back({F, nullptr, m, 0, z + off, nullptr, nullptr, nullptr, nullptr, nullptr, x + off});
+    }
+    for (int q = 0; q < (int)out[0].nodes.size(); ++q)
+        for (int rt = 0; rt * 32 < out[0].nodes[q].m; ++rt) {
+            out[0].items.push_back({q, 0, rt});
+            out[1].items.push_back({q, 2, rt});
+        }
+    return out;
+}
+
+void bj_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, cudaStream_t s) {
+    for (const auto& ph : bj_solve_plan(H, b, x, z)) launch_phase(s, ph);
+}
+
 void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
                    const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s) {
     for (const auto& ph : hss_solve_plan(H, b, x, z, zl, zs, ub)) launch_phase(s, ph);

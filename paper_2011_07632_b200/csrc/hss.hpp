@@ -56,8 +56,11 @@ void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const st
                    const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s);
 void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64_t ldx, int k, cudaStream_t s);
 void hss_query(const spd_hss_s* H, int what, void* buf, size_t bytes);
+// precond: PC_HSS (the SPD-HSS solve), PC_BJ (block Jacobi from its leaf factors); M == nullptr: none
+enum { PC_HSS = 0, PC_BJ = 1 };
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,
-              cudaStream_t s);
+              cudaStream_t s, int precond = PC_HSS);
+void bj_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, cudaStream_t s);
 // persistent (cooperative) PCG kernel, pcgk.cu
 struct PcgPersistent {
     struct Impl;
@@ -65,7 +68,7 @@ struct PcgPersistent {
     ~PcgPersistent();
 };
 bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double* x, double* r, double* p, double* q,
-                            double* z, cudaStream_t s);
+                            double* z, cudaStream_t s, int precond = 0);
 // out: ||r||^2, iterations, converged, error (1: p^T A p <= 0, 2: r^T M r <= 0)
 void pcg_persistent_run(PcgPersistent& pk, double rz, double nb, double tol, int maxit, double out[4], cudaStream_t s);
 const spd_hss_s* hss_if_hss(const void* handle);      // nullptr when handle is not an HSS

@@ -79,7 +79,14 @@ static void dot_into(cudaStream_t s, PcgWork& w, const double* a, const double* 
 }
 
 // one PCG iteration after the first: q = A p, alpha, x/r update, z = M r, beta, p update
-static void iteration_body(spd_h2_s* A, spd_hss_s* M, double* x, PcgWork& w, int64_t N, cudaStream_t s) {
+static void apply_precond(spd_hss_s* M, int precond, PcgWork& w, int64_t N, cudaStream_t s) {
+    if (!M) SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    else if (precond == PC_BJ) bj_solve_vec(M, w.r.p, w.z.p, M->bt.p, s);
+    else hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);
+}
+
+static void iteration_body(spd_h2_s* A, spd_hss_s* M, int precond, double* x, PcgWork& w, int64_t N,
+                           cudaStream_t s) {
     h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);
     dot_into(s, w, w.p.p, w.q.p, N, S_PQ, 1);
     {
@@ -89,8 +96,7 @@ static void iteration_body(spd_h2_s* A, spd_hss_s* M, double* x, PcgWork& w, int
         finish_kernel<<<1, RED_THREADS, 0, s>>>(w.partial.p, w.scal.p, S_RR, 0);
         SPD_LAUNCH();
     }
-    if (M) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);
-    else SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    apply_precond(M, precond, w, N, s);
     dot_into(s, w, w.r.p, w.z.p, N, S_RZNEW, 2);
     {
         ProfScope prof(s, "pcg_vec", 2.0 * N, 24.0 * N);
@@ -100,7 +106,7 @@ static void iteration_body(spd_h2_s* A, spd_hss_s* M, double* x, PcgWork& w, int
 }
 
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,
-              cudaStream_t user) {
+              cudaStream_t user, int precond) {
     const int64_t N = A->N;
     const auto t0 = std::chrono::steady_clock::now();
     // private non-blocking stream (graph capture is illegal on the legacy stream)
@@ -139,8 +145,8 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     rep->iters = 0; rep->converged = 0; rep->relres = 1.0; rep->seconds = 0.0;
     if (nb == 0.0) { rep->converged = 1; rep->relres = 0.0; return; }
     // z = M r, p = z, rz = r^T z
-    if (M) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);
-    else SPD_CUDA(cudaMemcpyAsync(w.z.p, w.r.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    if (M && precond == PC_BJ) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);   // allocates the solve workspace
+    apply_precond(M, precond, w, N, s);
     SPD_CUDA(cudaMemcpyAsync(w.p.p, w.z.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
     dot_into(s, w, w.r.p, w.z.p, N, S_RZ, 0);
     SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
@@ -151,7 +157,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     // selects the per-iteration CUDA graph below instead (per-kernel profiling)
     if (!getenv("SPD_PCG_GRAPH")) {
         PcgPersistent pk;
-        if (pcg_persistent_prepare(pk, A, M, x, w.r.p, w.p.p, w.q.p, w.z.p, s)) {
+        if (pcg_persistent_prepare(pk, A, M, x, w.r.p, w.p.p, w.q.p, w.z.p, s, precond)) {
             double out[4];
             pcg_persistent_run(pk, hs[S_RZ], nb, tol, maxit, out, s);
             rep->iters = (int)out[1];
@@ -173,7 +179,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             desc_arena() = &arena;
             const size_t mark = prof_mark();
             SPD_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-            try { iteration_body(A, M, x, w, N, s); }
+            try { iteration_body(A, M, precond, x, w, N, s); }
             catch (...) { cudaGraph_t g; cudaStreamEndCapture(s, &g); if (g) cudaGraphDestroy(g); throw; }
             SPD_CUDA(cudaStreamEndCapture(s, &cl.g));
             SPD_CUDA(cudaGraphInstantiate(&cl.ge, cl.g, 0));
@@ -199,7 +205,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             SPD_CUDA(cudaGraphLaunch(cl.ge, s));
             count_launches(graph_kernels);
         } else {
-            iteration_body(A, M, x, w, N, s);
+            iteration_body(A, M, precond, x, w, N, s);
         }
         SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
         SPD_CUDA(cudaStreamSynchronize(s));

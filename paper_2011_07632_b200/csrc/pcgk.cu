@@ -213,7 +213,7 @@ static void* kernel_ptr(int kid, bool eval) {
 }
 
 bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double* x, double* r, double* p, double* q,
-                            double* z, cudaStream_t s) {
+                            double* z, cudaStream_t s, int precond) {
     const TreeH& t = A->tree;
     const int L = t.L;
     if (L < 2 || !M || A->stored_mode != 1) return false;
@@ -233,7 +233,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     std::vector<double*> zl(L + 1, nullptr), zs(L + 1, nullptr), ub(L + 1, nullptr);
     for (int l = 1; l < L; ++l) { zl[l] = M->z[l].p; zs[l] = M->zs[l].p; }
     for (int l = 2; l <= L; ++l) ub[l] = M->ub[l].p;
-    auto hs = hss_solve_plan(M, r, z, M->bt.p, zl, zs, ub);
+    auto hs = precond == 1 ? bj_solve_plan(M, r, z, M->bt.p) : hss_solve_plan(M, r, z, M->bt.p, zl, zs, ub);
     if ((int)hs.size() > PK_MAXPH || L - 1 > PK_MAXPH) return false;
     std::vector<char> buf;
     std::vector<size_t> fix;

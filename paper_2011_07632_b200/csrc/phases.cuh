@@ -408,6 +408,7 @@ std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const doubl
 std::vector<std::vector<BasisItem>> basis_down_plan(const spd_h2_s* h, const std::vector<double*>& yh, int top,
                                                     double* y, int* smax_out, std::vector<double>* bytes);
 struct HsPhase { int mode = 0; std::vector<HsNode> nodes; std::vector<HsItem> items; };
+std::vector<HsPhase> bj_solve_plan(const spd_hss_s* H, const double* b, double* x, double* z);
 std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double* x, double* z,
                                     const std::vector<double*>& zl, const std::vector<double*>& zs,
                                     const std::vector<double*>& ub);
