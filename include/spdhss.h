@@ -118,6 +118,16 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
 spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample, uint64_t seed,
                         const double* omega, void* stream, spd_hss_t* out);
 
+/* spdhss_build_adaptive: the threshold-driven variant sketched in PAPER.md P:998-999
+ * ("adaptively adding more vectors to Omega and compressing Lambda_{ii^c} Omega_{i^c}
+ * with this error threshold"), in restart form (reading R27): builds with rank cap
+ * r0, 2 r0, 4 r0, ... (<= r_max) until every node's rank stops on the threshold
+ * |R_tt| <= rel_tol |R_00| below the cap.  Omega = the leading cap + oversample
+ * columns of one sketch: Philox(seed), or omega (device, N x (r_max + oversample),
+ * ld = N, tree order).  *cap_out (host, nullable) = the cap used. */
+spd_status spdhss_build_adaptive(spd_h2_t h, int r0, int r_max, double rel_tol, int oversample, uint64_t seed,
+                                 const double* omega, void* stream, spd_hss_t* out, int* cap_out);
+
 /* hss_solve: X = H^{-1} B for the SPD HSS H, by the recursive solve of reading
  * R12 (the "ULV-style" solve of PAPER.md P:1119-1123), nrhs columns. */
 spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, double* X,

@@ -25,6 +25,6 @@ from .tree import Tree, build_tree, interaction_lists, Lists
 from .linalg import NotPD, cholesky, qrcp, sym_sqrt_pair
 from .h2 import H2, h2_build, h2_matvec, h2_densify, proxy_points, halton
 from .spdhss import (HSS, spdhss_build, hss_matvec, hss_densify, hss_solve,
-                     pcg, block_jacobi_solve, alg1_generalized, special_products, hss_error)
+                     pcg, block_jacobi_solve, spdhss_build_adaptive, alg1_generalized, special_products, hss_error)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -267,6 +267,18 @@ def hss_solve(hss: HSS, b):
     return x[:, 0] if vec else x
 
 
+def spdhss_build_adaptive(h2: H2, rel_tol, r0, r_max, omega_full, p=10, form="chol"):
+    """Threshold-driven SPD HSS, restart form (reading R27): cap = r0,
+    2 r0, ... <= r_max until every rank stops on |R_tt| <= tol |R_00| below the cap;
+    Omega = the leading cap + p columns of omega_full.  Returns (HSS, cap)."""
+    cap = r0
+    while True:
+        H = spdhss_build(h2, cap, rel_tol, omega_full[:, :cap + p], form=form)
+        if max(H.rank.values(), default=0) < cap or cap >= r_max:
+            return H, cap
+        cap = min(2 * cap, r_max)
+
+
 def block_jacobi_solve(h2: H2, b):
     """Block-Jacobi preconditioner: x_i = A_ii^{-1} b_i for every leaf i, by the
     Cholesky factor of A_ii (SPD-HSS = BJ's diagonal blocks + off-diagonal

@@ -70,6 +70,7 @@ def lib():
         "hss_solve": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
         "pcg_solve": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
         "pcg_solve_bj": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
+        "spdhss_build_adaptive": ([vp, c_int, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp), P(c_int)], c_int),
         "spd_query": ([vp, c_int, vp, ctypes.c_size_t], c_int),
         "h2_free": ([vp], None),
         "hss_free": ([vp], None),
@@ -95,7 +96,7 @@ def lib():
 
 
 EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
-            "pcg_solve", "pcg_solve_bj", "spd_query", "h2_free", "hss_free", "spd_last_error"]
+            "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error"]
 
 
 def _check(status):
@@ -309,6 +310,21 @@ def spdhss_build(h2, rank_cap, rel_tol, oversample=10, seed=0, omega=None):
     _check(lib().spdhss_build(h2.ptr, int(rank_cap), float(rel_tol), int(oversample), int(seed), om,
                               _stream(), ctypes.byref(out)))
     return HSS(out, h2)
+
+
+def spdhss_build_adaptive(h2, r0, r_max, rel_tol, oversample=10, seed=0, omega=None):
+    """Threshold-driven SPD-HSS (restart form).  Returns (HSS, cap used).
+    omega: optional n x (r_max + oversample) tree-order sketch."""
+    out = ctypes.c_void_p()
+    cap = ctypes.c_int(0)
+    om = None
+    if omega is not None:
+        om, ld, w = _mat(omega, "omega")
+        if ld != h2.n or w != r_max + oversample:
+            raise ValueError("omega must be n x (r_max + oversample) with ld = n")
+    _check(lib().spdhss_build_adaptive(h2.ptr, int(r0), int(r_max), float(rel_tol), int(oversample), int(seed), om,
+                                       _stream(), ctypes.byref(out), ctypes.byref(cap)))
+    return HSS(out, h2), cap.value
 
 
 def hss_solve(hss, B, layout=LAYOUT_ORIGINAL, out=None):

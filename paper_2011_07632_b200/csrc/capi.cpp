@@ -1,5 +1,6 @@
 // capi.cpp -- the extern "C" boundary of libspdhss (include/spdhss.h).
 // Argument validation, error translation, layout handling.  No numerics here.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -110,6 +111,40 @@ spd_status spdhss_build(spd_h2_t h, int rank_cap, double rel_tol, int oversample
         try { hss_build_impl(H, omega, seed, (cudaStream_t)stream); }
         catch (...) { delete H; throw; }
         *out = H;
+    })
+}
+
+spd_status spdhss_build_adaptive(spd_h2_t h, int r0, int r_max, double rel_tol, int oversample, uint64_t seed,
+                                 const double* omega, void* stream, spd_hss_t* out, int* cap_out) {
+    SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
+        SPD_REQUIRE(out != nullptr, "spdhss_build_adaptive: out is NULL");
+        *out = nullptr;
+        SPD_REQUIRE(h != nullptr, "spdhss_build_adaptive: null H2 handle");
+        SPD_REQUIRE(r0 >= 1 && r_max >= r0 && oversample >= 0, "spdhss_build_adaptive: need 1 <= r0 <= r_max");
+        SPD_REQUIRE(rel_tol >= 0.0 && rel_tol < 1.0, "spdhss_build_adaptive: rel_tol in [0, 1)");
+        // grow Omega until every sketch Lambda_{ii^c} Omega is compressed to the
+        // threshold (its rank stops on |R_tt| <= tol |R_00| below the cap); restart form:
+        // cap = r0, 2 r0, ... up to r_max, Omega = the leading cap + p columns of one
+        // sketch (Philox counters / the injected N x (r_max + p) matrix), reading R27
+        int cap = r0;
+        for (;;) {
+            auto* H = new spd_hss_s();
+            H->h2 = h; H->cap = cap; H->p = oversample; H->w = cap + oversample; H->tol = rel_tol;
+            try { hss_build_impl(H, omega, seed, (cudaStream_t)stream); }
+            catch (...) { delete H; throw; }
+            int maxr = 0;
+            for (size_t l = 1; l + 1 < H->lv.size(); ++l)
+                for (int r : H->lv[l].rank) maxr = std::max(maxr, r);
+            if (maxr < cap || cap >= r_max) {
+                *out = H;
+                if (cap_out) *cap_out = cap;
+                break;
+            }
+            cudaStreamSynchronize((cudaStream_t)stream);
+            delete H;
+            cap = std::min(2 * cap, r_max);
+        }
     })
 }
 

@@ -215,3 +215,24 @@ def test_pcg_block_jacobi_matches_oracle(spd, name):
     xg = host(x)[ho.tree.perm]
     res = oracle.h2_matvec(ho, xg) - b[ho.tree.perm]
     assert np.linalg.norm(res) <= 1e-7 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("name", ["C1s", "C2s"])
+def test_adaptive_build_matches_oracle(spd, name):
+    """Threshold-driven build (R27) with the same injected sketch: the GPU
+    picks the oracle's cap, the same ranks, and the same HSS (applied by the oracle)."""
+    import torch
+    cfg = CASES[name]
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    ho = oracle.h2_build(X, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    r_max = 64
+    om = synth.omega(cfg, w=r_max + cfg.oversample)
+    Ho, cap_o = oracle.spdhss_build_adaptive(ho, cfg.hss_tol, 4, r_max, om, p=cfg.oversample, form="chol")
+    H, cap = spd.spdhss_build_adaptive(h, 4, r_max, cfg.hss_tol, cfg.oversample, omega=cuda(om))
+    assert cap == cap_o
+    rg = H.ranks()
+    assert all(abs(int(rg[i]) - r) <= 1 for i, r in Ho.rank.items())
+    G = gpu_as_oracle_hss(H, ho)
+    v = synth.multivec(cfg.n, 3, seed=8)[ho.tree.perm]
+    assert rel(oracle.hss_matvec(G, v), oracle.hss_matvec(Ho, v)) <= 1e-9

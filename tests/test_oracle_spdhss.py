@@ -229,3 +229,28 @@ def test_block_jacobi_pins(c1small):
     _, it_b, cb, _ = oracle.pcg(A, lambda v: oracle.block_jacobi_solve(h, v), b, 1e-8, 3000)
     _, it_n, cn, _ = oracle.pcg(A, lambda v: v, b, 1e-8, 3000)
     assert ch and cb and it_h < it_b < it_n
+
+
+def test_adaptive_threshold_build():
+    """P:998-999 (restart form, R27): the chosen cap is the first in r0, 2 r0, ...
+    at which every sketch compression stops on the threshold; the previous cap did
+    not; the error metric does not increase; and a threshold below
+    rounding with a cap above the node sizes reproduces the H2 exactly."""
+    cfg = synth.C1.scaled(512, leaf=32)
+    X = synth.points(cfg)
+    h = oracle.h2_build(X, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    om = synth.omega(cfg, w=64 + 10)
+    H, cap = oracle.spdhss_build_adaptive(h, 1e-3, 4, 64, om)
+    assert max(H.rank.values()) < cap and cap > 4
+    Hprev = oracle.spdhss_build(h, cap // 2, 1e-3, om[:, :cap // 2 + 10], form="chol")
+    assert max(Hprev.rank.values()) == cap // 2
+    probes = synth.multivec(512, 6, seed=3)
+    assert oracle.hss_error(H, probes) <= oracle.hss_error(Hprev, probes)
+    # no truncation: tol below rounding, cap above every node's rows -> HSS == H2
+    cfg2 = synth.C1.scaled(128, leaf=32)
+    X2 = synth.points(cfg2)
+    h2 = oracle.h2_build(X2, cfg2.kernel, cfg2.ell, cfg2.shift, cfg2.leaf, 1e-14)
+    om2 = synth.omega(cfg2, w=128 + 10)
+    H2, cap2 = oracle.spdhss_build_adaptive(h2, 1e-15, 8, 128, om2)
+    Ad = oracle.h2_densify(h2)
+    np.testing.assert_allclose(oracle.hss_densify(H2), Ad, atol=1e-11 * np.abs(Ad).max())
