@@ -113,25 +113,25 @@ __global__ void __launch_bounds__(256) gemv_kernel(const GemmDesc* __restrict__ 
     }
 }
 
-template <int BM, int BN, int WM, int WN, int ST, bool TA, bool TB>
+template <int BM, int BN, int WM, int WN, int ST, bool TA, bool TB, bool PRE>
 static void launch_gemm_pipe1(cudaStream_t s, unsigned nb, const GemmDesc* d, const TileRef* t, double alpha, double beta) {
     constexpr size_t sh = gemm_pipe_smem<BM, BN, WM, WN, ST, TA, TB>();
     static bool attr = false;
     if (!attr) {
-        SPD_CUDA(cudaFuncSetAttribute(gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB>,
+        SPD_CUDA(cudaFuncSetAttribute(gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB, PRE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
         attr = true;
     }
-    gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB><<<nb, (BM / WM) * (BN / WN) * 32, sh, s>>>(d, t, alpha, beta);
+    gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB, PRE><<<nb, (BM / WM) * (BN / WN) * 32, sh, s>>>(d, t, alpha, beta);
     SPD_LAUNCH();
 }
-template <int BM, int BN, int WM, int WN, int ST>
+template <int BM, int BN, int WM, int WN, int ST, bool PRE = false>
 static void launch_gemm_pipe(cudaStream_t s, unsigned nb, const GemmDesc* d, const TileRef* t, double alpha,
                              double beta, bool ta, bool tb) {
-    if (!ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, false>(s, nb, d, t, alpha, beta);
-    else if (ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, true, false>(s, nb, d, t, alpha, beta);
-    else if (!ta && tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, true>(s, nb, d, t, alpha, beta);
-    else launch_gemm_pipe1<BM, BN, WM, WN, ST, true, true>(s, nb, d, t, alpha, beta);
+    if (!ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, false, PRE>(s, nb, d, t, alpha, beta);
+    else if (ta && !tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, true, false, PRE>(s, nb, d, t, alpha, beta);
+    else if (!ta && tb) launch_gemm_pipe1<BM, BN, WM, WN, ST, false, true, PRE>(s, nb, d, t, alpha, beta);
+    else launch_gemm_pipe1<BM, BN, WM, WN, ST, true, true, PRE>(s, nb, d, t, alpha, beta);
 }
 
 // split-K epilogue: C = alpha sum_s P_s + beta C, slices added in order
@@ -189,6 +189,11 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     // cuBLAS DGEMM, against 28-30 TF/s for 128 x 128); env SPD_GEMM_TILE=128 overrides
     int T = 64;
     if (const char* e = getenv("SPD_GEMM_TILE")) T = atoi(e) == 128 ? 128 : 64;
+    // m <= 32 everywhere (V^T A of the blocked QR): 32 x 64 tiles, no wasted DMMA rows
+    int mmax_all = 0, kmax_all = 0;
+    for (const auto& g : d) { mmax_all = std::max(mmax_all, g.m); kmax_all = std::max(kmax_all, g.k); }
+    const bool m32 = T == 64 && mmax_all <= 32;
+    const int TM = m32 ? 32 : T;
     // output tiles; when they are too few to fill the GPU and K is long (the tall
     // skinny V^T A of the blocked QR), K is split into S slices whose raw partial
     // tiles are summed in slice order by gemm_reduce_kernel (deterministic)
@@ -196,12 +201,13 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     int kmax = 0;
     for (const auto& g : d) {
         if (g.m <= 0 || g.n <= 0) continue;
-        ntiles += (long long)ceil_div(g.m, T) * ceil_div(g.n, T);
+        ntiles += (long long)ceil_div(g.m, TM) * ceil_div(g.n, T);
         kmax = std::max(kmax, g.k);
     }
+    // split K when a tile's K loop is long and the tiles are too few for ~8 resident per SM
     int S = 1;
-    if (ntiles > 0 && ntiles < 2 * 148 && kmax >= 8 * 64)
-        S = (int)std::max<long long>(1, std::min<long long>(kmax / 256, (4 * 148 + ntiles - 1) / ntiles));
+    if (ntiles > 0 && ((ntiles < 2 * 148 && kmax >= 1024) || (ntiles < 4 * 148 && kmax >= 4096)))
+        S = (int)std::max<long long>(1, std::min<long long>(kmax / 512, (8 * 148 + ntiles - 1) / ntiles));
     std::vector<TileRef> tiles;
     std::vector<ReduceDesc> red;
     size_t poff = 0;
@@ -213,7 +219,7 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         const int Seff = Si > 1 ? ceil_div(d[i].k, kc) : 1;
         for (int ks = 0; ks < Seff; ++ks)
             for (int tn = 0; tn < ceil_div(d[i].n, T); ++tn)
-                for (int tm = 0; tm < ceil_div(d[i].m, T); ++tm) {
+                for (int tm = 0; tm < ceil_div(d[i].m, TM); ++tm) {
                     TileRef tr{i, tm, tn, ks * kc, std::min(d[i].k, (ks + 1) * kc), nullptr, d[i].m};
                     if (Seff > 1) tr.P = (double*)(uintptr_t)(poff + (size_t)ks * d[i].m * d[i].n + 1);  // offset+1, patched below
                     tiles.push_back(tr);
@@ -241,7 +247,10 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         ProfScope prof(s, "gemm_dmma", fl, by);
         for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
             unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
+            const bool pre = beta != 0.0 && kmax_all <= 64;      // short-K update: C read early
             if (T == 128) launch_gemm_pipe<128, 128, 64, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
+            else if (m32) launch_gemm_pipe<32, 64, 32, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
+            else if (pre) launch_gemm_pipe<64, 64, 32, 32, 2, true>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
             else launch_gemm_pipe<64, 64, 32, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
         }
     }

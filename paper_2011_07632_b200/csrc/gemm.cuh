@@ -38,7 +38,9 @@ struct GemmSmem {
     static constexpr int B_ELEMS = TB ? BK * B_LD : BN * B_LD;
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool TA, bool TB>
+// PRE: the C tile (beta != 0) is loaded at kernel start, so its read latency overlaps
+// the A/B loads (short-K updates such as the rank-32 trailing update of the blocked QR)
+template <int BM, int BN, int WM, int WN, int STAGES, bool TA, bool TB, bool PRE = false>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 gemm_pipe_kernel(const GemmDesc* __restrict__ descs, const TileRef* __restrict__ tiles, double alpha, double beta) {
     using SM = GemmSmem<BM, BN, TA, TB>;
@@ -84,6 +86,19 @@ gemm_pipe_kernel(const GemmDesc* __restrict__ descs, const TileRef* __restrict__
     for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double cpre[PRE ? FM : 1][PRE ? FN : 1][2];
+    if (PRE) {
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int gi = m0 + wm * WM + i * 8 + g;
+                    const int gj = n0 + wn * WN + j * 8 + 2 * q + h;
+                    cpre[PRE ? i : 0][PRE ? j : 0][h] = (gi < d.m && gj < d.n && !tr.P) ? d.C[gi + (size_t)gj * d.ldc] : 0.0;
+                }
+    }
 
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -134,14 +149,15 @@ gemm_pipe_kernel(const GemmDesc* __restrict__ descs, const TileRef* __restrict__
                         tr.P[gi + (size_t)gj * tr.ldp] = acc[i][j][h];
                     } else {
                         double* c = d.C + gi + (size_t)gj * d.ldc;
-                        *c = (beta == 0.0 ? 0.0 : beta * *c) + alpha * acc[i][j][h];
+                        const double cold = PRE ? cpre[PRE ? i : 0][PRE ? j : 0][h] : (beta == 0.0 ? 0.0 : *c);
+                        *c = (beta == 0.0 ? 0.0 : beta * cold) + alpha * acc[i][j][h];
                     }
                 }
             }
 }
 
 template <int BM, int BN, int WM, int WN, int STAGES, bool TA, bool TB>
-constexpr size_t gemm_pipe_smem() {
+constexpr size_t gemm_pipe_smem() {   // (independent of PRE)
     using SM = GemmSmem<BM, BN, TA, TB>;
     return sizeof(double) * (size_t)STAGES * (SM::A_ELEMS + SM::B_ELEMS);
 }
