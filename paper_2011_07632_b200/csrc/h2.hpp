@@ -45,6 +45,8 @@ struct H2SymStore {
     DBuf<SymContrib> gcon;
     int npieces = 0, ngnodes = 0, nbig = 0;      // gnodes[0, nbig): long lists
     int nbmax = 1;
+    std::vector<int> piece_off;                  // pieces of slot l: [piece_off[l], piece_off[l+1])
+    std::vector<SymGNode> gnodes_h;              // host copy (per-slot schedules of the persistent PCG)
     double flops = 0, bytes = 0, stored_frac = 1.0;
     bool built = false;
 };

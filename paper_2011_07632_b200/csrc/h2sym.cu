@@ -206,6 +206,15 @@ void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
     st.scratch.alloc(std::max<int64_t>(1, ns));
     st.pieces.upload(pieces, s);
     st.gnodes.upload(gnodes, s);
+    st.gnodes_h = gnodes;
+    {
+        const int L = h->tree.L;
+        st.piece_off.assign(L + 1, 0);
+        for (const auto& pc : pieces) st.piece_off[pc.slot + 1]++;
+        for (int l = 0; l < L; ++l) st.piece_off[l + 1] += st.piece_off[l];
+        for (size_t i = 1; i < pieces.size(); ++i)
+            SPD_REQUIRE(pieces[i].slot >= pieces[i - 1].slot, "h2sym: pieces not ordered by slot");
+    }
     st.gcon.upload(gcon, s);
     st.npieces = (int)pieces.size();
     st.ngnodes = (int)gnodes.size();
