@@ -30,9 +30,10 @@ static void launch_phase(cudaStream_t s, const HsPhase& ph) {
     for (auto& n : ph.nodes) {
         mmax = std::max(mmax, n.m);
         rmax = std::max(rmax, n.r);
-        by += 8.0 * (0.5 * n.m * (n.m + 1) + (double)n.m * n.r + 2.0 * n.m + 2.0 * n.r);
+        by += ph.mode == 3 ? 8.0 * ((double)n.m * n.m + 2.0 * n.m)
+                           : 8.0 * (0.5 * n.m * (n.m + 1) + (double)n.m * n.r + 2.0 * n.m + 2.0 * n.r);
     }
-    SPD_REQUIRE(mmax <= 32 * HS_MT, "hss_solve: node too large for the k=1 solve");
+    SPD_REQUIRE(ph.mode == 3 || mmax <= 32 * HS_MT, "hss_solve: node too large for the k=1 solve");
     const size_t smem = sizeof(double) * (size_t)hss_item_smem_doubles(mmax, rmax);
     if (smem > 48 * 1024)
         SPD_CUDA(cudaFuncSetAttribute(hss_item_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -75,7 +76,10 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
     }
     up_items(ph);
     out.push_back(ph);
-    for (int l = 2; l < L; ++l) {
+    // dense top operator (spdhss.cu build_top_operator): up to level gt, one GEMV, down
+    const int gt = H->gt_level;
+    const int top_up = gt > 0 ? gt : L - 1;
+    for (int l = 2; l <= top_up; ++l) {
         const HssLevel& lv = H->lv[l];
         const HssLevel& pv = H->lv[l - 1];
         ph = HsPhase();
@@ -89,7 +93,15 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
         up_items(ph);
         out.push_back(ph);
     }
-    {   // root: u = F w into ub[L], then x = F^T u back into zl[L-1]
+    if (gt > 0) {
+        ph = HsPhase();
+        ph.mode = 3;
+        const int R = (int)H->gt_R;
+        ph.nodes.push_back({H->Gtop.p, nullptr, R, 0, zl[gt], nullptr, nullptr, nullptr, nullptr, nullptr,
+                            H->gt_out.p});
+        for (int rt = 0; rt * 32 < R; ++rt) ph.items.push_back({0, 3, rt});
+        out.push_back(ph);
+    } else {   // root: u = F w into ub[L], then x = F^T u back into zl[L-1]
         const HssLevel& rt = H->lv[L];
         if (rt.m[0]) {
             ph = HsPhase();
@@ -106,7 +118,9 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
             out.push_back(ph);
         }
     }
-    for (int l = L - 1; l >= 2; --l) {
+    // xh of level l: from the top operator at l = gt, else written into zl[l] by the level above
+    auto xh_of = [&](int l) { return l == gt ? H->gt_out.p : zl[l]; };
+    for (int l = (gt > 0 ? gt : L - 1); l >= 2; --l) {
         const HssLevel& lv = H->lv[l];
         const HssLevel& pv = H->lv[l - 1];
         ph = HsPhase();
@@ -115,7 +129,7 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
             if (!lv.m[a]) continue;
             ph.nodes.push_back({lv.Finv.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a],
-                                ub[l] + pv.off[c1], zl[l] + lv.off[a], zs[l] + lv.off[a], nullptr, nullptr, nullptr,
+                                ub[l] + pv.off[c1], xh_of(l) + lv.off[a], zs[l] + lv.off[a], nullptr, nullptr, nullptr,
                                 zl[l - 1] + pv.off[c1]});
         }
         down_items(ph);
@@ -127,7 +141,7 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
         const int64_t off = t.begin[l1.first + a];
         if (!l1.m[a]) continue;
         ph.nodes.push_back({l1.Finv.p + l1.F_off[a], l1.P.p + l1.V_off[a], l1.m[a], l1.rank[a], z + off,
-                            zl[1] + l1.off[a], zs[1] + l1.off[a], nullptr, nullptr, nullptr, x + off});
+                            xh_of(1) + l1.off[a], zs[1] + l1.off[a], nullptr, nullptr, nullptr, x + off});
     }
     down_items(ph);
     out.push_back(ph);

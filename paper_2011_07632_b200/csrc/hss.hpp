@@ -46,6 +46,12 @@ struct spd_hss_s {
     // solve workspace
     int64_t ws_k = 0;
     spd::DBuf<double> bt, xt;
+    // dense operator of the top of the solve recursion (levels > gt_level, root): the
+    // linear map zh (level gt_level coefficients) -> xh; replaces 2 (L - 1 - gt_level) + 2
+    // dependent single-vector phases by one GEMV (0: not built)
+    int gt_level = 0;
+    int64_t gt_R = 0;
+    spd::DBuf<double> Gtop, gt_out;
     std::vector<spd::DBuf<double>> z, ub, zs;
 };
 

@@ -260,12 +260,15 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     for (const auto& ph : hs) {
         if (ph.items.empty()) continue;
         const int base = (int)hsf.size();
-        for (const auto& nd : ph.nodes) { mmax = std::max(mmax, nd.m); rmax = std::max(rmax, nd.r); }
+        for (const auto& nd : ph.nodes) {
+            mmax = std::max(mmax, nd.m);
+            rmax = std::max(rmax, nd.r);
+            if (ph.mode != 3 && nd.m > 32 * HS_MT) return false;
+        }
         hsf.insert(hsf.end(), ph.nodes.begin(), ph.nodes.end());
         for (auto itm : ph.items) { itm.node += base; hsi.push_back(itm); }
         P.hs_off[++P.nhs] = (int)hsi.size();
     }
-    if (mmax > 32 * HS_MT) return false;
     const BasisItem* up_rel = put(buf, upf, fix);
     const BasisItem* dn_rel = put(buf, dnf, fix);
     const HsNode* hs_rel = put(buf, hsf, fix);
@@ -314,7 +317,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
         const H2Level& lv = A->lv[lk];
         for (int a = 0; a < lv.count; ++a) by += 2.0 * 8.0 * (double)lv.rank[a] * (lv.ncand[a] - lv.rank[a]);
     }
-    for (const auto& nd : hsf) by += 8.0 * (0.5 * nd.m * (nd.m + 1) + (double)nd.m * nd.r);
+    for (const auto& nd : hsf) by += nd.P ? 8.0 * (0.5 * nd.m * (nd.m + 1) + (double)nd.m * nd.r) : 8.0 * (double)nd.m * nd.m;
     by += 8.0 * 14.0 * A->N;
     im->bytes_per_iter = by;
     return true;

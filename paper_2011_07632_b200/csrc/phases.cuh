@@ -305,6 +305,7 @@ struct HsNode {
 //   kind 0  u0[rt] = F[rt rows, :] w             (lower: columns <= row)
 //   kind 1  zh[ct] = P[:, ct cols]^T w           (also written to zh2)
 //   kind 2  out[rt] = (F^T u)[rt] + P[rt rows, :] (xh - zh)   (root: zh, xh absent)
+//   kind 3  out[rt] = F[rt rows, :] w   (F full m x m: the dense top-of-tree operator)
 struct HsItem { int node, kind, tile; };
 
 // sm: m + r + PH_W * 32 doubles
@@ -319,13 +320,14 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
     if (it.kind == 2 && nd.xh)
         for (int j = threadIdx.x; j < r; j += PH_T) dv[j] = ldv(nd.xh + j) - ldv(nd.zhi + j);
     __syncthreads();
-    if (it.kind == 0) {
+    if (it.kind == 0 || it.kind == 3) {
+        const bool lower = it.kind == 0;
         const int i = it.tile * 32 + lane;
-        const int ncc = min((m + 31) >> 5, it.tile + 1);          // chunks with a column <= the tile's rows
+        const int ncc = lower ? min((m + 31) >> 5, it.tile + 1) : (m + 31) >> 5;   // lower: columns <= rows
         double acc = 0.0;
         for (int cc = warp; cc < ncc; cc += PH_W) {
             const int j0 = cc * 32;
-            const int j1 = min(min(m, j0 + 32), i + 1);           // lower triangle, row i
+            const int j1 = lower ? min(min(m, j0 + 32), i + 1) : min(m, j0 + 32);
             const double* p = nd.F + i + (size_t)j0 * m;
             double v[32];
 #pragma unroll
@@ -344,7 +346,8 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
             double sum = 0.0;
 #pragma unroll
             for (int q = 0; q < PH_W; ++q) sum += red[q * 32 + lane];
-            nd.u[i] = sum;
+            if (lower) nd.u[i] = sum;
+            else nd.out[i] = sum;
         }
     } else if (it.kind == 1) {
         for (int q = 0; q < 4; ++q) {

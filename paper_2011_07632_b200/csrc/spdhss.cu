@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 namespace spd {
 
@@ -319,6 +320,90 @@ static void invert_factors(cudaStream_t s, HssLevel& lv) {
         }
     }
     trsm_batched(s, td, 'L', false);                  // F^{-1} = F \ I (lower triangular)
+}
+
+// ================================================================= dense top of the solve
+// The part of the recursive solve (R12) above level t -- up levels t+1..L-1, the root
+// factor, down levels L-1..t+1 -- is a linear map of the level-t coefficients zh_t
+// onto xh_t.  For the smallest t whose coefficient space R_t is at most 3072 it is
+// formed once, densely, by running that part of the recursion on the identity
+// (multi-column GEMMs), so the single-vector solve applies it as one GEMV.
+static void solve_middle(spd_hss_s* H, int t, int k, const std::vector<double*>& zz, const std::vector<double*>& uu,
+                         cudaStream_t s) {
+    const int L = H->h2->tree.L;
+    for (int l = t + 1; l < L; ++l) {
+        const HssLevel& lv = H->lv[l];
+        const HssLevel& pv = H->lv[l - 1];
+        std::vector<GemmDesc> g0, g1, g2;
+        for (int a = 0; a < lv.count; ++a) {
+            const int c1 = 2 * (lv.first + a) + 1 - pv.first;
+            const int m = lv.m[a];
+            if (!m) continue;
+            double* u = uu[l] + pv.off[c1];
+            g0.push_back({lv.Finv.p + lv.F_off[a], zz[l - 1] + pv.off[c1], u, m, k, m, m, (int)pv.R, (int)pv.R});
+            if (lv.rank[a]) {
+                g1.push_back({lv.V.p + lv.V_off[a], u, zz[l] + lv.off[a], lv.rank[a], k, m, m, (int)pv.R, (int)lv.R});
+                g2.push_back({lv.V.p + lv.V_off[a], zz[l] + lv.off[a], u, m, k, lv.rank[a], m, (int)lv.R, (int)pv.R});
+            }
+        }
+        gemm_batched(s, g0, false, false, 1.0, 0.0);
+        gemm_batched(s, g1, true, false, 1.0, 0.0);
+        gemm_batched(s, g2, false, false, -1.0, 1.0);
+    }
+    {
+        const HssLevel& rt = H->lv[L];
+        const HssLevel& pv = H->lv[L - 1];
+        const int m = rt.m[0];
+        if (m) {
+            gemm_batched(s, {{rt.Finv.p, zz[L - 1], uu[L], m, k, m, m, (int)pv.R, (int)pv.R}}, false, false, 1.0, 0.0);
+            gemm_batched(s, {{rt.Finv.p, uu[L], zz[L - 1], m, k, m, m, (int)pv.R, (int)pv.R}}, true, false, 1.0, 0.0);
+        }
+    }
+    for (int l = L - 1; l > t; --l) {
+        const HssLevel& lv = H->lv[l];
+        const HssLevel& pv = H->lv[l - 1];
+        std::vector<GemmDesc> g, g3;
+        for (int a = 0; a < lv.count; ++a) {
+            const int c1 = 2 * (lv.first + a) + 1 - pv.first;
+            const int m = lv.m[a];
+            if (!m) continue;
+            double* u = uu[l] + pv.off[c1];
+            if (lv.rank[a])
+                g.push_back({lv.V.p + lv.V_off[a], zz[l] + lv.off[a], u, m, k, lv.rank[a], m, (int)lv.R, (int)pv.R});
+            g3.push_back({lv.Finv.p + lv.F_off[a], u, zz[l - 1] + pv.off[c1], m, k, m, m, (int)pv.R, (int)pv.R});
+        }
+        gemm_batched(s, g, false, false, 1.0, 1.0);
+        gemm_batched(s, g3, true, false, 1.0, 0.0);
+    }
+}
+
+__global__ void identity_kernel(double* A, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
+        A[e] = (e % n == e / n) ? 1.0 : 0.0;
+}
+
+static void build_top_operator(spd_hss_s* H, cudaStream_t s) {
+    const int L = H->h2->tree.L;
+    H->gt_level = 0;
+    if (L < 2 || getenv("SPD_NO_GTOP")) return;
+    int t = 0;
+    for (int l = 1; l < L; ++l)
+        if (H->lv[l].R <= 3072) { t = l; break; }
+    if (t == 0 || H->lv[t].R == 0) return;
+    const int64_t R = H->lv[t].R;
+    const int k = (int)R;
+    std::vector<DBuf<double>> zb(L), ubuf(L + 1);
+    std::vector<double*> zz(L, nullptr), uu(L + 1, nullptr);
+    H->Gtop.alloc((size_t)R * R);
+    zz[t] = H->Gtop.p;
+    for (int l = t + 1; l < L; ++l) { zb[l].alloc(std::max<int64_t>(1, H->lv[l].R * k)); zz[l] = zb[l].p; }
+    for (int l = t + 1; l <= L; ++l) { ubuf[l].alloc(std::max<int64_t>(1, H->lv[l - 1].R * k)); uu[l] = ubuf[l].p; }
+    identity_kernel<<<148 * 4, 256, 0, s>>>(H->Gtop.p, R);
+    SPD_LAUNCH();
+    solve_middle(H, t, k, zz, uu, s);
+    H->gt_out.alloc(R);
+    H->gt_level = t;
+    H->gt_R = R;
 }
 
 // ================================================================= the build
@@ -623,6 +708,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     // solve factors: explicit S_i^{-1}, F_i^{-1} (triangular inverses by blocked TRSM on I),
     // so every step of hss_solve is an HBM-bound GEMV
     for (int k = 1; k <= L; ++k) invert_factors(s, H->lv[k]);
+    build_top_operator(H, s);
     SPD_CUDA(cudaStreamSynchronize(s));
     stage_mark(s, "hss invert factors");
     H->timings[2] = now_s() - t2;
