@@ -501,6 +501,12 @@ void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, boo
 
 // ================================================================= QRCP
 constexpr int QR_THREADS = 256;
+__device__ unsigned long long g_qr_trace[64];      // debug (SPD_QR_TRACE): phase timestamps
+__device__ __forceinline__ void qr_tr(int k) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_qr_trace[k] = t;
+}
 
 struct QrItem { int desc, g, G; };
 
@@ -583,6 +589,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
     __shared__ int si[32];
     __shared__ int s_stop;
     __shared__ double s_nu0;
+    extern __shared__ double vsh[];                 // m: the current reflector
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = QR_THREADS / 32;
     const int2 range = cta_items[blockIdx.x];
     for (int it = range.x; it < range.y; ++it) {
@@ -607,6 +614,8 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
         if (threadIdx.x == 0) { s_stop = 0; s_nu0 = 0.0; }
         group_barrier(bar, G);
         for (int t = 0;; ++t) {
+            const bool trc = (item.desc == 0 && g == 0 && t == 100 && threadIdx.x == 0);
+            if (trc) qr_tr(10);
             // ---- leader: pivot, stop test, Householder of column t
             if (g == 0) {
                 double bv = -1.0;
@@ -658,34 +667,84 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
                 }
                 __syncthreads();
             }
+            if (trc) qr_tr(11);
             group_barrier(bar, G);
+            if (trc) qr_tr(12);
             {
                 const int r = __ldcg(d.rank);
                 if (r >= 0) break;
             }
             // ---- all CTAs: apply H_t to owned columns j > t, recompute norms over rows t+1..
-            const double* v = A + (size_t)t * ld;     // v_t = 1 (implicit), v_i = A[i, t], i > t
+            //      v (v_t = 1) cached in shared memory; per column two passes with 8 loads in
+            //      flight per lane (the update phase is latency-bound otherwise)
+            const double* vg = A + (size_t)t * ld;     // v_i = A[i, t], i > t
             const double beta = __ldcg(d.beta + t);
-            int local = 0;
-            for (int j = g; j < n; j += G, ++local) {
-                if (j <= t || local % nw != warp) continue;
-                double* c = A + (size_t)j * ld;
-                double s = ldcg(c + t) * (lane == 0 ? 1.0 : 0.0);
-                for (int i = t + 1 + lane; i < m; i += 32) s += ldcg(v + i) * ldcg(c + i);
-                s = warp_sum(s);
-                // lane 0 above counted c[t] * 1 only once
-                const double w = beta * s;
-                double nn = 0.0;
-                if (lane == 0) c[t] = ldcg(c + t) - w;
-                for (int i = t + 1 + lane; i < m; i += 32) {
-                    double x = ldcg(c + i) - w * ldcg(v + i);
-                    c[i] = x;
-                    nn += x * x;
+            for (int i = t + threadIdx.x; i < m; i += QR_THREADS) vsh[i] = (i == t) ? 1.0 : ldcg(vg + i);
+            __syncthreads();
+            // this warp's columns: j = g + G * local (local = warp mod nw), j > t; two at a
+            // time (16 loads in flight per lane)
+            int j0 = g + G * warp;
+            while (j0 <= t && j0 < n) j0 += G * nw;
+            for (; j0 < n; j0 += 2 * G * nw) {
+                const int j1 = j0 + G * nw;
+                const bool two = j1 < n;
+                double* c0 = A + (size_t)j0 * ld;
+                double* c1 = A + (size_t)(two ? j1 : j0) * ld;
+                double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+                int i0 = t + lane;
+                for (; i0 + 3 * 32 < m; i0 += 4 * 32) {
+                    double x[4], y[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { const double vv = vsh[i0 + 32 * u]; sa[u] += vv * x[u]; sb[u] += vv * y[u]; }
                 }
-                nn = warp_sum(nn);
-                if (lane == 0) d.norms[j] = nn;
+                for (int i = i0; i < m; i += 32) {
+                    sa[0] += vsh[i] * ldcg(c0 + i);
+                    if (two) sb[0] += vsh[i] * ldcg(c1 + i);
+                }
+                const double w0 = beta * warp_sum((sa[0] + sa[1]) + (sa[2] + sa[3]));
+                const double w1 = beta * warp_sum((sb[0] + sb[1]) + (sb[2] + sb[3]));
+                double na[4] = {0.0, 0.0, 0.0, 0.0}, nb[4] = {0.0, 0.0, 0.0, 0.0};
+                i0 = t + lane;
+                for (; i0 + 3 * 32 < m; i0 += 4 * 32) {
+                    double x[4], y[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + 32 * u;
+                        const double vv = vsh[i];
+                        const double a = x[u] - w0 * vv;
+                        c0[i] = a;
+                        if (i > t) na[u] += a * a;
+                        if (two) {
+                            const double b = y[u] - w1 * vv;
+                            c1[i] = b;
+                            if (i > t) nb[u] += b * b;
+                        }
+                    }
+                }
+                for (int i = i0; i < m; i += 32) {
+                    const double a = ldcg(c0 + i) - w0 * vsh[i];
+                    c0[i] = a;
+                    if (i > t) na[0] += a * a;
+                    if (two) {
+                        const double b = ldcg(c1 + i) - w1 * vsh[i];
+                        c1[i] = b;
+                        if (i > t) nb[0] += b * b;
+                    }
+                }
+                const double n0 = warp_sum((na[0] + na[1]) + (na[2] + na[3]));
+                const double n1 = warp_sum((nb[0] + nb[1]) + (nb[2] + nb[3]));
+                if (lane == 0) {
+                    d.norms[j0] = n0;
+                    if (two) d.norms[j1] = n1;
+                }
             }
+            if (trc) qr_tr(13);
             group_barrier(bar, G);
+            if (trc) qr_tr(14);
         }
         group_barrier(bar, G);
     }
@@ -697,7 +756,16 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
     SPD_CUDA(cudaGetDevice(&dev));
     int nsm = 0, per_sm = 0;
     SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_kernel, QR_THREADS, 0));
+    int mmax = 1;
+    for (auto& q : d) mmax = std::max(mmax, q.m);
+    const size_t qsmem = sizeof(double) * (size_t)mmax;
+    SPD_REQUIRE(qsmem <= 200 * 1024, "qrcp: matrix too tall");
+    static bool qattr = false;
+    if (!qattr) {
+        SPD_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        qattr = true;
+    }
+    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_kernel, QR_THREADS, qsmem));
     const int cap = std::max(1, nsm * std::max(1, per_sm));
     // work estimate per matrix ~ m * n * min(m, n, max_rank)
     std::vector<double> work(d.size());
@@ -759,7 +827,16 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
     void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
     ProfScope prof(s, "qrcp", fl, by);     // flops: upper bound 4 m n kmax (rank unknown at launch)
     SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
-                                         args, 0, s));
+                                         args, qsmem, s));
+    static const bool trace = getenv("SPD_QR_TRACE") != nullptr;
+    if (trace) {
+        unsigned long long tr[16];
+        SPD_CUDA(cudaStreamSynchronize(s));
+        SPD_CUDA(cudaMemcpyFromSymbol(tr, g_qr_trace, sizeof(tr), 10 * sizeof(unsigned long long)));
+        fprintf(stderr, "[qrcp trace] %zu mats, %zu CTAs, m %d n %d: leader %.2f bar1 %.2f update %.2f bar2 %.2f us\n",
+                d.size(), cta.size(), d[0].m, d[0].n, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3,
+                (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3);
+    }
     count_launch();
     SPD_CUDA(cudaFreeAsync(bars, s));
 }
@@ -857,13 +934,8 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(const PanelDesc* descs) {
 // T[:j, j] = -beta_j T[:j, :j] V^T v_j; Golub-Van Loan 5.1.2), without a second pass.
 namespace cg = cooperative_groups;
 
-__device__ unsigned long long g_qr_trace[64];      // debug (SPD_QR_TRACE): CTA 0 phase timestamps
-__device__ __forceinline__ void qr_tr(int k) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        g_qr_trace[k] = t;
-    }
+__device__ __forceinline__ void qr_tr0(int k) {        // CTA 0 only
+    if (blockIdx.x == 0 && threadIdx.x == 0) qr_tr(k);
 }
 
 template <int QCL>
@@ -884,7 +956,7 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
     const int L = d.m - d.p, jb = d.jb;
     const int r0 = g * rp, nr = max(0, min(rp, L - r0));
     double* P = d.A + d.p + (size_t)d.p * d.ld;
-    qr_tr(0);
+    qr_tr0(0);
     // panel slice -> smem with asynchronous copies (all in flight at once)
     for (int c = 0; c < jb; ++c)
         for (int i = threadIdx.x; i < rp; i += blockDim.x)
@@ -892,10 +964,10 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    qr_tr(1);
+    qr_tr0(1);
     for (int j = 0; j < jb; ++j) {
-        if (j == 1) qr_tr(2);
-        if (j == 16) qr_tr(3);
+        if (j == 1) qr_tr0(2);
+        if (j == 16) qr_tr0(3);
         const int buf = j & 1;
         const double* colj = sm + j * rp;
         // ---- partial sums over my rows i > j (warp w: entries e = w, w + 8, ...)
@@ -971,15 +1043,15 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
         }
         __syncthreads();
     }
-    qr_tr(4);
+    qr_tr0(4);
     // write the R part (rows <= column) back; the rest of the slice is scratch
     for (int c = 0; c < jb; ++c)
         for (int i = threadIdx.x; i < nr; i += blockDim.x)
             if (r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
     if (g == 0)
         for (int e = threadIdx.x; e < QB * QB; e += blockDim.x) d.T[e] = T[e % QB][e / QB];
-    qr_tr(5);
-    qr_tr(6);
+    qr_tr0(5);
+    qr_tr0(6);
     cluster.sync();                                   // keep smem alive for remote readers
 }
 
