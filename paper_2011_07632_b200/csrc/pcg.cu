@@ -109,6 +109,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
               cudaStream_t user, int precond) {
     const int64_t N = A->N;
     const auto t0 = std::chrono::steady_clock::now();
+    stage_mark(user, nullptr);
     // private non-blocking stream (graph capture is illegal on the legacy stream)
     cudaStream_t s;
     SPD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -152,14 +153,18 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
     SPD_CUDA(cudaStreamSynchronize(s));
 
+    stage_mark(s, "pcg init (r, z, p, rz)");
     h2_prepare(A, 1, s);
+    stage_mark(s, "pcg h2_prepare");
     // persistent cooperative kernel for the whole loop (pcgk.cu); env SPD_PCG_GRAPH=1
     // selects the per-iteration CUDA graph below instead (per-kernel profiling)
     if (!getenv("SPD_PCG_GRAPH")) {
         PcgPersistent pk;
         if (pcg_persistent_prepare(pk, A, M, x, w.r.p, w.p.p, w.q.p, w.z.p, s, precond)) {
+            stage_mark(s, "pcg persistent prepare");
             double out[4];
             pcg_persistent_run(pk, hs[S_RZ], nb, tol, maxit, out, s);
+            stage_mark(s, "pcg persistent run");
             rep->iters = (int)out[1];
             rep->relres = std::sqrt(out[0]) / nb;
             rep->converged = out[2] != 0.0;

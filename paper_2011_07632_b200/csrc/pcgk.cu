@@ -218,6 +218,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     const int L = t.L;
     if (L < 2 || !M || A->stored_mode != 1) return false;
     h2sym_build(A, A->sym_budget, s);
+    stage_mark(s, "pcg h2sym_build");
     auto* im = new PcgPersistent::Impl();
     pk.impl = im;
     PcgPlan& P = im->plan;
