@@ -486,7 +486,10 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     size_t fr = 0, tot = 0;
     SPD_CUDA(cudaMemGetInfo(&fr, &tot));
     h->stored_mode = 1;
-    h->sym_budget = (env && env[0] == '1') ? need : std::min(need, 0.4 * (double)fr);
+    // store as much as fits, keeping 6 GB and 15 % of the free memory for everything else
+    h->sym_budget = (env && env[0] == '1') ? need
+                                           : std::min(need, std::max(0.0, std::min(0.85 * (double)fr,
+                                                                                    (double)fr - 6e9)));
     if (const char* b = getenv("SPD_SYM_BUDGET")) h->sym_budget = std::min(need, atof(b));   // bytes (tests)
     // Blocks past the memory budget are evaluated on the fly.  (Measured on C2: the
     // evaluation path runs at ~1e11 entries/s inside the sym kernel against ~8e11

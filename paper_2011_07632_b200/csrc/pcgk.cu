@@ -218,6 +218,9 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     const int L = t.L;
     if (L < 2 || !M || A->stored_mode != 1) return false;
     h2sym_build(A, A->sym_budget, s);
+    // blocks evaluated on the fly: the stand-alone kernels (CUDA-graph path) run them at
+    // full occupancy, the persistent kernel would with 8 warps per SM
+    if (A->sym.stored_frac < 1.0 && !getenv("SPD_PCG_PERSISTENT_EVAL")) return false;
     stage_mark(s, "pcg h2sym_build");
     auto* im = new PcgPersistent::Impl();
     pk.impl = im;

@@ -68,7 +68,12 @@ void init_mem_pool() {
         if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) { cudaGetLastError(); return; }
-        uint64_t thr = (uint64_t)24 << 30;     // keep up to 24 GB cached between calls
+        // keep up to half of the device memory cached in the pool: the builds at N = 2^20
+        // work with tens of GB, and returning them to the OS at every synchronization
+        // (then mapping them again) costs seconds
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); tot = (size_t)48 << 30; }
+        uint64_t thr = (uint64_t)(tot / 2);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     });
 }

@@ -469,6 +469,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         DBuf<int> info(nl); DBuf<double> bad(nl); info.zero(s);
         potrf_batched(s, md, info.p, bad.p);                        // A_ii = S_i S_i^T
         check_info(s, info, bad, 1, l1.first, "leaf block A_ii");
+        stage_mark(s, "hss leaf potrf");
     }
     {
         std::vector<TrsmDesc> td;                                   // Lambda = S^{-1} Y^(1)_i (in place)
@@ -479,6 +480,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         std::vector<int> ldA(nl, (int)N);
         for (int a = 0; a < nl; ++a) A[a] = Yk(1) + t.begin[l1.first + a];
         sketch_qr(H, s, l1, A, ldA);                               // V_i, rank, Phi^T = S^{-T} V
+        stage_mark(s, "hss leaf sketch qr");
     }
     // (Phi U)^T = E^T Phi^T for active leaves
     const H2Level& h1 = h->lv[1];
@@ -510,6 +512,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     // leaf B_ij: Type-1 (near, on the fly) and Type-3 (skeletons, on the fly)
     {
         alloc_B(l1, h->lists.type1[1], h->lists.type3[1], l1.first);
+        stage_mark(s, "hss leaf PU/T/allocB");
         std::vector<KbBlock> blocks;
         std::vector<const double*> X, Left;
         std::vector<int> ldX, ldLeft;
@@ -522,6 +525,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         std::vector<PairProd> pairs;
         for (auto& pr : h->lists.type1[1]) if (pr.first < pr.second) pairs.push_back({pr.first, pr.second});
         kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1);
+        stage_mark(s, "hss leaf B type1");
         blocks.clear(); X.clear(); ldX.clear(); Left.clear(); ldLeft.clear();
         for (int a = 0; a < nl; ++a) {
             blocks.push_back({h1.skelX.p + h1.off[a], h1.S, h1.rank[a], -1});
@@ -572,6 +576,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             DBuf<int> info(n); DBuf<double> bad(n); info.zero(s);
             potrf_batched(s, md, info.p, bad.p);
             check_info(s, info, bad, k, lv.first, "I + B_ii");
+            stage_mark(s, "hss lvl potrf");
         }
         if (k == L) break;
         // Alg. 3 sketch: Lambda_i = F^{-1} [T_c1; T_c2]^(k)
@@ -594,6 +599,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             std::vector<int> ldA(n);
             for (int a = 0; a < n; ++a) { A[a] = Lam.p + lam_off[a]; ldA[a] = std::max(1, lv.m[a]); }
             sketch_qr(H, s, lv, A, ldA);                           // Vbar', P = F^{-T} Vbar'
+            stage_mark(s, "hss lvl sketch qr");
         }
         // R_i = F_i Vbar'_i
         lv.Rt.alloc(std::max<int64_t>(1, lv.V_off[n]));
@@ -646,6 +652,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         }
         // B_ij at level k
         alloc_B(lv, h->lists.type1[k], h->lists.type3[k], lv.first);
+        stage_mark(s, "hss lvl PU/T/allocB");
         {   // Type-1: B_ij = P_i^T bold(B_ij) P_j
             std::vector<Pair> t1;
             for (auto& pr : h->lists.type1[k]) if (pr.first < pr.second) t1.push_back(pr);
