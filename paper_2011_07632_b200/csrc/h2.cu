@@ -494,7 +494,9 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     // Blocks past the memory budget are evaluated on the fly.  (Measured on C2: the
     // evaluation path runs at ~1e11 entries/s inside the sym kernel against ~8e11
     // streamed, so nothing is evaluated while memory allows.)  SPD_SYM_FRAC: test hook.
-    h->sym_frac = 1.0;
+    // When not everything fits, the stored fraction is spread evenly over the bands, so
+    // streamed and evaluated bands interleave and HBM and the FP64 pipe work together.
+    h->sym_frac = need > 0.0 && h->sym_budget < need ? h->sym_budget / need : 1.0;
     if (const char* f = getenv("SPD_SYM_FRAC")) h->sym_frac = atof(f);
 }
 
