@@ -88,6 +88,23 @@ typedef struct {
  * Errors: SPD_EINVAL (bad nranks / rank), SPD_ENCCL (library or NCCL failure). */
 spd_status spd_comm_unique_id(void* nccl_unique_id_out);
 spd_status spd_comm_init(const void* nccl_unique_id, int nranks, int rank, spd_comm_t* out);
+
+/* Host-staged collectives: the same sharded path with every exchange routed through
+ * caller callbacks on host buffers (the library drains the stream, copies the device
+ * buffer to pageable host memory, calls, copies back).  For transports without NCCL
+ * (e.g. torch.distributed over gloo) and for multi-process tests of the sharded path;
+ * slow by construction.  Callbacks return 0 on success (else SPD_ENCCL), operate in
+ * place, and are called by every rank in the same order:
+ *   allreduce_sum_f64 / _i32: buf[0..n) = sum over ranks
+ *   broadcast:                buf[0..bytes) = root's buf
+ * ops is copied; ctx is passed back untouched and must outlive the communicator. */
+typedef struct {
+    void* ctx;
+    int (*allreduce_sum_f64)(void* ctx, double* buf, size_t n);
+    int (*allreduce_sum_i32)(void* ctx, int* buf, size_t n);
+    int (*broadcast)(void* ctx, void* buf, size_t bytes, int root);
+} spd_host_coll;
+spd_status spd_comm_init_host(const spd_host_coll* ops, int nranks, int rank, spd_comm_t* out);
 void spd_comm_free(spd_comm_t c);
 
 /* h2_build: H2 representation of A = K(X, X) + shift I.
@@ -168,7 +185,10 @@ enum {
                                sibling B_{c1 c2} (r_c1 r_c2) for every nonleaf parent
                                in heap order; all column-major                   */
     SPD_Q_HSS_PIVOTS = 23,  /* int32[sum w]: QRCP pivots of every node (w each) */
-    SPD_Q_TIMINGS = 30      /* double[16]: phase seconds of the last build      */
+    SPD_Q_TIMINGS = 30,     /* double[16]: phase seconds of the last build      */
+    SPD_Q_SHARD_WORK = 31   /* int64[2]: nodes whose per-node work (H2: proxy ID; HSS:
+                               factorisation, QRCP, bases) this process computed, and
+                               the number of such nodes; equal unless sharded (§8(e)) */
 };
 spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
 

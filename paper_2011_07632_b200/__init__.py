@@ -20,6 +20,7 @@ LAYOUT_ORIGINAL, LAYOUT_TREE = 0, 1
 Q_N, Q_LEVELS, Q_PERM, Q_NODES, Q_BOXES, Q_NNODES, Q_H2_RANKS, Q_SKELETONS = 1, 2, 3, 4, 5, 6, 7, 8
 Q_LIST_COUNTS, Q_NEAR, Q_TYPE3, Q_TYPE1 = 9, 10, 11, 12
 Q_HSS_RANKS, Q_HSS_EXPORT_SIZE, Q_HSS_EXPORT, Q_HSS_PIVOTS, Q_TIMINGS = 20, 21, 22, 23, 30
+Q_SHARD_WORK = 31
 
 
 class SpdError(RuntimeError):
@@ -62,6 +63,7 @@ def lib():
         "spd_last_error": ([], ctypes.c_char_p),
         "spd_comm_init": ([vp, c_int, c_int, P(vp)], c_int),
         "spd_comm_unique_id": ([vp], c_int),
+        "spd_comm_init_host": ([P(_HostColl), c_int, c_int, P(vp)], c_int),
         "spd_test_shard_owner": ([c_int, c_int, c_int], c_int),
         "spd_comm_free": ([vp], None),
         "h2_build": ([vp, i64, c_int, _Kernel, c_int, c_double, P(_H2Opts), vp, vp, P(vp)], c_int),
@@ -95,7 +97,7 @@ def lib():
     return L
 
 
-EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
+EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_init_host", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
             "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error"]
 
 
@@ -205,6 +207,10 @@ class H2:
     def timings(self):
         return self.query(Q_TIMINGS, np.float64, 16)
 
+    def shard_work(self):
+        """(nodes whose per-node work this process computed, nodes with per-node work)."""
+        return tuple(int(v) for v in self.query(Q_SHARD_WORK, np.int64, 2))
+
     def proxies(self, node):
         n_p = 4096 if self.d == 2 else 6144
         return None if node < 0 else _proxies(self, node)
@@ -233,6 +239,60 @@ class Comm:
         if getattr(self, "ptr", None) and _lib is not None:
             _lib.spd_comm_free(self.ptr)
             self.ptr = None
+
+
+_F64CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t)
+_I32CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_size_t)
+_BCB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int)
+
+
+class _HostColl(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce_sum_f64", _F64CB), ("allreduce_sum_i32", _I32CB),
+                ("broadcast", _BCB)]
+
+
+class HostComm(Comm):
+    """Host-staged communicator (spd_comm_init_host): the library's sharded path with
+    every exchange done by torch.distributed on host tensors (any backend that takes
+    CPU tensors, e.g. gloo).  For tests of the sharded path in several processes
+    (possibly sharing one GPU); NCCL (Comm) is the production transport."""
+
+    def __init__(self, group=None):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        self.ptr = ctypes.c_void_p()
+        nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+
+        def view(ptr, n, ctype, dtype):
+            return torch.from_numpy(np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), (n,)))
+
+        def f64(_ctx, buf, n):
+            try:
+                dist.all_reduce(view(buf, n, ctypes.c_double, None), group=group)
+                return 0
+            except Exception:          # noqa: BLE001 -- reported to the library as a failed collective
+                return 1
+
+        def i32(_ctx, buf, n):
+            try:
+                dist.all_reduce(view(buf, n, ctypes.c_int, None), group=group)
+                return 0
+            except Exception:          # noqa: BLE001
+                return 1
+
+        def bcast(_ctx, buf, nbytes, root):
+            try:
+                src = dist.get_global_rank(group, root) if group is not None else root
+                dist.broadcast(view(buf, nbytes, ctypes.c_uint8, None), src=src, group=group)
+                return 0
+            except Exception:          # noqa: BLE001
+                return 1
+
+        self._cbs = (_F64CB(f64), _I32CB(i32), _BCB(bcast))      # kept alive with the communicator
+        self._ops = _HostColl(None, *self._cbs)
+        _check(lib().spd_comm_init_host(ctypes.byref(self._ops), int(nranks), int(rank), ctypes.byref(self.ptr)))
+        self.nranks, self.rank = nranks, rank
 
 
 def comm_unique_id():
@@ -298,6 +358,10 @@ class HSS:
 
     def timings(self):
         return self.query(Q_TIMINGS, np.float64, 16)
+
+    def shard_work(self):
+        """(nodes whose per-node work this process computed, nodes with per-node work)."""
+        return tuple(int(v) for v in self.query(Q_SHARD_WORK, np.int64, 2))
 
 
 def spdhss_build(h2, rank_cap, rel_tol, oversample=10, seed=0, omega=None):

@@ -40,6 +40,12 @@ spd_status spd_comm_init(const void* id, int nranks, int rank, spd_comm_t* out) 
         *out = comm_create(id, nranks, rank);
     })
 }
+spd_status spd_comm_init_host(const spd_host_coll* ops, int nranks, int rank, spd_comm_t* out) {
+    SPD_TRY({
+        SPD_REQUIRE(out != nullptr, "spd_comm_init_host: out is NULL");
+        *out = comm_create_host(ops, nranks, rank);
+    })
+}
 void spd_comm_free(spd_comm_t c) { comm_destroy(c); }
 
 int spd_test_shard_owner(int nranks, int count, int a) {
@@ -222,6 +228,13 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
         SPD_REQUIRE(handle != nullptr && buf != nullptr, "spd_query: null argument");
         if (what >= SPD_Q_HSS_RANKS && what < SPD_Q_TIMINGS) {
             hss_query((const spd_hss_s*)handle, what, buf, bytes);
+            return SPD_OK;
+        }
+        if (what == SPD_Q_SHARD_WORK) {
+            const spd_hss_s* H = hss_if_hss(handle);
+            const int64_t* sw = H ? hss_shard_work(H) : ((const spd_h2_s*)handle)->shard_work;
+            need(bytes, 2 * sizeof(int64_t));
+            std::memcpy(buf, sw, 2 * sizeof(int64_t));
             return SPD_OK;
         }
         if (what == SPD_Q_TIMINGS) {

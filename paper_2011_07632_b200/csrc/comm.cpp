@@ -12,6 +12,12 @@
 // single process on one GPU: every virtual rank's share is computed in turn and the
 // exchange is the identity.  It exercises the ownership / ordering logic of the
 // sharded build against the unsharded one (tests), not the transport.
+//
+// A "host-staged" communicator (spd_comm_init_host) runs every collective through
+// caller-supplied host callbacks (e.g. torch.distributed over gloo): the stream is
+// drained, the buffer goes through host memory.  Several processes can then run the
+// real sharded path -- separate address spaces, real exchanges -- on one GPU or on
+// CPU-only transports; tests use it, production uses NCCL.
 #include <dlfcn.h>
 #include <cstring>
 #include "comm.hpp"
@@ -84,6 +90,37 @@ spd_comm_s* comm_create(const void* id, int nranks, int rank) {
     return c;
 }
 
+spd_comm_s* comm_create_host(const spd_host_coll* ops, int nranks, int rank) {
+    SPD_REQUIRE(ops && ops->allreduce_sum_f64 && ops->allreduce_sum_i32 && ops->broadcast,
+                "spd_comm_init_host: missing callback");
+    SPD_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "spd_comm_init_host: bad nranks / rank");
+    SPD_REQUIRE((nranks & (nranks - 1)) == 0, "spd_comm_init_host: nranks must be a power of 2 (binary subtrees)");
+    auto* c = new spd_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->hosted = true;
+    c->host = *ops;
+    return c;
+}
+
+namespace {
+// host-staged collective: stream drained, buffer through pageable host memory
+void host_check(int r, const char* what) {
+    if (r != 0) throw Error(SPD_ENCCL, std::string("host collective ") + what + " failed");
+}
+template <class T>
+void host_allreduce(const spd_comm_s* c, T* buf, size_t n, cudaStream_t s,
+                    int (*fn)(void*, T*, size_t)) {
+    if (!n) return;
+    std::vector<T> h(n);
+    SPD_CUDA(cudaMemcpyAsync(h.data(), buf, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    host_check(fn(c->host.ctx, h.data(), n), "allreduce");
+    SPD_CUDA(cudaMemcpyAsync(buf, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+
 void comm_destroy(spd_comm_s* c) {
     if (!c) return;
     if (c->nccl) nccl().destroy(c->nccl);
@@ -100,6 +137,19 @@ int shard_owner(const spd_comm_s* c, int count, int a) {
 void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::vector<int64_t>& begin,
                        const std::vector<int64_t>& end, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;   // one copy of everything already
+    if (c->hosted) {
+        SPD_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < c->nranks; ++q) {
+            const int64_t n = end[q] - begin[q];
+            if (n <= 0) continue;
+            std::vector<char> h((size_t)n * elem);
+            char* p = (char*)buf + (size_t)begin[q] * elem;
+            if (q == c->rank) SPD_CUDA(cudaMemcpy(h.data(), p, h.size(), cudaMemcpyDeviceToHost));
+            host_check(c->host.broadcast(c->host.ctx, h.data(), h.size(), q), "broadcast");
+            if (q != c->rank) SPD_CUDA(cudaMemcpy(p, h.data(), h.size(), cudaMemcpyHostToDevice));
+        }
+        return;
+    }
     NcclApi& api = nccl();
     check(api.group_start(), "ncclGroupStart");
     for (int q = 0; q < c->nranks; ++q) {
@@ -113,10 +163,12 @@ void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::v
 
 void comm_allreduce_sum(const spd_comm_s* c, double* buf, size_t n, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
+    if (c->hosted) return host_allreduce<double>(c, buf, n, s, c->host.allreduce_sum_f64);
     check(nccl().allreduce(buf, buf, n, NCCL_FLOAT64, NCCL_SUM, c->nccl, s), "ncclAllReduce");
 }
 void comm_allreduce_sum(const spd_comm_s* c, int* buf, size_t n, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
+    if (c->hosted) return host_allreduce<int>(c, buf, n, s, c->host.allreduce_sum_i32);
     check(nccl().allreduce(buf, buf, n, NCCL_INT32, NCCL_SUM, c->nccl, s), "ncclAllReduce");
 }
 

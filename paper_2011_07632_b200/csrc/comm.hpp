@@ -7,6 +7,8 @@ struct spd_comm_s {
     int nranks = 1, rank = 0;
     bool virt = false;          // single-process emulation of nranks ranks (tests)
     void* nccl = nullptr;       // ncclComm_t
+    bool hosted = false;        // host-staged collectives through caller callbacks
+    spd_host_coll host{};
 };
 
 namespace spd {
@@ -15,6 +17,9 @@ struct Nccl128 { char b[128]; };   // ncclUniqueId
 
 void comm_unique_id(void* out128);
 spd_comm_s* comm_create(const void* id, int nranks, int rank);
+spd_comm_s* comm_create_host(const spd_host_coll* ops, int nranks, int rank);
+// true when collectives really move data (NCCL or host-staged), i.e. the sharded path runs
+inline bool comm_real(const spd_comm_s* c) { return c && c->nranks > 1 && !c->virt; }
 void comm_destroy(spd_comm_s* c);
 // owner rank of node a (0 <= a < count) of a level, -1 when the level is redundant
 int shard_owner(const spd_comm_s* c, int count, int a);

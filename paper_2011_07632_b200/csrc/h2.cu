@@ -266,6 +266,8 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             }
             if (!cur.nodes.empty()) chunks.push_back(cur);
         }
+        for (auto& ch : chunks) h->shard_work[0] += (int64_t)ch.nodes.size();
+        h->shard_work[1] += (int64_t)nodes.size();
         // final outputs need ranks: keep each chunk's Mt until E is built
         std::vector<int> rank_h(lv.count, 0);
         // E, skel built per chunk into temporaries, then packed

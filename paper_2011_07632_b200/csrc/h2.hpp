@@ -69,6 +69,7 @@ struct spd_h2_s {
     spd::DBuf<int64_t> perm;      // tree position -> original index
     std::vector<spd::H2Level> lv; // [0..L-1], level k at lv[k] (lv[0] unused)
     double timings[16] = {0};
+    int64_t shard_work[2] = {0, 0};  // nodes ID'd by this process / nodes with an ID (sharding evidence)
     // matvec workspace
     int64_t ws_k = 0;
     spd::DBuf<double> xt, yt;

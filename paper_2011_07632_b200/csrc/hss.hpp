@@ -42,6 +42,7 @@ struct spd_hss_s {
     double tol = 0.0;
     std::vector<spd::HssLevel> lv;   // levels 1..L (level L: root factor only)
     double timings[16] = {0};
+    int64_t shard_work[2] = {0, 0};  // nodes factorised by this process / nodes (sharding evidence)
     int64_t sketch_groups = 0;       // instrumentation: number of Y^(k) sketch groups
     // solve workspace
     int64_t ws_k = 0;
@@ -79,5 +80,6 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
 void pcg_persistent_run(PcgPersistent& pk, double rz, double nb, double tol, int maxit, double out[4], cudaStream_t s);
 const spd_hss_s* hss_if_hss(const void* handle);      // nullptr when handle is not an HSS
 const double* hss_timings(const spd_hss_s* H);
+const int64_t* hss_shard_work(const spd_hss_s* H);
 inline uint64_t pair_key(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uint32_t)j; }
 }  // namespace spd

@@ -21,6 +21,7 @@
 //  P:1053  R_i = F_i Vbar'_i   (= (I+B)^{1/2} Vbar_i)
 //  root    F_root = chol(I + B_root) for the solve (reading R11)
 #include "hss.hpp"
+#include "comm.hpp"
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -103,8 +104,37 @@ static void check_info(cudaStream_t s, const DBuf<int>& info, const DBuf<double>
         }
 }
 
+// ================================================================= subtree sharding
+// With a real communicator (NCCL or host-staged; comm.cpp) of P ranks, at every level
+// with >= P nodes rank p computes only the per-node work of its subtree (shard_owner,
+// the H2 build's plan): Y^(k) rows of its leaves, factorisations, QRCP and bases of its
+// nodes, the B_ij of pairs whose first node it owns.  Level arrays start zeroed and are
+// all-reduced (summed) once their owners have written them, so every rank ends with the
+// full HSS (the solve and PCG run replicated).  Levels with fewer nodes run redundantly.
+struct HssShard {
+    const spd_comm_s* c = nullptr;
+    bool real = false;
+    bool on(int count) const { return real && count >= c->nranks; }
+    std::vector<char> own(int count) const {
+        std::vector<char> o(count, 1);
+        if (on(count))
+            for (int a = 0; a < count; ++a) o[a] = shard_owner(c, count, a) == c->rank;
+        return o;
+    }
+    void zero(DBuf<double>& b, int count, cudaStream_t s) const { if (on(count)) b.zero(s); }
+    void sum(DBuf<double>& b, int64_t n, int count, cudaStream_t s) const {
+        if (on(count) && n > 0) comm_allreduce_sum(c, b.p, (size_t)n, s);
+    }
+    void sum(DBuf<int>& b, int64_t n, int count, cudaStream_t s) const {
+        if (on(count) && n > 0) comm_allreduce_sum(c, b.p, (size_t)n, s);
+    }
+};
+
 // ================================================================= Y^(k) by LCA buckets
-static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& Y, cudaStream_t s) {
+// sharded: near and coupling targets restricted to the owned nodes, so exactly the Y
+// rows of the owned leaves are complete (the only rows this rank reads)
+static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& Y, const HssShard& sh,
+                                  cudaStream_t s) {
     spd_h2_s* h = H->h2;
     const TreeH& t = h->tree;
     const int L = t.L, w = H->w;
@@ -121,8 +151,10 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
         std::vector<KbEntry> entries;
         size_t e = 0;
         const auto& near = h->lists.near;
+        const std::vector<char> own = sh.own(nl);
         while (e < near.size()) {
             const int i = near[e].first;
+            if (!own[i - l1]) { ++e; continue; }
             std::vector<std::pair<int, int>> js;       // (lca, j)
             while (e < near.size() && near[e].first == i) {
                 if (near[e].second != i) js.push_back({t.lca_level(i, near[e].second), near[e].second});
@@ -166,9 +198,11 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
         for (int a = 0; a < lv.count; ++a) blocks.push_back({lv.skelX.p + lv.off[a], lv.S, lv.rank[a], -1});
         std::vector<KbTarget> targets;
         std::vector<KbEntry> entries;
+        const std::vector<char> own = sh.own(lv.count);
         size_t e = 0;
         while (e < T3.size()) {
             const int i = T3[e].first, a = i - lv.first;
+            if (!own[a]) { ++e; continue; }
             std::vector<std::pair<int, int>> js;
             while (e < T3.size() && T3[e].first == i) { js.push_back({t.lca_level(i, T3[e].second), T3[e].second}); ++e; }
             std::stable_sort(js.begin(), js.end(), [](auto& x, auto& y) { return x.first < y.first; });
@@ -256,15 +290,21 @@ static void alloc_B(HssLevel& lv, const std::vector<Pair>& t1, const std::vector
 
 // QRCP of the per-node sketches; ranks to host; explicit V (m x r)
 static void sketch_qr(spd_hss_s* H, cudaStream_t s, HssLevel& lv, const std::vector<double*>& A,
-                      const std::vector<int>& ldA) {
+                      const std::vector<int>& ldA, const HssShard& sh) {
     const int n = lv.count, w = H->w;
+    const std::vector<char> own = sh.own(n);
     DBuf<int> piv((size_t)n * w), rank(n);
     DBuf<double> beta((size_t)n * w), norms((size_t)n * w);
+    if (sh.on(n)) { piv.zero(s); rank.zero(s); }
+    for (int a = 0; a < n; ++a) H->shard_work[0] += own[a];
+    H->shard_work[1] += n;
     std::vector<QrcpDesc> qd;
     for (int a = 0; a < n; ++a)
-        qd.push_back({A[a], lv.m[a], w, ldA[a], std::min(H->cap, std::min(lv.m[a], w)), piv.p + (size_t)a * w,
+        if (own[a]) qd.push_back({A[a], lv.m[a], w, ldA[a], std::min(H->cap, std::min(lv.m[a], w)), piv.p + (size_t)a * w,
                       beta.p + (size_t)a * w, rank.p + a, norms.p + (size_t)a * w});
     qrcp_batched(s, qd, H->tol);
+    sh.sum(rank, n, n, s);
+    sh.sum(piv, (int64_t)n * w, n, s);
     lv.rank = rank.download(s);
     lv.piv = piv.download(s);
     lv.off.assign(n + 1, 0);
@@ -275,9 +315,10 @@ static void sketch_qr(spd_hss_s* H, cudaStream_t s, HssLevel& lv, const std::vec
     }
     lv.R = lv.off[n];
     lv.V.alloc(std::max<int64_t>(1, lv.V_off[n]));
+    sh.zero(lv.V, n, s);
     std::vector<FormQDesc> fq;
     for (int a = 0; a < n; ++a)
-        fq.push_back({A[a], beta.p + (size_t)a * w, rank.p + a, lv.V.p + lv.V_off[a], lv.m[a], w, ldA[a],
+        if (own[a]) fq.push_back({A[a], beta.p + (size_t)a * w, rank.p + a, lv.V.p + lv.V_off[a], lv.m[a], w, ldA[a],
                       std::max(1, lv.m[a])});
     formq_batched(s, fq);
     // P = F^{-T} V  (leaf: Phi^T = S^{-T} V)
@@ -285,9 +326,12 @@ static void sketch_qr(spd_hss_s* H, cudaStream_t s, HssLevel& lv, const std::vec
     SPD_CUDA(cudaMemcpyAsync(lv.P.p, lv.V.p, sizeof(double) * lv.V_off[n], cudaMemcpyDeviceToDevice, s));
     std::vector<TrsmDesc> td;
     for (int a = 0; a < n; ++a)
-        td.push_back({lv.F.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a], std::max(1, lv.m[a]),
-                      std::max(1, lv.m[a])});
+        if (own[a])
+            td.push_back({lv.F.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a], std::max(1, lv.m[a]),
+                          std::max(1, lv.m[a])});
     trsm_batched(s, td, 'L', true);
+    sh.sum(lv.V, lv.V_off[n], n, s);                  // bases of every node, for the B_ij of cross pairs
+    sh.sum(lv.P, lv.V_off[n], n, s);
 }
 
 // ================================================================= solve factors
@@ -299,27 +343,29 @@ __global__ void set_identity_kernel(const MatDesc* descs) {
         d.A[i + (size_t)j * d.ld] = (i == j) ? 1.0 : 0.0;
     }
 }
-static void invert_factors(cudaStream_t s, HssLevel& lv) {
+static void invert_factors(cudaStream_t s, HssLevel& lv, const HssShard& sh) {
     const int n = lv.count;
     if (n == 0 || lv.F_off.empty()) return;
     lv.Finv.alloc(std::max<int64_t>(1, lv.F_off[n]));
+    sh.zero(lv.Finv, n, s);
+    const std::vector<char> own = sh.own(n);
     std::vector<MatDesc> md;
     std::vector<TrsmDesc> td;
     for (int a = 0; a < n; ++a) {
         const int m = lv.m[a];
-        if (!m) continue;
+        if (!m || !own[a]) continue;
         md.push_back({lv.Finv.p + lv.F_off[a], m, m, m});
         td.push_back({lv.F.p + lv.F_off[a], lv.Finv.p + lv.F_off[a], m, m, m, m});
     }
-    if (md.empty()) return;
-    {
+    if (!md.empty()) {
         DevArray<MatDesc> dm(s, md);
         for (size_t off = 0; off < md.size(); off += 65535) {
             set_identity_kernel<<<dim3(8, (unsigned)std::min<size_t>(65535, md.size() - off)), 256, 0, s>>>(dm.p + off);
             SPD_LAUNCH();
         }
+        trsm_batched(s, td, 'L', false);              // F^{-1} = F \ I (lower triangular)
     }
-    trsm_batched(s, td, 'L', false);                  // F^{-1} = F \ I (lower triangular)
+    sh.sum(lv.Finv, lv.F_off[n], n, s);
 }
 
 // ================================================================= dense top of the solve
@@ -413,6 +459,8 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     const int L = t.L, w = H->w, d = h->d;
     const int64_t N = h->N;
     const double t0 = now_s();
+    const HssShard sh{h->comm, comm_real(h->comm)};
+    H->shard_work[0] = H->shard_work[1] = 0;
     H->lv.clear();
     H->lv.resize(L + 1);
     if (L == 1) {                                   // single node: the HSS is the dense block
@@ -424,7 +472,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         DBuf<int> info(1); DBuf<double> bad(1); info.zero(s);
         potrf_batched(s, {{r.F.p, (int)N, (int)N, (int)N}}, info.p, bad.p);
         check_info(s, info, bad, 1, 0, "leaf block A_ii");
-        invert_factors(s, r);
+        invert_factors(s, r, HssShard{});
         return;
     }
     // ---------------- Omega (parity hook or Philox)
@@ -439,7 +487,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     // ---------------- P:1009  all Y^(k)
     DBuf<double> Y;
     stage_mark(s, nullptr);
-    lca_bucketed_products(H, om, Y, s);
+    lca_bucketed_products(H, om, Y, sh, s);
     auto Yk = [&](int k) { return Y.p + (size_t)(k - 1) * N * w; };
     SPD_CUDA(cudaStreamSynchronize(s));
     const double t1 = now_s();
@@ -457,10 +505,13 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         l1.F_off[a + 1] = l1.F_off[a] + (int64_t)l1.m[a] * l1.m[a];
     }
     l1.F.alloc(l1.F_off[nl]);
+    sh.zero(l1.F, nl, s);
+    const std::vector<char> own1 = sh.own(nl);
     {
         std::vector<DenseKDesc> dk;
         std::vector<MatDesc> md;
         for (int a = 0; a < nl; ++a) {
+            if (!own1[a]) continue;
             const int i = l1.first + a;
             dk.push_back({h->X.p + t.begin[i], N, l1.m[a], t.begin[i], l1.F.p + l1.F_off[a], l1.m[a]});
             md.push_back({l1.F.p + l1.F_off[a], l1.m[a], l1.m[a], l1.m[a]});
@@ -474,12 +525,13 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     {
         std::vector<TrsmDesc> td;                                   // Lambda = S^{-1} Y^(1)_i (in place)
         for (int a = 0; a < nl; ++a)
-            td.push_back({l1.F.p + l1.F_off[a], Yk(1) + t.begin[l1.first + a], l1.m[a], w, l1.m[a], (int)N});
+            if (own1[a])
+                td.push_back({l1.F.p + l1.F_off[a], Yk(1) + t.begin[l1.first + a], l1.m[a], w, l1.m[a], (int)N});
         trsm_batched(s, td, 'L', false);
         std::vector<double*> A(nl);
         std::vector<int> ldA(nl, (int)N);
         for (int a = 0; a < nl; ++a) A[a] = Yk(1) + t.begin[l1.first + a];
-        sketch_qr(H, s, l1, A, ldA);                               // V_i, rank, Phi^T = S^{-T} V
+        sketch_qr(H, s, l1, A, ldA, sh);                               // V_i, rank, Phi^T = S^{-T} V
         stage_mark(s, "hss leaf sketch qr");
     }
     // (Phi U)^T = E^T Phi^T for active leaves
@@ -490,28 +542,35 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         lv.PU.alloc(std::max<int64_t>(1, lv.PU_off[lv.count]));
     };
     alloc_PU(l1, h1);
+    sh.zero(l1.PU, nl, s);
     {
         std::vector<GemmDesc> gd;
         for (int a = 0; a < nl; ++a)
-            if (h1.rank[a] && l1.rank[a])
+            if (own1[a] && h1.rank[a] && l1.rank[a])
                 gd.push_back({h1.E.p + h1.E_off[a], l1.P.p + l1.V_off[a], l1.PU.p + l1.PU_off[a], h1.rank[a],
                               l1.rank[a], l1.m[a], h1.ncand[a], l1.m[a], h1.rank[a]});
         gemm_batched(s, gd, true, false, 1.0, 0.0);
     }
+    sh.sum(l1.PU, l1.PU_off[nl], nl, s);
+    // the last sharded level hands its pending sketches to the redundant level above
+    auto handoff = [&](int k) { return sh.on(t.count(k)) && k + 1 <= L && !sh.on(t.count(k + 1)); };
     // pending sketches T^(k') = Phi_i Y_i^(k'), k' = 2..L-1  (Alg. 3 step 1)
     std::vector<DBuf<double>> Tprev(L), Tcur(L);
     for (int kp2 = 2; kp2 < L; ++kp2) {
         Tprev[kp2].alloc(std::max<int64_t>(1, l1.R * w));
+        if (handoff(1)) Tprev[kp2].zero(s);
         std::vector<GemmDesc> gd;
         for (int a = 0; a < nl; ++a)
-            if (l1.rank[a])
+            if (own1[a] && l1.rank[a])
                 gd.push_back({l1.P.p + l1.V_off[a], Yk(kp2) + t.begin[l1.first + a], Tprev[kp2].p + l1.off[a],
                               l1.rank[a], w, l1.m[a], l1.m[a], (int)N, (int)std::max<int64_t>(1, l1.R)});
         gemm_batched(s, gd, true, false, 1.0, 0.0);
+        if (handoff(1)) sh.sum(Tprev[kp2], l1.R * w, nl, s);
     }
     // leaf B_ij: Type-1 (near, on the fly) and Type-3 (skeletons, on the fly)
     {
         alloc_B(l1, h->lists.type1[1], h->lists.type3[1], l1.first);
+        sh.zero(l1.B, nl, s);
         stage_mark(s, "hss leaf PU/T/allocB");
         std::vector<KbBlock> blocks;
         std::vector<const double*> X, Left;
@@ -522,8 +581,9 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             X.push_back(l1.P.p + l1.V_off[a]); ldX.push_back(std::max(1, l1.m[a]));
             Left.push_back(l1.P.p + l1.V_off[a]); ldLeft.push_back(std::max(1, l1.m[a]));
         }
-        std::vector<PairProd> pairs;
-        for (auto& pr : h->lists.type1[1]) if (pr.first < pr.second) pairs.push_back({pr.first, pr.second});
+        std::vector<PairProd> pairs;                                // B_ij by the owner of i (i < j)
+        for (auto& pr : h->lists.type1[1])
+            if (pr.first < pr.second && own1[pr.first - l1.first]) pairs.push_back({pr.first, pr.second});
         kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1);
         stage_mark(s, "hss leaf B type1");
         blocks.clear(); X.clear(); ldX.clear(); Left.clear(); ldLeft.clear();
@@ -533,8 +593,11 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             Left.push_back(l1.PU.p + l1.PU_off[a]); ldLeft.push_back(std::max(1, h1.rank[a]));
         }
         pairs.clear();
-        for (auto& pr : h->lists.type3[1]) if (pr.first < pr.second) pairs.push_back({pr.first, pr.second});
+        for (auto& pr : h->lists.type3[1])
+            if (pr.first < pr.second && own1[pr.first - l1.first]) pairs.push_back({pr.first, pr.second});
         kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1);
+        sh.sum(l1.B, l1.B.n, nl, s);
+        sh.sum(l1.F, l1.F_off[nl], nl, s);
     }
     SPD_CUDA(cudaStreamSynchronize(s));
     const double t2 = now_s();
@@ -558,10 +621,12 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         }
         lv.F.alloc(std::max<int64_t>(1, lv.F_off[n]));
         lv.F.zero(s);
+        const std::vector<char> own = sh.own(n);
         {   // I + B_ii (lower part: B_c2c1 = B_c1c2^T), then Cholesky
             std::vector<CopyDesc> cd;
             std::vector<MatDesc> md;
             for (int a = 0; a < n; ++a) {
+                if (!own[a]) continue;
                 const int i = lv.first + a, c1 = 2 * i + 1, c2 = 2 * i + 2;
                 const int m = lv.m[a];
                 if (r1[a] > 0 && m - r1[a] > 0) {
@@ -576,6 +641,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             DBuf<int> info(n); DBuf<double> bad(n); info.zero(s);
             potrf_batched(s, md, info.p, bad.p);
             check_info(s, info, bad, k, lv.first, "I + B_ii");
+            sh.sum(lv.F, lv.F_off[n], n, s);
             stage_mark(s, "hss lvl potrf");
         }
         if (k == L) break;
@@ -588,7 +654,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             std::vector<TrsmDesc> td;
             for (int a = 0; a < n; ++a) {
                 const int c1 = 2 * (lv.first + a) + 1 - pv.first;
-                if (lv.m[a] == 0) continue;
+                if (lv.m[a] == 0 || !own[a]) continue;
                 cd.push_back({Tprev[k].p + pv.off[c1], Lam.p + lam_off[a], lv.m[a], w, (int)std::max<int64_t>(1, pv.R),
                               lv.m[a], 0});
                 td.push_back({lv.F.p + lv.F_off[a], Lam.p + lam_off[a], lv.m[a], w, lv.m[a], lv.m[a]});
@@ -598,23 +664,26 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             std::vector<double*> A(n);
             std::vector<int> ldA(n);
             for (int a = 0; a < n; ++a) { A[a] = Lam.p + lam_off[a]; ldA[a] = std::max(1, lv.m[a]); }
-            sketch_qr(H, s, lv, A, ldA);                           // Vbar', P = F^{-T} Vbar'
+            sketch_qr(H, s, lv, A, ldA, sh);                       // Vbar', P = F^{-T} Vbar'
             stage_mark(s, "hss lvl sketch qr");
         }
         // R_i = F_i Vbar'_i
         lv.Rt.alloc(std::max<int64_t>(1, lv.V_off[n]));
+        sh.zero(lv.Rt, n, s);
         {
             std::vector<GemmDesc> gd;
             for (int a = 0; a < n; ++a)
-                if (lv.rank[a] && lv.m[a])
+                if (own[a] && lv.rank[a] && lv.m[a])
                     gd.push_back({lv.F.p + lv.F_off[a], lv.V.p + lv.V_off[a], lv.Rt.p + lv.V_off[a], lv.m[a], lv.rank[a],
                                   lv.m[a], lv.m[a], lv.m[a], lv.m[a]});
             gemm_batched(s, gd, false, false, 1.0, 0.0);
+            sh.sum(lv.Rt, lv.V_off[n], n, s);
         }
         // (Phi U)_i^T = E_i^T blockdiag((Phi U)_c^T) P_i
         const H2Level& hk = h->lv[k];
         const H2Level& hp = h->lv[k - 1];
         alloc_PU(lv, hk);
+        sh.zero(lv.PU, n, s);
         {
             std::vector<int64_t> woff(n + 1, 0);
             for (int a = 0; a < n; ++a) woff[a + 1] = woff[a] + (int64_t)hk.ncand[a] * lv.rank[a];
@@ -622,7 +691,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             W.zero(s);
             std::vector<GemmDesc> g1, g2;
             for (int a = 0; a < n; ++a) {
-                if (!hk.rank[a] || !lv.rank[a]) continue;
+                if (!own[a] || !hk.rank[a] || !lv.rank[a]) continue;
                 const int c1 = 2 * (lv.first + a) + 1 - pv.first;
                 const int sc1 = hp.rank[c1], sc2 = hp.rank[c1 + 1];
                 const int nc = hk.ncand[a];
@@ -638,24 +707,29 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             gemm_batched(s, g1, false, false, 1.0, 0.0);
             gemm_batched(s, g2, true, false, 1.0, 0.0);
         }
+        sh.sum(lv.PU, lv.PU_off[n], n, s);
         // pending sketches for k' > k: T_i = P_i^T [T_c1; T_c2]
         for (int kp2 = k + 1; kp2 < L; ++kp2) {
             Tcur[kp2].alloc(std::max<int64_t>(1, lv.R * w));
+            if (handoff(k)) Tcur[kp2].zero(s);
             std::vector<GemmDesc> gd;
             for (int a = 0; a < n; ++a) {
-                if (!lv.rank[a]) continue;
+                if (!own[a] || !lv.rank[a]) continue;
                 const int c1 = 2 * (lv.first + a) + 1 - pv.first;
                 gd.push_back({lv.P.p + lv.V_off[a], Tprev[kp2].p + pv.off[c1], Tcur[kp2].p + lv.off[a], lv.rank[a], w,
                               lv.m[a], lv.m[a], (int)std::max<int64_t>(1, pv.R), (int)std::max<int64_t>(1, lv.R)});
             }
             gemm_batched(s, gd, true, false, 1.0, 0.0);
+            if (handoff(k)) sh.sum(Tcur[kp2], lv.R * w, n, s);
         }
         // B_ij at level k
         alloc_B(lv, h->lists.type1[k], h->lists.type3[k], lv.first);
+        sh.zero(lv.B, n, s);
         stage_mark(s, "hss lvl PU/T/allocB");
-        {   // Type-1: B_ij = P_i^T bold(B_ij) P_j
+        {   // Type-1: B_ij = P_i^T bold(B_ij) P_j  (sharded: by the owner of i)
             std::vector<Pair> t1;
-            for (auto& pr : h->lists.type1[k]) if (pr.first < pr.second) t1.push_back(pr);
+            for (auto& pr : h->lists.type1[k])
+                if (pr.first < pr.second && own[pr.first - lv.first]) t1.push_back(pr);
             std::vector<int64_t> bo(t1.size() + 1, 0), go(t1.size() + 1, 0);
             for (size_t q = 0; q < t1.size(); ++q) {
                 const int a = t1[q].first - lv.first, b = t1[q].second - lv.first;
@@ -704,9 +778,11 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
                 Left.push_back(lv.PU.p + lv.PU_off[a]); ldLeft.push_back(std::max(1, hk.rank[a]));
             }
             std::vector<PairProd> pairs;
-            for (auto& pr : h->lists.type3[k]) if (pr.first < pr.second) pairs.push_back({pr.first, pr.second});
+            for (auto& pr : h->lists.type3[k])
+                if (pr.first < pr.second && own[pr.first - lv.first]) pairs.push_back({pr.first, pr.second});
             kernel_sandwich(H, s, pairs, blocks, lv.first, X, ldX, Left, ldLeft, lv.rank, lv);
         }
+        sh.sum(lv.B, lv.B.n, n, s);
         for (int kp2 = k + 1; kp2 < L; ++kp2) std::swap(Tprev[kp2], Tcur[kp2]);
         Tprev[k].release();
         SPD_CUDA(cudaStreamSynchronize(s));
@@ -714,7 +790,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     }
     // solve factors: explicit S_i^{-1}, F_i^{-1} (triangular inverses by blocked TRSM on I),
     // so every step of hss_solve is an HBM-bound GEMV
-    for (int k = 1; k <= L; ++k) invert_factors(s, H->lv[k]);
+    for (int k = 1; k <= L; ++k) invert_factors(s, H->lv[k], sh);
     build_top_operator(H, s);
     SPD_CUDA(cudaStreamSynchronize(s));
     stage_mark(s, "hss invert factors");
@@ -845,6 +921,7 @@ const spd_hss_s* hss_if_hss(const void* h) {
     return *(const uint32_t*)h == 0x48535348u ? (const spd_hss_s*)h : nullptr;
 }
 const double* hss_timings(const spd_hss_s* H) { return H->timings; }
+const int64_t* hss_shard_work(const spd_hss_s* H) { return H->shard_work; }
 
 static std::vector<double> dl(const double* p, int64_t n) {
     std::vector<double> v(n);
