@@ -91,12 +91,13 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
         if (k == 0) return SPD_OK;
         SPD_REQUIRE(X != nullptr && Y != nullptr, "h2_matvec: null X or Y");
         cudaStream_t s = (cudaStream_t)stream;
+        const bool shard = k >= 2;                 // multi-vector products are subtree-sharded
         if (layout == SPD_LAYOUT_TREE) {
-            h2_apply_tree(h, X, ldx, Y, ldy, (int)k, s);
+            h2_apply_tree(h, X, ldx, Y, ldy, (int)k, s, shard);
         } else {
             DBuf<double> xt((size_t)h->N * k), yt((size_t)h->N * k);
             permute_rows(s, h->perm.p, h->N, (int)k, X, ldx, xt.p, h->N, true);
-            h2_apply_tree(h, xt.p, h->N, yt.p, h->N, (int)k, s);
+            h2_apply_tree(h, xt.p, h->N, yt.p, h->N, (int)k, s, shard);
             permute_rows(s, h->perm.p, h->N, (int)k, yt.p, h->N, Y, ldy, false);
         }
     })

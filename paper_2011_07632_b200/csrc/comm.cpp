@@ -161,6 +161,31 @@ void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::v
     check(api.group_end(), "ncclGroupEnd");
 }
 
+void comm_bcast_rows(const spd_comm_s* c, double* buf, int64_t ld, int ncols, const std::vector<int64_t>& begin,
+                     const std::vector<int64_t>& end, cudaStream_t s) {
+    if (!c || c->nranks <= 1 || c->virt) return;
+    if (c->hosted) {
+        for (int j = 0; j < ncols; ++j) comm_bcast_ranges(c, buf + (size_t)j * ld, sizeof(double), begin, end, s);
+        return;
+    }
+    NcclApi& api = nccl();
+    constexpr int kGroupOps = 512;                 // bounded group size
+    int ops = 0;
+    check(api.group_start(), "ncclGroupStart");
+    for (int j = 0; j < ncols; ++j)
+        for (int q = 0; q < c->nranks; ++q) {
+            const int64_t n = end[q] - begin[q];
+            if (n <= 0) continue;
+            double* p = buf + (size_t)j * ld + begin[q];
+            check(api.bcast(p, p, (size_t)n, NCCL_FLOAT64, q, c->nccl, s), "ncclBroadcast");
+            if (++ops % kGroupOps == 0) {
+                check(api.group_end(), "ncclGroupEnd");
+                check(api.group_start(), "ncclGroupStart");
+            }
+        }
+    check(api.group_end(), "ncclGroupEnd");
+}
+
 void comm_allreduce_sum(const spd_comm_s* c, double* buf, size_t n, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
     if (c->hosted) return host_allreduce<double>(c, buf, n, s, c->host.allreduce_sum_f64);

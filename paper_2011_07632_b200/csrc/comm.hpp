@@ -26,6 +26,9 @@ int shard_owner(const spd_comm_s* c, int count, int a);
 // every rank q broadcasts elements [begin[q], end[q]) of buf (elem bytes each), in one group
 void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::vector<int64_t>& begin,
                        const std::vector<int64_t>& end, cudaStream_t s);
+// column-major rows: every rank q broadcasts rows [begin[q], end[q]) of all ncols columns
+void comm_bcast_rows(const spd_comm_s* c, double* buf, int64_t ld, int ncols, const std::vector<int64_t>& begin,
+                     const std::vector<int64_t>& end, cudaStream_t s);
 void comm_allreduce_sum(const spd_comm_s* c, double* buf, size_t n, cudaStream_t s);
 void comm_allreduce_sum(const spd_comm_s* c, int* buf, size_t n, cudaStream_t s);
 

@@ -581,11 +581,21 @@ void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double*
     }
 }
 
-void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s) {
+void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s,
+                   bool shard) {
     const TreeH& t = h->tree;
     const int L = t.L;
     const int64_t N = h->N;
-    if (k == 1 && h->stored_mode == 1) {
+    const spd_comm_s* cm = h->comm;
+    const int l1 = t.first(1), nl = t.count(1);
+    shard = shard && comm_real(cm) && nl >= cm->nranks;
+    // sharded: does this rank own node a of a level with `count` nodes (redundant levels: yes)
+    auto mine = [&](int count, int a) {
+        if (!shard) return true;
+        const int o = shard_owner(cm, count, a);
+        return o < 0 || o == cm->rank;
+    };
+    if (k == 1 && h->stored_mode == 1 && !shard) {
         // stored symmetric blocks: up pass, near + all coupling levels in one launch, gather, down pass
         h2sym_build(h, h->sym_budget, s);
         std::vector<double*> xh(L, nullptr), yh(L, nullptr);
@@ -601,6 +611,11 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
     std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
     near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
+    if (shard) {
+        std::vector<KbTarget> kept;
+        for (auto& tg : targets) if (mine(nl, tg.blk)) kept.push_back(tg);
+        targets.swap(kept);
+    }
     if (L == 1) {
         kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
         return;
@@ -625,6 +640,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         size_t e = 0;
         while (e < T3.size()) {
             const int i = T3[e].first, a = i - lv.first;
+            if (!mine(lv.count, a)) { ++e; continue; }
             KbTarget tg{b0 + a, (int)entries.size(), 0};
             while (e < T3.size() && T3[e].first == i) {
                 const int bj = T3[e].second - lv.first;
@@ -638,6 +654,16 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     }
     kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
     h2_down(h, yh, L - 1, y, ldy, k, s);
+    if (shard) {                                  // owners' leaf rows -> every rank
+        const int P = cm->nranks, per = nl / P;
+        std::vector<int64_t> rb(P), re(P);
+        for (int q = 0; q < P; ++q) {
+            const int i0 = l1 + q * per, i1 = l1 + (q + 1) * per - 1;
+            rb[q] = t.begin[i0];
+            re[q] = t.begin[i1] + t.size(i1);
+        }
+        comm_bcast_rows(cm, y, ldy, k, rb, re, s);
+    }
 }
 
 }  // namespace spd

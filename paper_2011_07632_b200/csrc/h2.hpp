@@ -84,9 +84,11 @@ struct spd_h2_s {
 };
 
 namespace spd {
-// y = A x in tree order (x, y: N x k, ld >= N); y is overwritten
+// y = A x in tree order (x, y: N x k, ld >= N); y is overwritten.  shard (real
+// communicator): near and coupling work only for the owned subtrees, then the owners'
+// rows of y are broadcast (x replicated; up/down passes redundant)
 void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
-                   cudaStream_t s);
+                   cudaStream_t s, bool shard = false);
 // gather/scatter between original and tree order
 void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const double* src, int64_t lds,
                   double* dst, int64_t ldd, bool to_tree);

@@ -2,8 +2,10 @@
 P processes (gloo rendezvous on 127.0.0.1) share cuda:0, each with its own address
 space and a host-staged communicator (spd_comm_init_host: every collective of the
 library goes through torch.distributed on host tensors).  Each rank computes only
-its subtrees' nodes of the H2 build (proxy-ID) and of the SPD-HSS build (Alg. 4,
-P:1001-1056), then exchanges -- the code path of an NCCL rank minus the transport.
+its subtrees' nodes of the H2 build (proxy-ID), of the SPD-HSS build (Alg. 4,
+P:1001-1056) and of a multi-vector H2 product (near + coupling blocks of its
+leaves, then a row exchange), then exchanges -- the code path of an NCCL rank minus
+the transport.
 
 Checks:
 * every rank ends with the identical H2 and HSS (bitwise: the exchanges are sums of
@@ -35,10 +37,12 @@ def _run(spd, synth, cfg, comm):
     x = spd.hss_solve(M, b).cpu().numpy()
     _, rep = spd.pcg_solve(h, M, b, tol=1e-8, maxit=500)
     y = spd.h2_matvec(h, b).cpu().numpy()
+    Xm = torch.tensor(synth.multivec(cfg.n, 8).T.copy(), device="cuda").t()     # column-major n x 8
+    ym = spd.h2_matvec(h, Xm).t().cpu().numpy()        # k >= 2: sharded product + row exchange
     ex = M.export()
     return {"h2_work": h.shard_work(), "hss_work": M.shard_work(), "h2_ranks": h.ranks(), "hss_ranks": M.ranks(),
-            "x": x, "y": y, "iters": rep.iters,
-            "sha": hashlib.sha256(ex.tobytes()).hexdigest() + hashlib.sha256(x.tobytes()).hexdigest()}
+            "x": x, "y": y, "ym": ym, "iters": rep.iters,
+            "sha": "".join(hashlib.sha256(a.tobytes()).hexdigest() for a in (ex, x, ym))}
 
 
 def _worker(rank, world, port, n, leaf, q):
@@ -92,5 +96,6 @@ def test_sharded_build_with_real_exchanges(P, n, leaf):
     assert np.abs(got["h2_ranks"] - ref["h2_ranks"]).max() <= 1
     assert np.abs(got["hss_ranks"] - ref["hss_ranks"]).max() <= 1
     assert np.linalg.norm(got["y"] - ref["y"]) <= 1e-11 * np.linalg.norm(ref["y"])
+    assert np.linalg.norm(got["ym"] - ref["ym"]) <= 1e-11 * np.linalg.norm(ref["ym"])
     assert np.linalg.norm(got["x"] - ref["x"]) <= 1e-10 * np.linalg.norm(ref["x"])
     assert abs(got["iters"] - ref["iters"]) <= 2
