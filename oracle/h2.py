@@ -26,9 +26,9 @@ from dataclasses import dataclass, field
 import numpy as np
 from scipy.linalg import solve_triangular
 
-from .kernels import kernel_matrix
+from .kernels import kernel_matrix, dofs_per_point, dof_points
 from .linalg import qrcp
-from .tree import Tree, Lists, build_tree, interaction_lists
+from .tree import Tree, Lists, build_tree, interaction_lists, expand_dofs
 
 HALTON_BASES = (2, 3, 5)
 
@@ -144,10 +144,15 @@ def default_n_proxy(d):
 
 
 def h2_build(X, kid, ell, shift, leaf, tol, n_proxy=0):
-    """H2 by proxy-point ID, bottom-up (R3, R4)."""
+    """H2 by proxy-point ID, bottom-up (R3, R4).  Tensor kernels (RPY, R28): the tree
+    is built on the points (leaf = points per leaf), then every index set, proxy set
+    and skeleton is over degrees of freedom (dof rows (x, y, z, c))."""
+    m = dofs_per_point(kid)
     tree = build_tree(X, leaf)
     lists = interaction_lists(tree)
-    Xt = np.asarray(X, dtype=np.float64)[tree.perm]
+    tree = expand_dofs(tree, m)
+    Xd = np.asarray(X, dtype=np.float64) if m == 1 else dof_points(X, m)
+    Xt = Xd[tree.perm]
     n_proxy = n_proxy or default_n_proxy(tree.d)
     h = H2(tree, lists, Xt, kid, ell, shift, tol, n_proxy, active_nodes(tree, lists))
     for k in range(1, tree.L):
@@ -157,6 +162,8 @@ def h2_build(X, kid, ell, shift, leaf, tol, n_proxy=0):
                 continue
             cand = h.candidates(i)
             Y = proxy_points(tree, i, n_proxy)
+            if m > 1:
+                Y = dof_points(Y, m)                        # proxy dofs (R28)
             M = kernel_matrix(kid, ell, Xt[cand], Y)       # n_c x n_p, no shift
             _, R, piv, s = qrcp(M.T, min(M.shape), tol, want_q=False)
             T = solve_triangular(R[:s, :s], R[:s, s:]) if s > 0 else np.zeros((0, len(cand) - s))

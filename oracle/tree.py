@@ -102,6 +102,16 @@ def build_tree(X, leaf):
     return Tree(N, d, L, perm, begin, end, lo, hi)
 
 
+def expand_dofs(tree: Tree, m: int) -> Tree:
+    """Tree over m degrees of freedom per point (RPY, m = 3; reading R28): the point
+    tree's nodes, boxes and levels, each tree position p becoming dofs m p .. m p + m-1,
+    so dof tree position m p + c holds component c of point perm[p]."""
+    if m == 1:
+        return tree
+    perm = (m * tree.perm[:, None] + np.arange(m)[None, :]).reshape(-1)
+    return Tree(m * tree.N, tree.d, tree.L, perm, m * tree.begin, m * tree.end, tree.lo, tree.hi)
+
+
 def far(tree: Tree, i, j):
     """Admissibility test R2 (symmetric by construction)."""
     if i == j:
