@@ -48,7 +48,12 @@ typedef enum {
     SPD_K_GAUSSIAN = 0,     /* exp(-r^2 / l^2)                       */
     SPD_K_MATERN32 = 1,     /* (1 + sqrt3 r / l) exp(-sqrt3 r / l)   */
     SPD_K_EXPONENTIAL = 2,  /* exp(-r / l)                           */
-    SPD_K_IMQ = 3           /* 1 / sqrt(r^2 + l^2)                   */
+    SPD_K_IMQ = 3,          /* 1 / sqrt(r^2 + l^2)                   */
+    SPD_K_RPY = 4           /* Rotne-Prager-Yamakawa 3x3 tensor, l = particle radius a
+                               (reading R28); points in 3D only.  The
+                               operator is over 3n DEGREES OF FREEDOM: dof 3p + c is
+                               component c of point p, so every vector / matrix
+                               argument of the H2 / HSS / PCG calls has 3n rows  */
 } spd_kernel_id;
 
 typedef struct { int id; double l; double shift; } spd_kernel;

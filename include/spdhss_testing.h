@@ -22,7 +22,8 @@ spd_status spd_test_qrcp(int batch, double* A, int m, int n, int ld, int64_t str
 /* unpivoted blocked Householder QR (R only) of `batch` matrices A_b = A + b*stride (m x n, ld);
  * on exit the upper triangle of each A_b[:n, :n] holds R with diag(R) >= 0 */
 spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int64_t stride, void* stream);
-/* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major */
+/* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major
+ * (d = spatial dimension; for RPY the points, not their 3 dofs each) */
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
 /* subtree-sharding plan (host logic only, no GPU): owner rank of node a of a level
  * with `count` nodes for nranks ranks, -1 when the level is computed redundantly */

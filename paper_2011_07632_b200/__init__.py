@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspdhss.so")
 
 SPD_OK, SPD_EINVAL, SPD_ENOTPD, SPD_ENOMEM, SPD_ECUDA, SPD_ENCCL, SPD_ENOCONV = range(7)
-GAUSSIAN, MATERN32, EXPONENTIAL, IMQ = range(4)
+GAUSSIAN, MATERN32, EXPONENTIAL, IMQ, K_RPY = range(5)
+RPY = K_RPY
 LAYOUT_ORIGINAL, LAYOUT_TREE = 0, 1
 Q_N, Q_LEVELS, Q_PERM, Q_NODES, Q_BOXES, Q_NNODES, Q_H2_RANKS, Q_SKELETONS = 1, 2, 3, 4, 5, 6, 7, 8
 Q_LIST_COUNTS, Q_NEAR, Q_TYPE3, Q_TYPE1 = 9, 10, 11, 12
@@ -318,7 +319,7 @@ def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0, comm=None):
     _check(lib().h2_build(_dptr(points, "points"), n, d, _Kernel(int(kernel_id), float(ell), float(shift)),
                           int(leaf), float(tol), ctypes.byref(opts), comm.ptr if comm is not None else None,
                           _stream(), ctypes.byref(out)))
-    h = H2(out, n, d)
+    h = H2(out, n * (3 if int(kernel_id) == K_RPY else 1), d)      # operator rows (RPY: 3 dofs per point)
     h._comm = comm            # keep the communicator alive as long as the handle
     return h
 

@@ -64,12 +64,17 @@ spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf,
         SPD_REQUIRE(d == 2 || d == 3, "h2_build: d must be 2 or 3");
         SPD_REQUIRE(leaf >= 1, "h2_build: leaf >= 1");
         SPD_REQUIRE(tol >= 0.0 && tol < 1.0, "h2_build: tol in [0, 1)");
-        SPD_REQUIRE(k.id >= 0 && k.id <= 3, "h2_build: unknown kernel id");
+        SPD_REQUIRE(k.id >= 0 && k.id <= 4, "h2_build: unknown kernel id");
+        SPD_REQUIRE(k.id != SPD_K_RPY || d == 3, "h2_build: the RPY kernel needs 3D points");
         SPD_REQUIRE(k.l > 0.0 && std::isfinite(k.l), "h2_build: kernel length l must be > 0");
         SPD_REQUIRE(k.shift >= 0.0 && std::isfinite(k.shift), "h2_build: shift must be >= 0");
         SPD_REQUIRE(n <= (int64_t)1 << 30, "h2_build: n too large");
         auto* h = new spd_h2_s();
-        h->N = n; h->d = d; h->kern = k; h->kp = make_kernel(k); h->tol = tol; h->leaf = leaf;
+        h->m = k.id == SPD_K_RPY ? 3 : 1;
+        h->dim = d;
+        h->N = n * h->m;                              // rows of the operator (dofs)
+        h->d = d + (h->m > 1 ? 1 : 0);               // coordinate rows of X (RPY: + component)
+        h->kern = k; h->kp = make_kernel(k); h->tol = tol; h->leaf = leaf;
         h->n_proxy = (opts && opts->n_proxy > 0) ? opts->n_proxy : (d == 2 ? 4096 : 6144);
         h->comm = c;
         try { h2_build_impl(h, pts, (cudaStream_t)stream); }
@@ -386,11 +391,12 @@ spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) 
         AllocStreamScope alloc_scope_((cudaStream_t)stream);
         SPD_REQUIRE(h != nullptr && P_host != nullptr, "spd_test_proxies: null argument");
         cudaStream_t s = (cudaStream_t)stream;
-        DBuf<double> P((size_t)h->n_proxy * h->d);
+        const int64_t np = (int64_t)h->m * h->n_proxy;     // proxy dofs (RPY: 3 per proxy point)
+        DBuf<double> P((size_t)np * h->d);
         proxies_for_node(h, node, P.p, s);
         std::vector<double> v = P.download(s);
-        for (int p = 0; p < h->n_proxy; ++p)
-            for (int a = 0; a < h->d; ++a) P_host[(size_t)p * h->d + a] = v[(size_t)a * h->n_proxy + p];
+        for (int p = 0; p < h->n_proxy; ++p)                // the proxy points (first dof of each)
+            for (int a = 0; a < h->dim; ++a) P_host[(size_t)p * h->dim + a] = v[(size_t)a * np + (size_t)h->m * p];
     })
 }
 

@@ -124,6 +124,34 @@ __device__ __forceinline__ double kernel_r2(const KernelParams& kp, double r2) {
     }
 }
 
+// RPY tensor entry (reading R28: 1/a on both near-branch
+// terms) for r = x - y = (d0, d1, d2) and components ca, cb of the two dofs
+__device__ __forceinline__ double rpy_entry(const KernelParams& kp, double d0, double d1, double d2, int ca,
+                                            int cb) {
+    const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
+    const double dl = ca == cb ? 1.0 : 0.0;
+    if (r2 == 0.0) return dl * kp.inv_l;
+    const double ra = ca == 0 ? d0 : (ca == 1 ? d1 : d2);
+    const double rb = cb == 0 ? d0 : (cb == 1 ? d1 : d2);
+    const double inv_r = 1.0 / sqrt(r2), r = r2 * inv_r;
+    const double rr = ra * rb * (inv_r * inv_r);
+    if (r >= 2.0 * kp.l)
+        return 0.75 * inv_r * (dl + rr) + 1.5 * kp.l2 * (inv_r * inv_r * inv_r) * (dl * (1.0 / 3.0) - rr);
+    const double t = r * kp.inv_l;
+    return kp.inv_l * ((1.0 - 0.28125 * t) * dl + 0.09375 * t * rr);
+}
+
+// one kernel entry between point / dof rows x and y (coordinate a at x[a * xs]); d
+// coordinates, for RPY (x, y, z, component)
+__device__ __forceinline__ double kernel_entry(const KernelParams& kp, const double* x, int64_t xs, const double* y,
+                                               int64_t ys, int d) {
+    if (kp.id == SPD_K_RPY)
+        return rpy_entry(kp, x[0] - y[0], x[xs] - y[ys], x[2 * xs] - y[2 * ys], (int)x[3 * xs], (int)y[3 * ys]);
+    double r2 = 0.0;
+    for (int a = 0; a < d; ++a) { const double df = x[a * xs] - y[a * ys]; r2 += df * df; }
+    return kernel_r2(kp, r2);
+}
+
 // ---------------------------------------------------------------- DMMA m8n8k4 fp64
 // Fragment layout (PTX ISA mma.m8n8k4 .f64): lane = 4*g + q (g = lane>>2, q = lane&3)
 //   A (8x4, row):  a = A[g][q]      B (4x8, col): b = B[q][g]

@@ -19,7 +19,7 @@
 namespace spd {
 
 // ================================================================= proxies (R3)
-struct ProxyDesc { int node; double* P; };     // P: d x n_p SoA (stride n_p)
+struct ProxyDesc { int node; double* P; };     // P: d x (m n_p) SoA, dof layout (m > 1: + component row)
 
 __device__ double halton_dev(long long k, int base) {
     long long num = 0, den = 1;
@@ -28,7 +28,8 @@ __device__ double halton_dev(long long k, int base) {
 }
 
 __global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, const double* lo, const double* hi,
-                                                    int d, int n_proxy) {
+                                                    int d, int n_proxy, int m) {
+    const int64_t stride = (int64_t)m * n_proxy;  // proxy dofs: point k -> dofs m k .. m k + m-1 (R28)
     __shared__ double ilo[3], ihi[3], slo[3], shi[3], dlo[3], dhi[3];
     __shared__ int s_cnt[8];
     __shared__ long long s_klast;
@@ -83,7 +84,11 @@ __global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, cons
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { if (w < warp) pre += s_cnt[w]; tot += s_cnt[w]; }
             const int pos = got + pre + wpre;
             if (ok && pos < quota) {
-                for (int a = 0; a < d; ++a) pd.P[(size_t)a * n_proxy + pos0 + pos] = p[a];
+                for (int c = 0; c < m; ++c) {
+                    const int64_t dof = (int64_t)m * (pos0 + pos) + c;
+                    for (int a = 0; a < d; ++a) pd.P[(size_t)a * stride + dof] = p[a];
+                    if (m > 1) pd.P[(size_t)d * stride + dof] = (double)c;
+                }
                 if (record_last && pos == quota - 1) s_klast = k;
             }
             got += tot;
@@ -112,12 +117,7 @@ __global__ void proxy_matrix_kernel(const ProxyMatDesc* descs, KernelParams kp, 
     const int64_t total = (int64_t)n_proxy * md.nc;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int p = (int)(e % n_proxy), c = (int)(e / n_proxy);
-        double r2 = 0.0;
-        for (int a = 0; a < d; ++a) {
-            double df = md.P[(size_t)a * n_proxy + p] - md.cx[(size_t)a * md.cds + c];
-            r2 += df * df;
-        }
-        md.Mt[e] = kernel_r2(kp, r2);
+        md.Mt[e] = kernel_entry(kp, md.P + p, n_proxy, md.cx + c, md.cds, d);
     }
 }
 
@@ -170,9 +170,26 @@ void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const d
     SPD_LAUNCH();
 }
 
-__global__ void points_soa_kernel(const int64_t* perm, int64_t N, int d, const double* pts, double* X) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x)
-        for (int a = 0; a < d; ++a) X[(size_t)a * N + p] = pts[perm[p] * d + a];
+// X (d rows of N, tree order) from the points; m > 1: dof m p + c of point perm[p / m]
+// gets the point's coordinates and the component c in row dim (reading R28)
+__global__ void points_soa_kernel(const int64_t* perm, int64_t N, int dim, int m, const double* pts, double* X) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t dof = perm[p], pt = dof / m;
+        for (int a = 0; a < dim; ++a) X[(size_t)a * N + p] = pts[pt * dim + a];
+        if (m > 1) X[(size_t)dim * N + p] = (double)(dof % m);
+    }
+}
+
+// tree over m dofs per point: node ranges x m, dof m p + c <- point position p (R28)
+static void expand_dofs(TreeH& t, int m) {
+    if (m == 1) return;
+    std::vector<int64_t> perm((size_t)t.N * m);
+    for (int64_t p = 0; p < t.N; ++p)
+        for (int c = 0; c < m; ++c) perm[(size_t)p * m + c] = t.perm[p] * m + c;
+    t.perm.swap(perm);
+    for (auto& b : t.begin) b *= m;
+    for (auto& e : t.end) e *= m;
+    t.N *= m;
 }
 
 // ================================================================= build
@@ -181,16 +198,18 @@ static double now_s() {
 }
 
 void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
-    const int64_t N = h->N;
-    const int d = h->d;
+    const int64_t N = h->N;                      // dofs
+    const int64_t npts = N / h->m;
+    const int d = h->d, dim = h->dim, m = h->m;
     double t0 = now_s();
-    // --- tree + lists (host metadata; R1, R2)
-    std::vector<double> pts((size_t)N * d);
-    SPD_CUDA(cudaMemcpyAsync(pts.data(), pts_dev, sizeof(double) * N * d, cudaMemcpyDeviceToHost, s));
+    // --- tree + lists (host metadata; R1, R2) on the points, then over dofs (R28)
+    std::vector<double> pts((size_t)npts * dim);
+    SPD_CUDA(cudaMemcpyAsync(pts.data(), pts_dev, sizeof(double) * npts * dim, cudaMemcpyDeviceToHost, s));
     SPD_CUDA(cudaStreamSynchronize(s));
     for (double v : pts) SPD_REQUIRE(std::isfinite(v), "h2_build: non-finite point coordinate");
-    build_tree(pts.data(), N, d, h->leaf, h->tree);
+    build_tree(pts.data(), npts, dim, h->leaf, h->tree);
     build_lists(h->tree, h->lists);
+    expand_dofs(h->tree, m);
     const TreeH& t = h->tree;
     const int L = t.L;
     // active nodes: Type-3 partner at own or ancestor level
@@ -205,10 +224,10 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
     stage_mark(s, nullptr);
     // --- device points (tree order, SoA)
     h->perm.upload(t.perm, s);
-    DBuf<double> pts_d((size_t)N * d);
-    SPD_CUDA(cudaMemcpyAsync(pts_d.p, pts_dev, sizeof(double) * N * d, cudaMemcpyDeviceToDevice, s));
+    DBuf<double> pts_d((size_t)npts * dim);
+    SPD_CUDA(cudaMemcpyAsync(pts_d.p, pts_dev, sizeof(double) * npts * dim, cudaMemcpyDeviceToDevice, s));
     h->X.alloc((size_t)N * d);
-    points_soa_kernel<<<148 * 4, 256, 0, s>>>(h->perm.p, N, d, pts_d.p, h->X.p);
+    points_soa_kernel<<<148 * 4, 256, 0, s>>>(h->perm.p, N, dim, m, pts_d.p, h->X.p);
     SPD_LAUNCH();
     DBuf<double> lo_d, hi_d;
     lo_d.upload(t.lo, s);
@@ -216,7 +235,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
 
     h->lv.clear();
     h->lv.resize(L);
-    const int n_p = h->n_proxy;
+    const int n_p = m * h->n_proxy;              // proxy dofs per node (rows of the proxy matrix)
     const size_t budget = (size_t)6 << 30;       // bytes of proxy matrices in flight
     for (int k = 1; k < L; ++k) {
         H2Level& lv = h->lv[k];
@@ -310,7 +329,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             {
                 DevArray<ProxyDesc> dp(s, pdesc);
                 ProfScope prof(s, "proxy_points", 0, 0);
-                proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, d, n_p);
+                proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, dim, h->n_proxy, m);
                 SPD_LAUNCH();
                 DevArray<ProxyMatDesc> dm(s, mdesc);
                 double by = 0;
@@ -454,7 +473,7 @@ void proxies_for_node(spd_h2_s* h, int node, double* P_dev, cudaStream_t s) {
     hi_d.upload(h->tree.hi, s);
     std::vector<ProxyDesc> pd{{node, P_dev}};
     DevArray<ProxyDesc> dp(s, pd);
-    proxy_kernel<<<1, 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, h->d, h->n_proxy);
+    proxy_kernel<<<1, 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, h->dim, h->n_proxy, h->m);
     SPD_LAUNCH();
     SPD_CUDA(cudaStreamSynchronize(s));
 }

@@ -68,6 +68,8 @@ struct spd_h2_s {
     spd::DBuf<double> X;          // d x N tree-order points (SoA)
     spd::DBuf<int64_t> perm;      // tree position -> original index
     std::vector<spd::H2Level> lv; // [0..L-1], level k at lv[k] (lv[0] unused)
+    int m = 1, dim = 3;              // dofs per point (RPY: 3), spatial dimension; N = m * points,
+                                     // d = coordinate rows of X (RPY: dim + 1, the component)
     double timings[16] = {0};
     int64_t shard_work[2] = {0, 0};  // nodes ID'd by this process / nodes with an ID (sharding evidence)
     // matvec workspace

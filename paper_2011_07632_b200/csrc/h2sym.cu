@@ -30,18 +30,24 @@ __global__ void __launch_bounds__(256) sym_build_kernel(KernelParams kp, double 
                                                         const SymBuild* __restrict__ bp, double* __restrict__ vals) {
     const SymBuild b = bp[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double rx[3] = {0.0, 0.0, 0.0};
+    double rx[4] = {0.0, 0.0, 0.0, 0.0};
     if (lane < b.nr)
         for (int a = 0; a < d; ++a) rx[a] = b.tx[(size_t)a * b.tds + lane];
     const bool sh = shift != 0.0 && b.tid0 >= 0;
     double* out = vals + b.vbase + lane;
     for (int c = warp; c < b.nb; c += 8) {
-        double r2 = 0.0;
-        for (int a = 0; a < d; ++a) {
-            const double df = rx[a] - b.sx[(size_t)a * b.sds + c];
-            r2 += df * df;
+        double kv;
+        if constexpr (KID == SPD_K_RPY) {
+            kv = rpy_entry(kp, rx[0] - b.sx[c], rx[1] - b.sx[b.sds + c], rx[2] - b.sx[2 * (size_t)b.sds + c],
+                           (int)rx[3], (int)b.sx[3 * (size_t)b.sds + c]);
+        } else {
+            double r2 = 0.0;
+            for (int a = 0; a < d; ++a) {
+                const double df = rx[a] - b.sx[(size_t)a * b.sds + c];
+                r2 += df * df;
+            }
+            kv = kval_sym<KID>(kp, r2);
         }
-        double kv = kval_sym<KID>(kp, r2);
         if (sh && b.tid0 + lane == b.sid0 + c) kv += shift;
         out[(size_t)c * 32] = lane < b.nr ? kv : 0.0;
     }
@@ -231,6 +237,7 @@ void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
             case SPD_K_GAUSSIAN: sym_build_kernel<SPD_K_GAUSSIAN><<<nb, 256, 0, s>>>(kp, sh, h->d, db.p + off, st.vals.p); break;
             case SPD_K_MATERN32: sym_build_kernel<SPD_K_MATERN32><<<nb, 256, 0, s>>>(kp, sh, h->d, db.p + off, st.vals.p); break;
             case SPD_K_EXPONENTIAL: sym_build_kernel<SPD_K_EXPONENTIAL><<<nb, 256, 0, s>>>(kp, sh, h->d, db.p + off, st.vals.p); break;
+            case SPD_K_RPY: sym_build_kernel<SPD_K_RPY><<<nb, 256, 0, s>>>(kp, sh, h->d, db.p + off, st.vals.p); break;
             default: sym_build_kernel<SPD_K_IMQ><<<nb, 256, 0, s>>>(kp, sh, h->d, db.p + off, st.vals.p); break;
             }
             SPD_LAUNCH();
@@ -276,6 +283,7 @@ void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<doub
         case SPD_K_GAUSSIAN: launch_sym<SPD_K_GAUSSIAN>(s, nb, smem, st, xin, kp, sh, h->d); break;
         case SPD_K_MATERN32: launch_sym<SPD_K_MATERN32>(s, nb, smem, st, xin, kp, sh, h->d); break;
         case SPD_K_EXPONENTIAL: launch_sym<SPD_K_EXPONENTIAL>(s, nb, smem, st, xin, kp, sh, h->d); break;
+        case SPD_K_RPY: launch_sym<SPD_K_RPY>(s, nb, smem, st, xin, kp, sh, h->d); break;
         default: launch_sym<SPD_K_IMQ>(s, nb, smem, st, xin, kp, sh, h->d); break;
         }
     }

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
     constexpr int EPT = KB_M * KB_K / NT;       // kernel evaluations per thread per chunk
     __shared__ double Ks[KB_K][KB_M + 8];            // row stride = 8 (mod 16) doubles: fragment reads in 2 wavefronts
     __shared__ double Xs[NC][KB_K + 4];              // kc contiguous: conflict-free writes and reads
-    __shared__ double Sx[3][KB_K];
+    __shared__ double Sx[4][KB_K];                   // coordinates (RPY: + component row)
     const KbWork wk = work[blockIdx.x];
     const KbTarget tg = targets[wk.target];
     const KbBlock tb = blocks[tg.blk];
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
     const int r0 = wk.tm * KB_M, c0 = wk.tn * NC;
     const int nrows = min(KB_M, tb.n - r0);
     const int er = tid & (KB_M - 1), ec0 = (tid / KB_M) * EPT;
-    double rx[3] = {0.0, 0.0, 0.0};
+    double rx[4] = {0.0, 0.0, 0.0, 0.0};
     if (er < nrows)
         for (int a = 0; a < d; ++a) rx[a] = tb.x[(size_t)a * tb.ds + r0 + er];
     const int64_t rid = tb.id0 >= 0 ? tb.id0 + r0 + er : -1;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
                     const int kk = idx % KB_K, j = idx / KB_K;
                     xr[u] = (kk < nk && j < ncols) ? __ldg(en.X + k0 + kk + (size_t)(c0 + j) * en.ldx) : 0.0;
                 }
-                if (tid < KB_K * 3) {
+                if (tid < KB_K * 4) {
                     const int a = tid / KB_K, c = tid % KB_K;
                     sr = (a < d && c < nk) ? __ldg(sb.x + (size_t)a * sb.ds + k0 + c) : 0.0;
                 }
@@ -96,14 +96,16 @@ __global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
                     const int idx = tid + u * NT;
                     Xs[idx / KB_K][idx % KB_K] = xr[u];
                 }
-                if (tid < KB_K * 3) Sx[tid / KB_K][tid % KB_K] = sr;
+                if (tid < KB_K * 4) Sx[tid / KB_K][tid % KB_K] = sr;
                 __syncthreads();
                 if (k0 + KB_K < sb.n) load(k0 + KB_K);          // prefetch the next chunk
 #pragma unroll
                 for (int c = 0; c < EPT; ++c) {
                     const int kc = ec0 + c;
                     const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
-                    double kv = kval<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
+                    double kv;
+                    if constexpr (KID == SPD_K_RPY) kv = rpy_entry(kp, d0, d1, d2, (int)rx[3], (int)Sx[3][kc]);
+                    else kv = kval<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
                     if (use_shift && rid == sb.id0 + k0 + kc) kv += shift;
                     Ks[kc][er] = (er < nrows && kc < nk) ? kv : 0.0;
                 }
@@ -189,10 +191,12 @@ __global__ void __launch_bounds__(256) kblock_vec_kernel(
     const int row = r0 + lane;
     const bool valid = row < tb.n;
     double rx0 = 0.0, rx1 = 0.0, rx2 = 0.0;
+    int rc = 0;                                  // RPY: component of the row dof
     if (valid) {
         rx0 = tb.x[row];
         if (d > 1) rx1 = tb.x[tb.ds + row];
         if (d > 2) rx2 = tb.x[2 * tb.ds + row];
+        if (KID == SPD_K_RPY) rc = (int)tb.x[3 * tb.ds + row];
     }
     const int64_t rid = tb.id0 >= 0 ? tb.id0 + row : -1;
     int g0 = tg.e_begin;
@@ -210,10 +214,12 @@ __global__ void __launch_bounds__(256) kblock_vec_kernel(
             for (int c0 = 0; c0 < sb.n; c0 += 32) {
                 const int c = c0 + lane;
                 double sx0 = 0.0, sx1 = 0.0, sx2 = 0.0, xv[NV];
+                int sc = 0;
                 if (c < sb.n) {
                     sx0 = sb.x[c];
                     if (d > 1) sx1 = sb.x[sb.ds + c];
                     if (d > 2) sx2 = sb.x[2 * sb.ds + c];
+                    if (KID == SPD_K_RPY) sc = (int)sb.x[3 * sb.ds + c];
                 }
 #pragma unroll
                 for (int v = 0; v < NV; ++v) xv[v] = (c < sb.n && v < nc) ? en.X[c + (size_t)v * en.ldx] : 0.0;
@@ -223,8 +229,10 @@ __global__ void __launch_bounds__(256) kblock_vec_kernel(
                     const double y1 = __shfl_sync(0xffffffffu, sx1, q);
                     const double y2 = __shfl_sync(0xffffffffu, sx2, q);
                     const double df0 = rx0 - y0, df1 = rx1 - y1, df2 = rx2 - y2;
-                    const double r2 = df0 * df0 + df1 * df1 + df2 * df2;
-                    double kv = kval<KID>(kp, r2);
+                    double kv;
+                    if constexpr (KID == SPD_K_RPY)
+                        kv = rpy_entry(kp, df0, df1, df2, rc, __shfl_sync(0xffffffffu, sc, q));
+                    else kv = kval<KID>(kp, df0 * df0 + df1 * df1 + df2 * df2);
                     if (sh && rid == sb.id0 + c0 + q) kv += shift;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) acc[v] += kv * __shfl_sync(0xffffffffu, xv[v], q);
@@ -284,6 +292,7 @@ static void kblock_vec(cudaStream_t s, const KernelParams& kp, double shift, int
     case SPD_K_GAUSSIAN: launch_vec<SPD_K_GAUSSIAN>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
     case SPD_K_MATERN32: launch_vec<SPD_K_MATERN32>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
     case SPD_K_EXPONENTIAL: launch_vec<SPD_K_EXPONENTIAL>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
+    case SPD_K_RPY: launch_vec<SPD_K_RPY>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
     default: launch_vec<SPD_K_IMQ>(s, nb, nv, kp, shift, d, db.p, dt.p, de.p, dw.p); break;
     }
     SPD_LAUNCH();
@@ -382,6 +391,7 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
     case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
     case SPD_K_EXPONENTIAL: SPD_KB_LAUNCH(SPD_K_EXPONENTIAL); break;
+    case SPD_K_RPY: SPD_KB_LAUNCH(SPD_K_RPY); break;
     default: SPD_KB_LAUNCH(SPD_K_IMQ); break;
     }
 #undef SPD_KB_LAUNCH

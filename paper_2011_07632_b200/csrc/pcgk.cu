@@ -208,6 +208,7 @@ static void* kernel_ptr(int kid, bool eval) {
     case SPD_K_GAUSSIAN: return eval ? (void*)pcg_persistent_kernel<SPD_K_GAUSSIAN, true> : (void*)pcg_persistent_kernel<SPD_K_GAUSSIAN, false>;
     case SPD_K_MATERN32: return eval ? (void*)pcg_persistent_kernel<SPD_K_MATERN32, true> : (void*)pcg_persistent_kernel<SPD_K_MATERN32, false>;
     case SPD_K_EXPONENTIAL: return eval ? (void*)pcg_persistent_kernel<SPD_K_EXPONENTIAL, true> : (void*)pcg_persistent_kernel<SPD_K_EXPONENTIAL, false>;
+    case SPD_K_RPY: return eval ? (void*)pcg_persistent_kernel<SPD_K_RPY, true> : (void*)pcg_persistent_kernel<SPD_K_RPY, false>;
     default: return eval ? (void*)pcg_persistent_kernel<SPD_K_IMQ, true> : (void*)pcg_persistent_kernel<SPD_K_IMQ, false>;
     }
 }

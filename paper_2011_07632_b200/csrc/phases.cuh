@@ -164,10 +164,12 @@ __device__ __forceinline__ void sym_piece(const SymPiece& pc, const SymVecs& xin
         const bool stored = !EVAL || pc.vbase >= 0;      // !EVAL: every piece is stored
         const double* v = vals + (stored ? pc.vbase + (int64_t)warp * 32 * nb : 0) + lane;
         double rx0 = 0.0, rx1 = 0.0, rx2 = 0.0;     // on the fly: this lane's row point
+        int rc = 0;                                 // RPY: component of the row dof
         if (!stored && lane < nr) {
             rx0 = pc.tx[r0 + lane];
             if (d > 1) rx1 = pc.tx[pc.tds + r0 + lane];
             if (d > 2) rx2 = pc.tx[2 * pc.tds + r0 + lane];
+            if (KID == SPD_K_RPY) rc = (int)pc.tx[3 * pc.tds + r0 + lane];
         }
         const bool sh = !stored && shift != 0.0 && pc.tid0 >= 0;
         double acc = 0.0;
@@ -187,17 +189,21 @@ __device__ __forceinline__ void sym_piece(const SymPiece& pc, const SymVecs& xin
                 }
             } else if (EVAL) {
                 double s0 = 0.0, s1 = 0.0, s2 = 0.0;  // source point c0 + lane, broadcast by shuffles
+                int sc = 0;
                 if (lane < cn) {
                     s0 = pc.sx[c0 + lane];
                     if (d > 1) s1 = pc.sx[pc.sds + c0 + lane];
                     if (d > 2) s2 = pc.sx[2 * pc.sds + c0 + lane];
+                    if (KID == SPD_K_RPY) sc = (int)pc.sx[3 * pc.sds + c0 + lane];
                 }
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
                     const double d0 = rx0 - __shfl_sync(0xffffffffu, s0, c);
                     const double d1 = rx1 - __shfl_sync(0xffffffffu, s1, c);
                     const double d2 = rx2 - __shfl_sync(0xffffffffu, s2, c);
-                    double k = kval_sym<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
+                    double k;
+                    if constexpr (KID == SPD_K_RPY) k = rpy_entry(kp, d0, d1, d2, rc, __shfl_sync(0xffffffffu, sc, c));
+                    else k = kval_sym<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
                     if (sh && pc.tid0 + r0 + lane == pc.sid0 + c0 + c) k += shift;
                     kv[c] = (c < cn && lane < nr) ? k : 0.0;
                 }

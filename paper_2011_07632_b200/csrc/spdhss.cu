@@ -63,9 +63,7 @@ __global__ void dense_kernel_blocks(const DenseKDesc* descs, KernelParams kp, do
     const int64_t total = (int64_t)dk.n * dk.n;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int i = (int)(e % dk.n), j = (int)(e / dk.n);
-        double r2 = 0.0;
-        for (int a = 0; a < d; ++a) { double df = dk.x[a * dk.ds + i] - dk.x[a * dk.ds + j]; r2 += df * df; }
-        double v = kernel_r2(kp, r2);
+        double v = kernel_entry(kp, dk.x + i, dk.ds, dk.x + j, dk.ds, d);
         if (i == j) v += shift;
         dk.A[i + (size_t)j * dk.ld] = v;
     }

@@ -15,6 +15,9 @@ CASES = {
     "C3s": synth.C3.scaled(2048, leaf=64),
     "C4s": synth.C4.scaled(4096, leaf=128),
     "ragged": synth.C1.scaled(1000, leaf=50),
+    # RPY tensor kernel over 3 dofs per point (§8(f) f1, R28); loose tols so IDs truncate
+    "R1s": synth.R1.scaled(800, leaf=64, h2_tol=1e-4),
+    "R2s": synth.R2.scaled(1200, leaf=64, h2_tol=1e-6),
 }
 
 
@@ -88,7 +91,7 @@ def test_skeletons(spd, name):
 @pytest.mark.parametrize("k", [1, 7, 64])
 def test_h2_matvec_vs_oracle(spd, name, k):
     cfg, X, h, ho = built(spd, name)
-    x = synth.multivec(cfg.n, k)
+    x = synth.multivec(cfg.dofs, k)
     y = host(spd.h2_matvec(h, cuda(x)))
     yo = np.empty_like(x)
     yo[ho.tree.perm] = oracle.h2_matvec(ho, x[ho.tree.perm])

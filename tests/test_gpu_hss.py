@@ -20,6 +20,8 @@ CASES = {
     "ragged": synth.C1.scaled(1000, leaf=50, rank_cap=16),
     "L2": synth.C1.scaled(128, leaf=64, rank_cap=20),
     "L1": synth.C1.scaled(60, leaf=64, rank_cap=20),
+    "R1s": synth.R1.scaled(800, leaf=64, h2_tol=1e-4, rank_cap=30),
+    "R2s": synth.R2.scaled(1200, leaf=64, h2_tol=1e-6, rank_cap=40),
 }
 
 
@@ -83,7 +85,7 @@ def test_hss_ranks_and_apply_match_oracle(spd, name):
     for i, r in Ho.rank.items():
         assert abs(int(rg[i]) - r) <= 1, f"node {i}: rank {rg[i]} vs {r}"
     G = gpu_as_oracle_hss(H, ho)
-    x = synth.multivec(cfg.n, 10, seed=11)
+    x = synth.multivec(cfg.dofs, 10, seed=11)
     yg = oracle.hss_matvec(G, x)
     yo = oracle.hss_matvec(Ho, x)
     assert rel(yg, yo) <= 1e-9
@@ -92,7 +94,7 @@ def test_hss_ranks_and_apply_match_oracle(spd, name):
 @pytest.mark.parametrize("name", list(CASES))
 def test_hss_solve_matches_oracle(spd, name):
     cfg, X, h, ho, H, Ho, om = built(spd, name)
-    b = synth.multivec(cfg.n, 3, seed=12)
+    b = synth.multivec(cfg.dofs, 3, seed=12)
     xg = host(spd.hss_solve(H, cuda(b)))
     xo = np.empty_like(b)
     xo[ho.tree.perm] = oracle.hss_solve(Ho, b[ho.tree.perm])
@@ -111,7 +113,7 @@ def test_gpu_hss_is_spd(spd):
     assert np.linalg.eigvalsh(0.5 * (D + D.T)).min() > 0
 
 
-@pytest.mark.parametrize("name", ["C1s", "C1", "C2s", "C4s"])
+@pytest.mark.parametrize("name", ["C1s", "C1", "C2s", "C4s", "R1s", "R2s"])
 def test_pcg_iterations_match_oracle(spd, name):
     cfg, X, h, ho, H, Ho, om = built(spd, name)
     b = synth.rhs(cfg)
