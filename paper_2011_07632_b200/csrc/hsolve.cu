@@ -23,6 +23,12 @@ __global__ void __launch_bounds__(PH_T) hss_item_kernel(const HsNode* __restrict
     hss_item(nodes, items[blockIdx.x], sm);
 }
 
+__global__ void __launch_bounds__(256, 2) hss_item_warp_kernel(const HsNode* __restrict__ nodes,
+                                                            const HsItem* __restrict__ items, int n) {
+    const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (w < n) hss_item_warp(nodes, items[w]);
+}
+
 static void launch_phase(cudaStream_t s, const HsPhase& ph) {
     if (ph.items.empty()) return;
     int mmax = 1, rmax = 1;
@@ -40,7 +46,18 @@ static void launch_phase(cudaStream_t s, const HsPhase& ph) {
     DevArray<HsNode> dn(s, ph.nodes);
     DevArray<HsItem> di(s, ph.items);
     ProfScope prof(s, "hss_solve_vec", 0, by);
-    hss_item_kernel<<<(unsigned)ph.items.size(), PH_T, smem, s>>>(dn.p, di.p);
+    static int nsm = 0;
+    if (!nsm) {
+        int dv = 0;
+        SPD_CUDA(cudaGetDevice(&dv));
+        SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dv));
+    }
+    if (!hss_phase_uses_warps(ph.mode, ph.items.size(), nsm) || getenv("SPD_HSS_CTA")) {
+        hss_item_kernel<<<(unsigned)ph.items.size(), PH_T, smem, s>>>(dn.p, di.p);
+    } else {
+        const int n = (int)ph.items.size();
+        hss_item_warp_kernel<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(dn.p, di.p, n);
+    }
     SPD_LAUNCH();
 }
 

@@ -44,6 +44,7 @@ struct PcgPlan {
     // HSS solve z = M r
     int nhs;
     const HsNode* hs; const HsItem* hsi; int hs_off[PK_MAXPH + 1];
+    unsigned char hs_cta[PK_MAXPH];   // 1: phase of CTA items (dense top operator), 0: warp items
     unsigned long long* trace;     // optional: globaltimer after every phase of iteration 2 (CTA 0)
 };
 
@@ -154,7 +155,13 @@ __global__ void __launch_bounds__(PH_T, EVAL ? 1 : 2) pcg_persistent_kernel(PcgP
         if (sqrt(rr) / P.nb <= P.tol) { conv = 1; break; }
         // ---------------- z = M r (HSS solve, k = 1)
         for (int l = 0; l < P.nhs; ++l) {
-            for (int w = P.hs_off[l] + blockIdx.x; w < P.hs_off[l + 1]; w += gridDim.x) hss_item(P.hs, P.hsi[w], sm);
+            if (P.hs_cta[l]) {
+                for (int w = P.hs_off[l] + blockIdx.x; w < P.hs_off[l + 1]; w += gridDim.x) hss_item(P.hs, P.hsi[w], sm);
+            } else {
+                for (int w = P.hs_off[l] + blockIdx.x * PH_W + (threadIdx.x >> 5); w < P.hs_off[l + 1];
+                     w += gridDim.x * PH_W)
+                    hss_item_warp(P.hs, P.hsi[w]);
+            }
             sync(it);
         }
         // ---------------- beta = r^T z / rz ; p = z + beta p
@@ -259,6 +266,12 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     }
     std::vector<HsNode> hsf;
     std::vector<HsItem> hsi;
+    int nsm_dev = 148;
+    {
+        int dv = 0;
+        SPD_CUDA(cudaGetDevice(&dv));
+        SPD_CUDA(cudaDeviceGetAttribute(&nsm_dev, cudaDevAttrMultiProcessorCount, dv));
+    }
     P.nhs = 0;
     P.hs_off[0] = 0;
     int mmax = 1, rmax = 1;
@@ -272,6 +285,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
         }
         hsf.insert(hsf.end(), ph.nodes.begin(), ph.nodes.end());
         for (auto itm : ph.items) { itm.node += base; hsi.push_back(itm); }
+        P.hs_cta[P.nhs] = (!hss_phase_uses_warps(ph.mode, ph.items.size(), nsm_dev) || getenv("SPD_HSS_CTA")) ? 1 : 0;
         P.hs_off[++P.nhs] = (int)hsi.size();
     }
     const BasisItem* up_rel = put(buf, upf, fix);

@@ -364,7 +364,12 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
 #pragma unroll
             for (int t = 0; t < HS_MT; ++t) {
                 const int i = t * 32 + lane;
-                v[t] = i < m ? __ldg(p + i) * w[i] : 0.0;
+                v[t] = i < m ? __ldg(p + i) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < HS_MT; ++t) {            // multiplies after all loads (in-order issue)
+                const int i = t * 32 + lane;
+                v[t] *= i < m ? w[i] : 0.0;
             }
             double sum = 0.0;
 #pragma unroll
@@ -383,7 +388,12 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
 #pragma unroll
                 for (int t = 0; t < HS_MT; ++t) {
                     const int k = t * 32 + lane;
-                    v[t] = (k >= i && k < m) ? __ldg(p + k) * w[k] : 0.0;
+                    v[t] = (k >= i && k < m) ? __ldg(p + k) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < HS_MT; ++t) {
+                    const int k = t * 32 + lane;
+                    v[t] *= (k >= i && k < m) ? w[k] : 0.0;
                 }
 #pragma unroll
                 for (int t = 0; t < HS_MT; ++t) sum += v[t];
@@ -396,7 +406,15 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
         double acc = 0.0;
         if (nd.xh && i < m) {
             const int jb = (int)((int64_t)r * warp / PH_W), je = (int)((int64_t)r * (warp + 1) / PH_W);
-            for (int j = jb; j < je; ++j) acc += __ldg(nd.P + i + (size_t)j * m) * dv[j];
+            int j = jb;
+            for (; j + 8 <= je; j += 8) {               // 8 loads in flight, then the FMAs
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(nd.P + i + (size_t)(j + u) * m);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += v[u] * dv[j + u];
+            }
+            for (; j < je; ++j) acc += __ldg(nd.P + i + (size_t)j * m) * dv[j];
         }
         red[32 + warp * 32 + lane] = acc;
         __syncthreads();
@@ -410,6 +428,91 @@ __device__ __forceinline__ void hss_item(const HsNode* __restrict__ nodes, const
     __syncthreads();
 }
 __host__ __device__ inline int hss_item_smem_doubles(int mmax, int rmax) { return mmax + rmax + (PH_W + 1) * 32; }
+
+// The same items (kinds 0, 1, 2) computed by ONE WARP each, with no shared memory and
+// no CTA barrier: the inputs come through L2 (ldv) in 32-element chunks broadcast by
+// shuffles, every chunk issues 32 independent loads per lane, and the warps of a CTA
+// work on different items -- a level's items all run at once instead of a few per CTA
+// in sequence (the CTA form is latency-bound on the per-item barriers and input fills).
+// Summation order is fixed per output (chunk order), so results are reproducible.
+// Warp items win when a level has many items (each warp walks its item's chunks in
+// sequence; measured on C2: leaf levels 2x faster), CTA items when it has few (the 8
+// warps split one item's chunks): warp form for >= 3.4 items per CTA slot (2 per SM).
+inline bool hss_phase_uses_warps(int mode, size_t nitems, int nsm) {
+    return mode != 3 && (double)nitems >= 3.4 * 2 * nsm;
+}
+__device__ __forceinline__ void hss_item_warp(const HsNode* __restrict__ nodes, const HsItem& it) {
+    const HsNode nd = nodes[it.node];
+    const int m = nd.m, r = nd.r;
+    const int lane = threadIdx.x & 31;
+    if (it.kind == 0) {                               // u0[i] = sum_{j <= i} F[i, j] w[j]
+        const int i = it.tile * 32 + lane;
+        double a0 = 0.0, a1 = 0.0;
+        for (int cc = 0; cc <= it.tile; ++cc) {
+            const int j0 = cc * 32;
+            const double wj = j0 + lane < m ? ldv(nd.in + j0 + lane) : 0.0;
+            const double* p = nd.F + i + (size_t)j0 * m;
+            double v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = (i < m && j0 + c <= i) ? __ldg(p + (size_t)c * m) : 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+                a0 += v[c] * __shfl_sync(0xffffffffu, wj, c);
+                a1 += v[c + 1] * __shfl_sync(0xffffffffu, wj, c + 1);
+            }
+        }
+        if (i < m) nd.u[i] = a0 + a1;
+    } else if (it.kind == 1) {                        // zh[c] = sum_k P[k, c] w[k], 32 columns
+        const int c0 = it.tile * 32, cn = min(32, r - c0);
+        double acc = 0.0;
+        for (int k0 = 0; k0 < m; k0 += 32) {
+            const int k = k0 + lane;
+            const double wk = k < m ? ldv(nd.in + k) : 0.0;
+            const double* p = nd.P + k + (size_t)c0 * m;
+            double v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = (k < m && c < cn) ? __ldg(p + (size_t)c * m) : 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] *= wk;      // after ALL loads: in-order issue
+            butterfly32(v);
+            acc += v[0];
+        }
+        if (lane < cn) { nd.zh[c0 + lane] = acc; nd.zh2[c0 + lane] = acc; }
+    } else {                                          // out[i] = (F^T u)[i] + (P (xh - zh))[i]
+        const int c0 = it.tile * 32, cn = min(32, m - c0);
+        double acc = 0.0;                             // lane c: sum_{k >= c0 + c} F[k, c0 + c] u[k]
+        for (int k0 = c0; k0 < m; k0 += 32) {
+            const int k = k0 + lane;
+            const double uk = k < m ? ldv(nd.in + k) : 0.0;
+            const double* p = nd.F + k + (size_t)c0 * m;
+            double v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = (k < m && c < cn && k >= c0 + c) ? __ldg(p + (size_t)c * m) : 0.0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] *= uk;
+            butterfly32(v);
+            acc += v[0];
+        }
+        const int i = c0 + lane;                      // lane = row i: + sum_j P[i, j] (xh - zh)[j]
+        if (nd.xh) {
+            double b0 = 0.0, b1 = 0.0;
+            for (int j0 = 0; j0 < r; j0 += 32) {
+                const double dj = j0 + lane < r ? ldv(nd.xh + j0 + lane) - ldv(nd.zhi + j0 + lane) : 0.0;
+                const double* p = nd.P + i + (size_t)j0 * m;
+                double v[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) v[c] = (i < m && j0 + c < r) ? __ldg(p + (size_t)c * m) : 0.0;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    b0 += v[c] * __shfl_sync(0xffffffffu, dj, c);
+                    b1 += v[c + 1] * __shfl_sync(0xffffffffu, dj, c + 1);
+                }
+            }
+            acc += b0 + b1;
+        }
+        if (i < m) nd.out[i] = acc;
+    }
+}
 
 // ================================================================= host-side plans (work items)
 std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const double* x, const std::vector<double*>& xh,
