@@ -238,6 +238,32 @@ __device__ __forceinline__ void sym_piece(const SymPiece& pc, const SymVecs& xin
 
 // one (output node, 32-row tile) by a whole CTA (long lists): warp w sums the w-th of
 // PH_W contiguous slices of the list, the slice sums are added in warp order.  red: PH_W*32.
+// sum of the partials con[cb, ce) over the 32 rows of a tile (lane = row) into a[4]
+// (entry c goes to a[(c - cb) & 3]: the order of the sums is fixed).  The descriptors
+// of 16 entries are fetched by 16 lanes at once and broadcast, then the 16 partial
+// loads are all in flight before the first add (one round trip per 16 entries).
+__device__ __forceinline__ void gather_range(const SymContrib* __restrict__ con, int cb, int ce,
+                                             const double* __restrict__ scratch, double (&a)[4]) {
+    const int lane = threadIdx.x & 31;
+    for (int c0 = cb; c0 < ce; c0 += 16) {
+        const int nc = min(16, ce - c0);
+        int64_t mo = 0;
+        int ml = 0;
+        if (lane < nc) { const SymContrib q = con[c0 + lane]; mo = q.soff; ml = q.len; }
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int64_t o = __shfl_sync(0xffffffffu, mo, u);
+            const int l = __shfl_sync(0xffffffffu, ml, u);
+            v[u] = (u < nc && lane < l) ? ldv(scratch + o + lane) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a[(c0 - cb + u) & 3] += v[u];
+    }
+}
+
+// one (output node, 32-row tile) by a CTA: warp w sums a contiguous slice of the list,
+// the slices are added in warp order
 __device__ __forceinline__ void gather_item_cta(const SymGNode& g, const SymContrib* __restrict__ con,
                                                 const SymVecsOut& yout, const double* __restrict__ scratch,
                                                 double* red) {
@@ -245,18 +271,7 @@ __device__ __forceinline__ void gather_item_cta(const SymGNode& g, const SymCont
     const int len = g.c1 - g.c0;
     const int cb = g.c0 + (int)((int64_t)len * warp / PH_W), ce = g.c0 + (int)((int64_t)len * (warp + 1) / PH_W);
     double a[4] = {0.0, 0.0, 0.0, 0.0};
-    int c = cb;
-    for (; c + 4 <= ce; c += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const SymContrib q = con[c + u];
-            if (lane < q.len) a[u] += ldv(scratch + q.soff + lane);
-        }
-    }
-    for (int u = 0; c < ce; ++c, ++u) {
-        const SymContrib q = con[c];
-        if (lane < q.len) a[u] += ldv(scratch + q.soff + lane);
-    }
+    gather_range(con, cb, ce, scratch, a);
     red[warp * 32 + lane] = (a[0] + a[1]) + (a[2] + a[3]);
     __syncthreads();
     if (warp == 0 && lane < g.n) {
@@ -274,18 +289,7 @@ __device__ __forceinline__ void gather_item_warp(const SymGNode& g, const SymCon
                                                  const SymVecsOut& yout, const double* __restrict__ scratch) {
     const int lane = threadIdx.x & 31;
     double a[4] = {0.0, 0.0, 0.0, 0.0};
-    int c = g.c0;
-    for (; c + 4 <= g.c1; c += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const SymContrib q = con[c + u];
-            if (lane < q.len) a[u] += ldv(scratch + q.soff + lane);
-        }
-    }
-    for (int u = 0; c < g.c1; ++c, ++u) {
-        const SymContrib q = con[c];
-        if (lane < q.len) a[u] += ldv(scratch + q.soff + lane);
-    }
+    gather_range(con, g.c0, g.c1, scratch, a);
     if (lane < g.n) yout.p[g.slot][g.off + lane] = (a[0] + a[1]) + (a[2] + a[3]);
 }
 
