@@ -191,9 +191,12 @@ enum {
                                in heap order; all column-major                   */
     SPD_Q_HSS_PIVOTS = 23,  /* int32[sum w]: QRCP pivots of every node (w each) */
     SPD_Q_TIMINGS = 30,     /* double[16]: phase seconds of the last build      */
-    SPD_Q_SHARD_WORK = 31   /* int64[2]: nodes whose per-node work (H2: proxy ID; HSS:
+    SPD_Q_SHARD_WORK = 31,  /* int64[2]: nodes whose per-node work (H2: proxy ID; HSS:
                                factorisation, QRCP, bases) this process computed, and
                                the number of such nodes; equal unless sharded (§8(e)) */
+    SPD_Q_SYM_STORE = 32    /* int64[2] (H2 handle): bytes of stored symmetric k = 1 blocks on
+                               this process and their number of pieces (0 before the first
+                               k = 1 product / PCG); sharded: the blocks touching owned nodes */
 };
 spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
 

@@ -22,6 +22,7 @@ Q_N, Q_LEVELS, Q_PERM, Q_NODES, Q_BOXES, Q_NNODES, Q_H2_RANKS, Q_SKELETONS = 1, 
 Q_LIST_COUNTS, Q_NEAR, Q_TYPE3, Q_TYPE1 = 9, 10, 11, 12
 Q_HSS_RANKS, Q_HSS_EXPORT_SIZE, Q_HSS_EXPORT, Q_HSS_PIVOTS, Q_TIMINGS = 20, 21, 22, 23, 30
 Q_SHARD_WORK = 31
+Q_SYM_STORE = 32
 
 
 class SpdError(RuntimeError):
@@ -211,6 +212,10 @@ class H2:
     def shard_work(self):
         """(nodes whose per-node work this process computed, nodes with per-node work)."""
         return tuple(int(v) for v in self.query(Q_SHARD_WORK, np.int64, 2))
+
+    def sym_store(self):
+        """(bytes, pieces) of the stored symmetric k = 1 blocks on this process."""
+        return tuple(int(v) for v in self.query(Q_SYM_STORE, np.int64, 2))
 
     def proxies(self, node):
         n_p = 4096 if self.d == 2 else 6144

@@ -96,7 +96,7 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
         if (k == 0) return SPD_OK;
         SPD_REQUIRE(X != nullptr && Y != nullptr, "h2_matvec: null X or Y");
         cudaStream_t s = (cudaStream_t)stream;
-        const bool shard = k >= 2;                 // multi-vector products are subtree-sharded
+        const bool shard = true;                   // products are subtree-sharded under a real communicator
         if (layout == SPD_LAYOUT_TREE) {
             h2_apply_tree(h, X, ldx, Y, ldy, (int)k, s, shard);
         } else {
@@ -234,6 +234,14 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
         SPD_REQUIRE(handle != nullptr && buf != nullptr, "spd_query: null argument");
         if (what >= SPD_Q_HSS_RANKS && what < SPD_Q_TIMINGS) {
             hss_query((const spd_hss_s*)handle, what, buf, bytes);
+            return SPD_OK;
+        }
+        if (what == SPD_Q_SYM_STORE) {
+            SPD_REQUIRE(!hss_if_hss(handle), "spd_query: SPD_Q_SYM_STORE needs an H2 handle");
+            const spd_h2_s* h2 = (const spd_h2_s*)handle;
+            const int64_t v[2] = {(int64_t)h2->sym.bytes, (int64_t)h2->sym.npieces};
+            need(bytes, sizeof(v));
+            std::memcpy(buf, v, sizeof(v));
             return SPD_OK;
         }
         if (what == SPD_Q_SHARD_WORK) {

@@ -614,8 +614,19 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         const int o = shard_owner(cm, count, a);
         return o < 0 || o == cm->rank;
     };
-    if (k == 1 && h->stored_mode == 1 && !shard) {
-        // stored symmetric blocks: up pass, near + all coupling levels in one launch, gather, down pass
+    auto exchange_rows = [&]() {                  // owners' leaf rows -> every rank
+        const int P = cm->nranks, per = nl / P;
+        std::vector<int64_t> rb(P), re(P);
+        for (int q = 0; q < P; ++q) {
+            const int i0 = l1 + q * per, i1 = l1 + (q + 1) * per - 1;
+            rb[q] = t.begin[i0];
+            re[q] = t.begin[i1] + t.size(i1);
+        }
+        comm_bcast_rows(cm, y, ldy, k, rb, re, s);
+    };
+    if (k == 1 && h->stored_mode == 1) {
+        // stored symmetric blocks: up pass, near + all coupling levels in one launch, gather,
+        // down pass (sharded: the store holds the blocks touching owned nodes, h2sym.cu)
         h2sym_build(h, h->sym_budget, s);
         std::vector<double*> xh(L, nullptr), yh(L, nullptr);
         if (L > 1) {
@@ -625,6 +636,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         }
         h2sym_apply(h, x, y, xh, yh, s);
         if (L > 1) h2_down(h, yh, L - 1, y, ldy, 1, s);
+        if (shard) exchange_rows();
         return;
     }
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
@@ -673,16 +685,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     }
     kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
     h2_down(h, yh, L - 1, y, ldy, k, s);
-    if (shard) {                                  // owners' leaf rows -> every rank
-        const int P = cm->nranks, per = nl / P;
-        std::vector<int64_t> rb(P), re(P);
-        for (int q = 0; q < P; ++q) {
-            const int i0 = l1 + q * per, i1 = l1 + (q + 1) * per - 1;
-            rb[q] = t.begin[i0];
-            re[q] = t.begin[i1] + t.size(i1);
-        }
-        comm_bcast_rows(cm, y, ldy, k, rb, re, s);
-    }
+    if (shard) exchange_rows();
 }
 
 }  // namespace spd

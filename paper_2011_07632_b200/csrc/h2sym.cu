@@ -19,6 +19,7 @@
 // and a gather kernel sums each output node's partials in a fixed order (no
 // atomics: the product is bitwise reproducible) and overwrites y / yh.
 #include "h2.hpp"
+#include "comm.hpp"
 #include "phases.cuh"
 #include <algorithm>
 
@@ -103,8 +104,18 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector
         con[lk].resize(h->lv[lk].count);
         for (int a = 0; a < h->lv[lk].count; ++a) con[lk][a].resize(ceil_div(h->lv[lk].rank[a], 32));
     }
+    // subtree sharding (real communicator, §8(e)): keep the blocks that touch an owned
+    // node and gather only owned outputs (boundary blocks are computed by both owners)
+    const spd_comm_s* cm = h->comm;
+    const bool shard = comm_real(cm) && nl >= cm->nranks;
+    auto mine = [&](int slot, int a) {
+        if (!shard) return true;
+        const int o = shard_owner(cm, slot == 0 ? nl : h->lv[slot].count, a);
+        return o < 0 || o == cm->rank;
+    };
     auto add_block = [&](int slot, int a, int b) {
         // rows: node a, columns: node b (local indices within the slot)
+        if (!mine(slot, a) && !mine(slot, b)) return;
         int na, nb;
         const double *tx, *sx;
         int64_t ds, tid0 = -1, sid0 = -1, xa0, xb0;
@@ -166,6 +177,7 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector
             for (int slot = 0; slot < L; ++slot) {
                 const int cnt = slot == 0 ? nl : h->lv[slot].count;
                 for (int a = 0; a < cnt; ++a) {
+                    if (!mine(slot, a)) continue;
                     const int n = slot == 0 ? (int)t.size(l1 + a) : h->lv[slot].rank[a];
                     const int64_t off = slot == 0 ? t.begin[l1 + a] : h->lv[slot].off[a];
                     for (int tt = 0; tt * 32 < n; ++tt) {

@@ -6,6 +6,7 @@
 // host reads back only (p^T q, ||r||^2, r^T z) per iteration for the stop and
 // breakdown tests.  Dot products use a fixed two-level reduction (deterministic).
 #include "hss.hpp"
+#include "comm.hpp"
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -87,7 +88,10 @@ static void apply_precond(spd_hss_s* M, int precond, PcgWork& w, int64_t N, cuda
 
 static void iteration_body(spd_h2_s* A, spd_hss_s* M, int precond, double* x, PcgWork& w, int64_t N,
                            cudaStream_t s) {
-    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);
+    // real communicator: the product is subtree-sharded (each rank its leaves' rows of q from
+    // the stored blocks touching its nodes, then the owners' rows are broadcast); vectors,
+    // dots and the preconditioner stay replicated (identical on every rank)
+    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s, comm_real(A->comm));
     dot_into(s, w, w.p.p, w.q.p, N, S_PQ, 1);
     {
         ProfScope prof(s, "pcg_vec", 4.0 * N, 40.0 * N);
@@ -158,7 +162,8 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     stage_mark(s, "pcg h2_prepare");
     // persistent cooperative kernel for the whole loop (pcgk.cu); env SPD_PCG_GRAPH=1
     // selects the per-iteration CUDA graph below instead (per-kernel profiling)
-    if (!getenv("SPD_PCG_GRAPH")) {
+    const bool sharded = comm_real(A->comm);
+    if (!getenv("SPD_PCG_GRAPH") && !sharded) {     // (sharded: no collective inside the persistent kernel)
         PcgPersistent pk;
         if (pcg_persistent_prepare(pk, A, M, x, w.r.p, w.p.p, w.q.p, w.z.p, s, precond)) {
             stage_mark(s, "pcg persistent prepare");
@@ -175,8 +180,8 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
         }
     }
     // capture one iteration as a graph (descriptors in a persistent arena)
-    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s);     // builds stored k=1 blocks outside the graph
-    bool use_graph = maxit > 1;
+    h2_apply_tree(A, w.p.p, N, w.q.p, N, 1, s, sharded);   // builds stored k=1 blocks outside the graph
+    bool use_graph = maxit > 1 && !(sharded && A->comm->hosted);   // host-staged collectives cannot be captured
     long long graph_kernels = 0;          // kernel nodes per replay (launch accounting)
     DescArena arena((size_t)64 << 20);
     if (use_graph) {

@@ -4,8 +4,9 @@ space and a host-staged communicator (spd_comm_init_host: every collective of th
 library goes through torch.distributed on host tensors).  Each rank computes only
 its subtrees' nodes of the H2 build (proxy-ID), of the SPD-HSS build (Alg. 4,
 P:1001-1056) and of a multi-vector H2 product (near + coupling blocks of its
-leaves, then a row exchange), then exchanges -- the code path of an NCCL rank minus
-the transport.
+leaves, then a row exchange) and of the k = 1 products inside PCG (stored symmetric
+blocks touching its nodes, row exchange every iteration), then exchanges -- the code
+path of an NCCL rank minus the transport.
 
 Checks:
 * every rank ends with the identical H2 and HSS (bitwise: the exchanges are sums of
@@ -35,14 +36,15 @@ def _run(spd, synth, cfg, comm):
     M = spd.spdhss_build(h, 40, 1e-3, seed=11)
     b = torch.tensor(synth.multivec(cfg.n, 1)[:, 0], device="cuda")
     x = spd.hss_solve(M, b).cpu().numpy()
-    _, rep = spd.pcg_solve(h, M, b, tol=1e-8, maxit=500)
+    xp, rep = spd.pcg_solve(h, M, b, tol=1e-8, maxit=500)   # sharded k=1 products inside
+    xp = xp.cpu().numpy()
     y = spd.h2_matvec(h, b).cpu().numpy()
     Xm = torch.tensor(synth.multivec(cfg.n, 8).T.copy(), device="cuda").t()     # column-major n x 8
     ym = spd.h2_matvec(h, Xm).t().cpu().numpy()        # k >= 2: sharded product + row exchange
     ex = M.export()
-    return {"h2_work": h.shard_work(), "hss_work": M.shard_work(), "h2_ranks": h.ranks(), "hss_ranks": M.ranks(),
-            "x": x, "y": y, "ym": ym, "iters": rep.iters,
-            "sha": "".join(hashlib.sha256(a.tobytes()).hexdigest() for a in (ex, x, ym))}
+    return {"sym": h.sym_store(), "h2_work": h.shard_work(), "hss_work": M.shard_work(), "h2_ranks": h.ranks(), "hss_ranks": M.ranks(),
+            "x": x, "y": y, "ym": ym, "xp": xp, "iters": rep.iters,
+            "sha": "".join(hashlib.sha256(a.tobytes()).hexdigest() for a in (ex, x, y, ym, xp))}
 
 
 def _worker(rank, world, port, n, leaf, q):
@@ -91,11 +93,15 @@ def test_sharded_build_with_real_exchanges(P, n, leaf):
         assert all(res[r][key][1] == total for r in range(P))
         assert all(res[r][key][0] < total for r in range(P))
         assert sum(res[r][key][0] for r in range(P)) >= total
-    print("P", P, "work", [res[r]["hss_work"] for r in range(P)], "x rel",
+    print("P", P, "work", [res[r]["hss_work"] for r in range(P)], "sym", [res[r]["sym"] for r in range(P)], ref["sym"], "x rel",
           np.linalg.norm(got["x"] - ref["x"]) / np.linalg.norm(ref["x"]), "iters", got["iters"], ref["iters"])
+    # the k = 1 block store is split too: each rank holds less than the whole, together >= it
+    assert ref["sym"][0] > 0 and all(res[r]["sym"][0] < ref["sym"][0] for r in range(P))
+    assert sum(res[r]["sym"][0] for r in range(P)) >= ref["sym"][0]
     assert np.abs(got["h2_ranks"] - ref["h2_ranks"]).max() <= 1
     assert np.abs(got["hss_ranks"] - ref["hss_ranks"]).max() <= 1
     assert np.linalg.norm(got["y"] - ref["y"]) <= 1e-11 * np.linalg.norm(ref["y"])
     assert np.linalg.norm(got["ym"] - ref["ym"]) <= 1e-11 * np.linalg.norm(ref["ym"])
     assert np.linalg.norm(got["x"] - ref["x"]) <= 1e-10 * np.linalg.norm(ref["x"])
     assert abs(got["iters"] - ref["iters"]) <= 2
+    assert np.linalg.norm(got["xp"] - ref["xp"]) <= 1e-6 * np.linalg.norm(ref["xp"])
