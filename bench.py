@@ -9,8 +9,8 @@ leaf 128, H2 tol 1e-10, HSS cap 100 / tol 1e-3, p = 10, PCG to 1e-8):
 `value` = seconds per step (max over ranks), lower is better.  Inputs are
 resident in HBM when the timed region starts; L2 (126 MB) is flushed between
 steps by writing a 256 MB buffer.  Multi-GPU (torchrun): independent replicas,
-weak scaling; with --shard one problem whose H2 build, SPD-HSS build and width-64
-product are sharded by subtrees over NCCL, strong scaling.
+weak scaling; with --shard one problem whose H2 build, SPD-HSS build and H2 products
+(PCG's included) are sharded by subtrees over NCCL, strong scaling.
 
 --impl reference: the CPU oracle (test infrastructure) timed on a bounded
 sample of the same workload; prints the same JSON line with "impl": "reference".
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
     ap.add_argument("--shard", action="store_true",
-                    help="N>1: ONE problem, H2/HSS builds and the k=64 product sharded by subtrees over NCCL "
+                    help="N>1: ONE problem, H2/HSS builds and all H2 products sharded by subtrees over NCCL "
                          "(strong scaling); "
                          "default: independent replicas (weak scaling)")
     return ap.parse_args()
@@ -373,7 +373,8 @@ def run_ours(args):
         "scaling": "strong" if comm is not None else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "l2_flush": "256 MB write between steps",
-                   "parallelism": ("h2_build, spdhss_build, k=64 product sharded by subtrees over NCCL; PCG replicated"
+                   "parallelism": ("h2_build, spdhss_build and every H2 product (PCG's k=1 too) sharded by subtrees over NCCL; "
+                                   "PCG vectors and HSS solve replicated"
                                    if comm is not None else "replicas") if world > 1 else "single GPU", "N": N},
         "breakdown": {k: round(statistics.mean(r[k] for r in recs), 4)
                       for k in ("h2_build_s", "spdhss_build_s", "pcg_s", "h2_mv_s")},
