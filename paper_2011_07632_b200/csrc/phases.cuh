@@ -46,6 +46,13 @@ __device__ __forceinline__ void basis_up_item(const BasisItem& it, double* sm) {
     if (k < s) {
         const double* p = it.T + k;
         int c = warp;
+        for (; c + 15 * PH_W < nr; c += 16 * PH_W) {     // 16 loads in flight per lane
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldg(p + (size_t)(c + u * PH_W) * s);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) acc[u & 7] += v[u] * xg[c + u * PH_W];
+        }
         for (; c + 7 * PH_W < nr; c += 8 * PH_W) {
             double v[8];
 #pragma unroll
