@@ -24,6 +24,9 @@ namespace cg = cooperative_groups;
 namespace spd {
 
 constexpr int PK_MAXPH = 64;
+#ifndef PCG_CTAS
+#define PCG_CTAS 2                 // CTAs per SM of the all-stored variant
+#endif
 
 struct PcgPlan {
     int64_t N;
@@ -86,7 +89,7 @@ __device__ __forceinline__ double grid_total(const double* part, double* bc) {
 // EVAL = false: every symmetric block is stored (no evaluation path compiled in, <= 128
 // registers, two CTAs per SM); EVAL = true: some blocks are evaluated (one CTA per SM)
 template <int KID, bool EVAL>
-__global__ void __launch_bounds__(PH_T, EVAL ? 1 : 2) pcg_persistent_kernel(PcgPlan P) {
+__global__ void __launch_bounds__(PH_T, EVAL ? 1 : PCG_CTAS) pcg_persistent_kernel(PcgPlan P) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     __shared__ double red[PH_W], bc;
@@ -319,7 +322,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, PH_T, im->smem));
     if (per < 1) return false;
-    im->grid = nsm * std::min(per, im->eval ? 1 : 2);    // all CTAs co-resident (cooperative launch)
+    im->grid = nsm * std::min(per, im->eval ? 1 : PCG_CTAS);    // all CTAs co-resident (cooperative launch)
     im->part.alloc((size_t)3 * im->grid);
     im->scal.alloc(8);
     P.part = im->part.p;
