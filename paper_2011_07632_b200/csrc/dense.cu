@@ -939,7 +939,7 @@ __device__ __forceinline__ void qr_tr0(int k) {        // CTA 0 only
 }
 
 template <int QCL>
-__global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
+__global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
     cg::cluster_group cluster = cg::this_cluster();
     const int g = (int)cluster.block_rank();
     const PanelDesc d = descs[blockIdx.x / QCL];
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(256) panel_qr_cluster_kernel(const PanelDesc* 
         const double* colj = sm + j * rp;
         // ---- partial sums over my rows i > j (warp w: entries e = w, w + 8, ...)
         //      e < QB: column c = j + e (c == j: sigma);  QB <= e < QB + j: reflector a = e - QB
-        for (int e = warp; e < QB + j; e += 8) {
+        for (int e = warp; e < QB + j; e += (int)(blockDim.x >> 5)) {
             double acc = 0.0;
             const double* other = e < QB ? (j + e < jb ? sm + (j + e) * rp : nullptr) : sm + (e - QB) * rp;
             if (other)
@@ -1106,7 +1106,7 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
                 }
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3((unsigned)pd.size() * qcl);
-                cfg.blockDim = dim3(256);
+                cfg.blockDim = dim3(512);
                 cfg.dynamicSmemBytes = sh;
                 cfg.stream = s;
                 cudaLaunchAttribute at[1];
