@@ -313,6 +313,27 @@ def run_ours(args):
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e-3)
+    # ---------------- H2 multi-vector sweep over BASELINE C5's widths k in {1, 16, 64, 256}
+    # on this workload's H2 (after the timed region; 3 timed products per k after one warm-up)
+    sweep = {}
+    _, h_sw, _ = step(pts, b)
+    fp64_pk = load_peaks().get("fp64_dgemm_tflops_sustained") or load_peaks().get("fp64_dgemm_tflops") or 35.5
+    for kk in (1, 16, 64, 256):
+        Vk = torch.tensor(np.asfortranarray(synth.multivec(N, kk)).T.copy(), device="cuda").t()
+        spd.h2_matvec(h_sw, Vk)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            spd.h2_matvec(h_sw, Vk)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        fl = h2_useful_flops(h_sw, kk)[0]
+        sweep[str(kk)] = {"ms": round(ms, 3), "useful_tflops": round(fl / ms / 1e9, 2),
+                          "frac_fp64_peak": round(fl / ms / 1e9 / fp64_pk, 3)}
+        del Vk
+    del h_sw
     # ---------------- profiled pass (same steps, per-kernel-class CUDA events on the
     # launching streams; kept out of the timed region because the per-launch event
     # pairs and their host-side drains perturb the step time)
@@ -384,6 +405,7 @@ def run_ours(args):
         "kernels": {k: {"launches": int(v["launches"]), "ms": round(v["ms"], 2),
                         "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
         "roofline": roof,
+        "h2_multivector_sweep": sweep,
         "h2_multivector": {"k": MV_K, "useful_gflop": round(record_flops["flops"] / 1e9, 2),
                            "gflops": round(record_flops["flops"] / mv / 1e9, 1),
                            "frac_fp64_peak": round(record_flops["flops"] / mv / 1e12 / fp64, 4),
