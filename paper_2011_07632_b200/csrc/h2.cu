@@ -522,6 +522,30 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
 }
 
 // Near-field targets/entries: Y[leaf a] += (K + shift) (X_a, X_b) X[b]
+// Multi-vector products read the kernel blocks from the symmetric k = 1 store when it
+// holds them (built on demand like the k = 1 product's; env SPD_MV_EVAL=1: evaluate):
+// no kernel evaluation, the blocks stream from HBM and the DMMA contraction is unchanged.
+static bool store_for_products(spd_h2_s* h, cudaStream_t s) {
+    static const bool eval = getenv("SPD_MV_EVAL") != nullptr;
+    if (eval || h->tree.L < 2) return false;
+    if (h->stored_mode == -1) h2_prepare(h, 1, s);
+    if (h->stored_mode != 1) return false;
+    h2sym_build(h, h->sym_budget, s);
+    return !h->sym.base.empty();
+}
+static void use_store(const spd_h2_s* h, int slot, int a, int b, int na, int nb, KbEntry& e) {
+    const auto& base = h->sym.base;
+    if (a <= b) {
+        auto it = base.find(sym_key(slot, a, b));
+        if (it == base.end()) return;
+        e.kst = h->sym.vals.p + it->second; e.kmode = 1; e.kld = nb;
+    } else {
+        auto it = base.find(sym_key(slot, b, a));
+        if (it == base.end()) return;
+        e.kst = h->sym.vals.p + it->second; e.kmode = 2; e.kld = na;
+    }
+}
+
 static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t ldy, int k,
                        std::vector<KbBlock>& blocks, std::vector<KbTarget>& targets,
                        std::vector<KbEntry>& entries) {
@@ -639,9 +663,15 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         if (shard) exchange_rows();
         return;
     }
+    const bool stored = k >= 2 && store_for_products(h, s);
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
     std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
     near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
+    if (stored)
+        for (auto& tg : targets)
+            for (int e = tg.e_begin; e < tg.e_end; ++e)
+                use_store(h, 0, tg.blk, entries[e].src, (int)t.size(l1 + tg.blk), (int)t.size(l1 + entries[e].src),
+                          entries[e]);
     if (shard) {
         std::vector<KbTarget> kept;
         for (auto& tg : targets) if (mine(nl, tg.blk)) kept.push_back(tg);
@@ -675,8 +705,10 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             KbTarget tg{b0 + a, (int)entries.size(), 0};
             while (e < T3.size() && T3[e].first == i) {
                 const int bj = T3[e].second - lv.first;
-                if (lv.rank[bj] > 0 && lv.rank[a] > 0)
+                if (lv.rank[bj] > 0 && lv.rank[a] > 0) {
                     entries.push_back({b0 + bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
+                    if (stored) use_store(h, lk, a, bj, lv.rank[a], lv.rank[bj], entries.back());
+                }
                 ++e;
             }
             tg.e_end = (int)entries.size();

@@ -1,6 +1,7 @@
 // h2.hpp -- H2 handle (internal).  PAPER.md §5.1.
 #pragma once
 #include "common.cuh"
+#include <unordered_map>
 #include "kblock.cuh"
 #include "tree.hpp"
 
@@ -49,7 +50,13 @@ struct H2SymStore {
     std::vector<SymGNode> gnodes_h;              // host copy (per-slot schedules of the persistent PCG)
     double flops = 0, bytes = 0, stored_frac = 1.0;
     bool built = false;
+    // fully stored blocks (a <= b) of slot s: sym_key(s, a, b) -> offset in vals of band 0
+    // (bands of a block are consecutive), for the multi-vector products (kblock kmode)
+    std::unordered_map<uint64_t, int64_t> base;
 };
+inline uint64_t sym_key(int slot, int a, int b) {
+    return ((uint64_t)slot << 56) | ((uint64_t)(uint32_t)a << 28) | (uint64_t)(uint32_t)b;
+}
 
 }  // namespace spd
 

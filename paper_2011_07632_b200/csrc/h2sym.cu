@@ -86,7 +86,7 @@ struct PlanBlock { int slot, a, b; };   // block (a <= b) of slot 0 (near, leave
 static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector<SymBuild>* builds,
                      std::vector<SymPiece>* pieces, std::vector<SymGNode>* gnodes, std::vector<SymContrib>* gcon,
                      int64_t* nvals, int64_t* nscratch, double* flops, int64_t* nall, int* nbig_out = nullptr,
-                     int* nbmax_out = nullptr) {
+                     int* nbmax_out = nullptr, std::unordered_map<uint64_t, int64_t>* bases = nullptr) {
     int64_t npiece = 0;
     int nbmax = 1;
     const TreeH& t = h->tree;
@@ -133,6 +133,8 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector
         if (na == 0 || nb == 0) return;
         const bool diag = (a == b);
         fl += 2.0 * na * nb * (diag ? 1.0 : 2.0);
+        const int64_t base0 = vb;
+        bool all_stored = true;
         for (int r0 = 0; r0 < na; r0 += 32 * SY_NW) {
             const int nr = std::min(32 * SY_NW, na - r0);          // band of up to 4 row tiles
             const int nt = ceil_div(nr, 32);
@@ -157,12 +159,14 @@ static void sym_plan(const spd_h2_s* h, int64_t budget, double frac, std::vector
             if (!diag) sc += nb;
             if (pieces) pieces->push_back(pc);
             if (store) vb += 32LL * nb * nt;
+            else all_stored = false;
             nbmax = std::max(nbmax, nb);
             for (int w = 0; w < nt; ++w)
                 con[slot][a][r0 / 32 + w].push_back({pc.fwd + 32 * w, 0, std::min(32, nr - 32 * w)});
             if (!diag)
                 for (int tb = 0; tb * 32 < nb; ++tb) con[slot][b][tb].push_back({pc.trn + 32 * tb, 0, std::min(32, nb - 32 * tb)});
         }
+        if (bases && all_stored) (*bases)[sym_key(slot, a, b)] = base0;
     };
     for (const auto& pr : h->lists.near)
         if (pr.first <= pr.second) add_block(0, pr.first - l1, pr.second - l1);
@@ -218,8 +222,9 @@ void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s) {
     std::vector<SymGNode> gnodes;
     std::vector<SymContrib> gcon;
     int64_t nv = 0, ns = 0, na = 0;
+    st.base.clear();
     sym_plan(h, (int64_t)(budget_bytes / 8), h->sym_frac, &builds, &pieces, &gnodes, &gcon, &nv, &ns, &st.flops, &na,
-             &st.nbig, &st.nbmax);
+             &st.nbig, &st.nbmax, &st.base);
     st.vals.alloc(std::max<int64_t>(1, nv));
     st.scratch.alloc(std::max<int64_t>(1, ns));
     st.pieces.upload(pieces, s);

@@ -99,15 +99,30 @@ __global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
                 if (tid < KB_K * 4) Sx[tid / KB_K][tid % KB_K] = sr;
                 __syncthreads();
                 if (k0 + KB_K < sb.n) load(k0 + KB_K);          // prefetch the next chunk
+                if (en.kmode == 0) {
 #pragma unroll
-                for (int c = 0; c < EPT; ++c) {
-                    const int kc = ec0 + c;
-                    const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
-                    double kv;
-                    if constexpr (KID == SPD_K_RPY) kv = rpy_entry(kp, d0, d1, d2, (int)rx[3], (int)Sx[3][kc]);
-                    else kv = kval<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
-                    if (use_shift && rid == sb.id0 + k0 + kc) kv += shift;
-                    Ks[kc][er] = (er < nrows && kc < nk) ? kv : 0.0;
+                    for (int c = 0; c < EPT; ++c) {
+                        const int kc = ec0 + c;
+                        const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
+                        double kv;
+                        if constexpr (KID == SPD_K_RPY) kv = rpy_entry(kp, d0, d1, d2, (int)rx[3], (int)Sx[3][kc]);
+                        else kv = kval<KID>(kp, d0 * d0 + d1 * d1 + d2 * d2);
+                        if (use_shift && rid == sb.id0 + k0 + kc) kv += shift;
+                        Ks[kc][er] = (er < nrows && kc < nk) ? kv : 0.0;
+                    }
+                } else {                          // stored block (symmetric store): loads only
+                    const int r = r0 + er;
+                    double kv[EPT];
+#pragma unroll
+                    for (int c = 0; c < EPT; ++c) {
+                        const int kc = ec0 + c, cc = k0 + kc;
+                        const double* a = en.kmode == 1
+                            ? en.kst + (size_t)(r >> 5) * 32 * en.kld + (size_t)cc * 32 + (r & 31)
+                            : en.kst + (size_t)(cc >> 5) * 32 * en.kld + (size_t)r * 32 + (cc & 31);
+                        kv[c] = (er < nrows && kc < nk) ? __ldg(a) : 0.0;
+                    }
+#pragma unroll
+                    for (int c = 0; c < EPT; ++c) Ks[ec0 + c][er] = kv[c];
                 }
                 __syncthreads();
 #pragma unroll

@@ -15,6 +15,13 @@ struct KbEntry {            // Y[:, :ncols] += K(target, blocks[src]) X[:, :ncol
     const double* X; int ldx;
     double* Y; int ldy;
     int ncols;
+    // optional: the block is read from the symmetric k = 1 store (h2sym.cu) instead of
+    // being evaluated: kmode 1 -- stored as (target, src), entry (r, c) at
+    // kst[(r / 32) 32 kld + 32 c + r % 32], kld = n_src; kmode 2 -- stored as (src, target),
+    // entry (r, c) at kst[(c / 32) 32 kld + 32 r + c % 32], kld = n_target.  Stored
+    // values include the diagonal shift.
+    const double* kst = nullptr;
+    int kmode = 0, kld = 0;
 };
 struct KbTarget { int blk; int e_begin, e_end; };
 
