@@ -202,8 +202,10 @@ static spd_status pcg_common(spd_h2_t A, spd_hss_t M, int precond, int layout, c
             DBuf<double> bt(N), xt(N);
             permute_rows(s, A->perm.p, N, 1, b, N, bt.p, N, true);
             pcg_tree(A, M, bt.p, xt.p, tol, maxit, rep, s, precond);
+            stage_mark(s, "pcg teardown");
             permute_rows(s, A->perm.p, N, 1, xt.p, N, x, N, false);
         }
+        stage_mark(s, "pcg permute back");
         if (!rep->converged) {
             set_last_error("pcg_solve: not converged in maxit iterations");
             return SPD_ENOCONV;

@@ -60,6 +60,7 @@ void prof_release(ProfCaptured* c);
 // builds off the host's critical path (cudaMalloc/cudaFree synchronize).
 cudaStream_t& alloc_stream();
 void init_mem_pool();
+size_t device_free_bytes();      // free device memory + the pool's unused reserve
 struct AllocStreamScope {
     cudaStream_t prev;
     explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { init_mem_pool(); alloc_stream() = s; }

@@ -504,8 +504,7 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
     const char* env = getenv("SPD_STORED");
     if (env && env[0] == '0') { h->stored_mode = 0; return; }
     const double need = (double)h2sym_bytes(h);
-    size_t fr = 0, tot = 0;
-    SPD_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t fr = device_free_bytes();      // free + the pool's unused reserve
     h->stored_mode = 1;
     // store as much as fits, keeping 6 GB and 15 % of the free memory for everything else
     h->sym_budget = (env && env[0] == '1') ? need
@@ -525,15 +524,20 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
 // Multi-vector products read the kernel blocks from the symmetric k = 1 store when it
 // holds them (built on demand like the k = 1 product's; env SPD_MV_EVAL=1: evaluate):
 // no kernel evaluation, the blocks stream from HBM and the DMMA contraction is unchanged.
-static bool store_for_products(spd_h2_s* h, cudaStream_t s) {
+bool h2_store_for_products(spd_h2_s* h, cudaStream_t s, bool build) {
     static const bool eval = getenv("SPD_MV_EVAL") != nullptr;
     if (eval || h->tree.L < 2) return false;
+    if (h->sym.built) return !h->sym.base.empty();
+    // built here only when it is small next to the free memory (the SPD-HSS build that
+    // usually follows needs its workspaces; PCG builds it within its own budget anyway)
+    if (h->sym_need < 0.0) h->sym_need = (double)h2sym_bytes(h);
+    if (!build || h->sym_need > 0.25 * (double)device_free_bytes()) return false;
     if (h->stored_mode == -1) h2_prepare(h, 1, s);
     if (h->stored_mode != 1) return false;
     h2sym_build(h, h->sym_budget, s);
     return !h->sym.base.empty();
 }
-static void use_store(const spd_h2_s* h, int slot, int a, int b, int na, int nb, KbEntry& e) {
+void h2_use_store(const spd_h2_s* h, int slot, int a, int b, int na, int nb, KbEntry& e) {
     const auto& base = h->sym.base;
     if (a <= b) {
         auto it = base.find(sym_key(slot, a, b));
@@ -663,15 +667,15 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         if (shard) exchange_rows();
         return;
     }
-    const bool stored = k >= 2 && store_for_products(h, s);
+    const bool stored = k >= 2 && h2_store_for_products(h, s);
     SPD_CUDA(cudaMemset2DAsync(y, sizeof(double) * ldy, 0, sizeof(double) * N, k, s));
     std::vector<KbBlock> blocks; std::vector<KbTarget> targets; std::vector<KbEntry> entries;
     near_descs(h, x, ldx, y, ldy, k, blocks, targets, entries);
     if (stored)
         for (auto& tg : targets)
             for (int e = tg.e_begin; e < tg.e_end; ++e)
-                use_store(h, 0, tg.blk, entries[e].src, (int)t.size(l1 + tg.blk), (int)t.size(l1 + entries[e].src),
-                          entries[e]);
+                h2_use_store(h, 0, tg.blk, entries[e].src, (int)t.size(l1 + tg.blk),
+                             (int)t.size(l1 + entries[e].src), entries[e]);
     if (shard) {
         std::vector<KbTarget> kept;
         for (auto& tg : targets) if (mine(nl, tg.blk)) kept.push_back(tg);
@@ -707,7 +711,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
                 const int bj = T3[e].second - lv.first;
                 if (lv.rank[bj] > 0 && lv.rank[a] > 0) {
                     entries.push_back({b0 + bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
-                    if (stored) use_store(h, lk, a, bj, lv.rank[a], lv.rank[bj], entries.back());
+                    if (stored) h2_use_store(h, lk, a, bj, lv.rank[a], lv.rank[bj], entries.back());
                 }
                 ++e;
             }

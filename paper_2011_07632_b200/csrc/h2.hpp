@@ -75,6 +75,7 @@ struct spd_h2_s {
     spd::DBuf<double> X;          // d x N tree-order points (SoA)
     spd::DBuf<int64_t> perm;      // tree position -> original index
     std::vector<spd::H2Level> lv; // [0..L-1], level k at lv[k] (lv[0] unused)
+    double sym_need = -1.0;          // bytes of the full symmetric store (cached plan size)
     int m = 1, dim = 3;              // dofs per point (RPY: 3), spatial dimension; N = m * points,
                                      // d = coordinate rows of X (RPY: dim + 1, the component)
     double timings[16] = {0};
@@ -112,6 +113,11 @@ void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& x
 void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s);
 size_t h2sym_bytes(const spd_h2_s* h);
 void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s);
+// kernel blocks of multi-vector products from the symmetric store (built on demand when
+// the k = 1 policy stores blocks); h2_use_store marks entry e of block (a, b) of slot
+// `slot` (0: leaves, l: level-l skeletons; na, nb their sizes) if the store holds it
+bool h2_store_for_products(spd_h2_s* h, cudaStream_t s, bool build = true);
+void h2_use_store(const spd_h2_s* h, int slot, int a, int b, int na, int nb, KbEntry& e);
 void h2sym_apply(spd_h2_s* h, const double* x, double* y, const std::vector<double*>& xh,
                  const std::vector<double*>& yh, cudaStream_t s);
 // proxy points of heap node `node` into P_dev (d x n_proxy SoA)

@@ -109,14 +109,34 @@ static void iteration_body(spd_h2_s* A, spd_hss_s* M, int precond, double* x, Pc
     }
 }
 
+static cudaStream_t pcg_private_stream() {
+    struct Cache {
+        int dev = -1; cudaStream_t s = nullptr;
+    };
+    static thread_local Cache c;
+    int dev = 0;
+    SPD_CUDA(cudaGetDevice(&dev));
+    if (!c.s || c.dev != dev) {
+        SPD_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));   // lives as long as the thread
+        c.dev = dev;
+    }
+    return c.s;
+}
+static double* pcg_pinned_scalars() {
+    static thread_local double* hs = nullptr;
+    if (!hs) SPD_CUDA(cudaMallocHost(&hs, sizeof(double) * S_NSCAL));
+    return hs;
+}
+
 void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol, int maxit, spd_pcg_report* rep,
               cudaStream_t user, int precond) {
     const int64_t N = A->N;
     const auto t0 = std::chrono::steady_clock::now();
     stage_mark(user, nullptr);
-    // private non-blocking stream (graph capture is illegal on the legacy stream)
-    cudaStream_t s;
-    SPD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    // private non-blocking stream (graph capture is illegal on the legacy stream), created
+    // once per thread and device: creating / destroying it per solve costs up to
+    // hundreds of ms at teardown when the driver reclaims its resources
+    cudaStream_t s = pcg_private_stream();
     AllocStreamScope alloc_scope(s);           // workspaces are stream-ordered on s
     cudaEvent_t ev;
     SPD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -133,13 +153,10 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             cudaStreamSynchronize(s);
             prof_release(pc);
             cudaEventDestroy(ev);
-            cudaStreamDestroy(s);
         }
     } cl{s, user, ev};
     PcgWork w(N);
-    double* hs = nullptr;                       // pinned host scalars
-    SPD_CUDA(cudaMallocHost(&hs, sizeof(double) * S_NSCAL));
-    struct FreeHost { double* p; ~FreeHost() { cudaFreeHost(p); } } fh{hs};
+    double* hs = pcg_pinned_scalars();          // pinned host scalars (per thread, reused)
 
     SPD_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * N, s));
     SPD_CUDA(cudaMemcpyAsync(w.r.p, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
@@ -170,6 +187,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             double out[4];
             pcg_persistent_run(pk, hs[S_RZ], nb, tol, maxit, out, s);
             stage_mark(s, "pcg persistent run");
+
             rep->iters = (int)out[1];
             rep->relres = std::sqrt(out[0]) / nb;
             rep->converged = out[2] != 0.0;

@@ -1,4 +1,5 @@
 // prof.cpp -- launch counter and per-kernel-class event timing (instrumentation).
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -68,14 +69,41 @@ void init_mem_pool() {
         if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) { cudaGetLastError(); return; }
-        // keep up to half of the device memory cached in the pool: the builds at N = 2^20
-        // work with tens of GB, and returning them to the OS at every synchronization
-        // (then mapping them again) costs seconds
+        // The pool keeps up to half the device memory mapped across synchronizations and is
+        // pre-grown once: growing it mid-build (mapping new physical memory when no free
+        // block fits) stalled single allocations for 50 ms - 1.3 s on B200 (measured in
+        // tools/phase_probe.py: spdhss_build 72 ms -> up to 1391 ms), a pre-grown pool of
+        // min(30 % of the free memory, 48 GB) removed the outliers.  SPD_POOL_RESERVE_GB
+        // overrides the reservation (0: none).
         size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); tot = (size_t)48 << 30; }
-        uint64_t thr = (uint64_t)(tot / 2);
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = tot = (size_t)48 << 30; }
+        uint64_t thr = getenv("SPD_POOL_KEEP_ALL") ? ~0ull : (uint64_t)(tot / 2);   // >= the reserve
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        size_t reserve = std::min<size_t>((size_t)(0.3 * (double)fr), (size_t)48 << 30);
+        if (const char* r = getenv("SPD_POOL_RESERVE_GB")) reserve = (size_t)(atof(r) * (double)(1ull << 30));
+        if (reserve > 0) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, reserve, 0) == cudaSuccess) { cudaFreeAsync(p, 0); cudaStreamSynchronize(0); }
+            cudaGetLastError();
+        }
     });
+}
+
+// device memory available to the library: free device memory plus the memory the pool
+// has mapped but not handed out (the pre-grown reserve)
+size_t device_free_bytes() {
+    size_t fr = 0, tot = 0;
+    SPD_CUDA(cudaMemGetInfo(&fr, &tot));
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t res = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && res > used)
+            fr += (size_t)(res - used);
+    }
+    cudaGetLastError();
+    return fr;
 }
 
 DescArena*& desc_arena() {

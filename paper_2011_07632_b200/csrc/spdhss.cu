@@ -137,6 +137,7 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
     const TreeH& t = h->tree;
     const int L = t.L, w = H->w;
     const int64_t N = h->N;
+    const bool stored = h2_store_for_products(h, s, false);     // kernel blocks from the symmetric store
     Y.alloc((size_t)(L - 1) * N * w);
     Y.zero(s);
     auto slice = [&](int c) { return Y.p + (size_t)(c - 2) * N * w; };   // bucket c = 2..L
@@ -160,8 +161,10 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
             }
             std::stable_sort(js.begin(), js.end(), [](auto& x, auto& y) { return x.first < y.first; });
             KbTarget tg{i - l1, (int)entries.size(), 0};
-            for (auto& [c, j] : js)
+            for (auto& [c, j] : js) {
                 entries.push_back({j - l1, om + t.begin[j], (int)N, slice(c) + t.begin[i], (int)N, w});
+                if (stored) h2_use_store(h, 0, i - l1, j - l1, (int)t.size(i), (int)t.size(j), entries.back());
+            }
             tg.e_end = (int)entries.size();
             targets.push_back(tg);
         }
@@ -207,8 +210,10 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
             KbTarget tg{a, (int)entries.size(), 0};
             for (auto& [c, j] : js) {
                 const int b = j - lv.first;
-                if (lv.rank[a] && lv.rank[b])
+                if (lv.rank[a] && lv.rank[b]) {
                     entries.push_back({b, xhp[l] + lv.off[b], (int)lv.S, ybp[c][l] + lv.off[a], (int)lv.S, w});
+                    if (stored) h2_use_store(h, l, a, b, lv.rank[a], lv.rank[b], entries.back());
+                }
             }
             tg.e_end = (int)entries.size();
             targets.push_back(tg);
@@ -237,9 +242,10 @@ static void kernel_sandwich(spd_hss_s* H, cudaStream_t s, const std::vector<Pair
                             const std::vector<KbBlock>& blocks, int first,
                             const std::vector<const double*>& X, const std::vector<int>& ldX,
                             const std::vector<const double*>& Left, const std::vector<int>& ldLeft,
-                            const std::vector<int>& rank, HssLevel& dst) {
+                            const std::vector<int>& rank, HssLevel& dst, int slot) {
     if (pairs.empty()) return;
     spd_h2_s* h = H->h2;
+    const bool stored = h2_store_for_products(h, s, false);     // slot: 0 leaf points, l level-l skeletons
     std::vector<int64_t> goff(pairs.size() + 1, 0);
     for (size_t q = 0; q < pairs.size(); ++q)
         goff[q + 1] = goff[q] + (int64_t)blocks[pairs[q].i - first].n * rank[pairs[q].j - first];
@@ -254,8 +260,11 @@ static void kernel_sandwich(spd_hss_s* H, cudaStream_t s, const std::vector<Pair
         while (q < pairs.size() && pairs[q].i == i) {
             const int j = pairs[q].j;
             const int ni = blocks[i - first].n;
-            if (rank[j - first] > 0 && ni > 0 && blocks[j - first].n > 0)
+            if (rank[j - first] > 0 && ni > 0 && blocks[j - first].n > 0) {
                 entries.push_back({j - first, X[j - first], ldX[j - first], G.p + goff[q], ni, rank[j - first]});
+                if (stored)
+                    h2_use_store(h, slot, i - first, j - first, ni, blocks[j - first].n, entries.back());
+            }
             ++q;
         }
         tg.e_end = (int)entries.size();
@@ -582,7 +591,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         std::vector<PairProd> pairs;                                // B_ij by the owner of i (i < j)
         for (auto& pr : h->lists.type1[1])
             if (pr.first < pr.second && own1[pr.first - l1.first]) pairs.push_back({pr.first, pr.second});
-        kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1);
+        kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1, 0);
         stage_mark(s, "hss leaf B type1");
         blocks.clear(); X.clear(); ldX.clear(); Left.clear(); ldLeft.clear();
         for (int a = 0; a < nl; ++a) {
@@ -593,7 +602,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
         pairs.clear();
         for (auto& pr : h->lists.type3[1])
             if (pr.first < pr.second && own1[pr.first - l1.first]) pairs.push_back({pr.first, pr.second});
-        kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1);
+        kernel_sandwich(H, s, pairs, blocks, l1.first, X, ldX, Left, ldLeft, l1.rank, l1, 1);
         sh.sum(l1.B, l1.B.n, nl, s);
         sh.sum(l1.F, l1.F_off[nl], nl, s);
     }
@@ -778,7 +787,7 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
             std::vector<PairProd> pairs;
             for (auto& pr : h->lists.type3[k])
                 if (pr.first < pr.second && own[pr.first - lv.first]) pairs.push_back({pr.first, pr.second});
-            kernel_sandwich(H, s, pairs, blocks, lv.first, X, ldX, Left, ldLeft, lv.rank, lv);
+            kernel_sandwich(H, s, pairs, blocks, lv.first, X, ldX, Left, ldLeft, lv.rank, lv, k);
         }
         sh.sum(lv.B, lv.B.n, n, s);
         for (int kp2 = k + 1; kp2 < L; ++kp2) std::swap(Tprev[kp2], Tcur[kp2]);

@@ -54,6 +54,7 @@ def _worker(rank, world, port, n, leaf, q):
         sys.path.insert(0, ROOT)
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
+        os.environ["SPD_POOL_RESERVE_GB"] = "2"     # P processes share one GPU
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         import paper_2011_07632_b200 as spd
