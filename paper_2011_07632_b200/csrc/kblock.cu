@@ -36,7 +36,7 @@ __device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
 // with the 16 x NC slice of X; the next chunk's X slice and coordinates are
 // prefetched into registers while the current chunk is evaluated/contracted.
 template <int KID, int NC>
-__global__ void __launch_bounds__(2 * NC, 256 / NC) kblock_kernel(
+__global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : 256 / NC) kblock_kernel(
     KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
     const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
     const KbWork* __restrict__ work, double* __restrict__ partial) {
@@ -324,7 +324,7 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     }
     int maxc_all = 0;
     for (auto& e : entries) maxc_all = std::max(maxc_all, e.ncols);
-    const int NC = maxc_all > 64 ? 128 : 64;
+    const int NC = maxc_all > 64 ? 128 : (maxc_all > 32 ? 64 : 32);   // column tile >= k for k <= 128
     // work items; a target whose entries (one output group) hold many more source
     // points than the average item is cut into segments at entry boundaries, so the
     // long top-level coupling lists spread over many CTAs (ordered reduction after)
@@ -401,7 +401,8 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     const unsigned nb = (unsigned)work.size();
 #define SPD_KB_LAUNCH(KID)                                                                                    \
     if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
-    else kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
+    else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); \
+    else kblock_kernel<KID, 32><<<nb, 64, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
     switch (kp.id) {
     case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
     case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
@@ -414,7 +415,8 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     if (!red.empty()) {
         DevArray<KbRed> dr(s, red);
         if (NC == 128) kb_reduce_kernel<128><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
-        else kb_reduce_kernel<64><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        else if (NC == 64) kb_reduce_kernel<64><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        else kb_reduce_kernel<32><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
         SPD_LAUNCH();
     }
 }
