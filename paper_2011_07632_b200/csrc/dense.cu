@@ -438,6 +438,10 @@ __global__ void __launch_bounds__(256) trsv_warp_kernel(const TrsmDesc* __restri
     for (int i = lane; i < n; i += 32) xg[i] = xs[i];
 }
 
+constexpr int TRSM_REC_N = 128;
+void trsm_rec(cudaStream_t s, const std::vector<TrsmDesc>& d, bool lower);
+void trsm_base(cudaStream_t s, const std::vector<TrsmDesc>& d, bool lower, bool trans);
+
 void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans) {
     {
         int nrmax = 0, nmax = 0;
@@ -479,6 +483,47 @@ void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, boo
             return;
         }
     }
+    const bool lower_ = (uplo == 'L' || uplo == 'l');
+    if (!trans) {
+        bool any_big = false;
+        for (auto& t : d) any_big |= t.n > TRSM_REC_N && t.nrhs >= 64;
+        if (any_big) { trsm_rec(s, d, lower_); return; }
+    }
+    trsm_base(s, d, lower_, trans);
+}
+
+// Recursive blocked TRSM (no transpose) for n > TRSM_REC_N: [T11 0; T21 T22] (lower) or
+// [T11 T12; 0 T22] (upper) split at a multiple of 32; the off-diagonal update
+// X_other -= T_off X_solved is one batched DMMA GEMM per recursion step (K = the
+// solved half), so most of the n^2 nrhs flops run on the tensor path; the
+// diagonal blocks at the bottom use the 32-row blocked kernel.
+void trsm_rec(cudaStream_t s, const std::vector<TrsmDesc>& d, bool lower) {
+    std::vector<TrsmDesc> small, first, second;
+    std::vector<GemmDesc> upd;
+    for (const auto& t : d) {
+        if (t.n <= 0 || t.nrhs <= 0) continue;
+        if (t.n <= TRSM_REC_N || t.nrhs < 64) { small.push_back(t); continue; }   // few columns: GEMMs too thin
+        const int h = ((t.n / 2 + 31) / 32) * 32;
+        const TrsmDesc a{t.T, t.X, h, t.nrhs, t.ldt, t.ldx};                                        // T11, X1
+        const TrsmDesc b{t.T + h + (size_t)h * t.ldt, t.X + h, t.n - h, t.nrhs, t.ldt, t.ldx};       // T22, X2
+        if (lower) {
+            first.push_back(a); second.push_back(b);
+            upd.push_back({t.T + h, t.X, t.X + h, t.n - h, t.nrhs, h, t.ldt, t.ldx, t.ldx});           // X2 -= T21 X1
+        } else {
+            first.push_back(b); second.push_back(a);
+            upd.push_back({t.T + (size_t)h * t.ldt, t.X + h, t.X, h, t.nrhs, t.n - h, t.ldt, t.ldx, t.ldx});  // X1 -= T12 X2
+        }
+    }
+    if (!small.empty()) trsm_base(s, small, lower, false);
+    if (first.empty()) return;
+    trsm_rec(s, first, lower);
+    gemm_batched(s, upd, false, false, -1.0, 1.0);
+    trsm_rec(s, second, lower);
+}
+
+// the 32-row blocked kernel: one CTA per (matrix, 32 right-hand sides)
+void trsm_base(cudaStream_t s, const std::vector<TrsmDesc>& d, bool lower_in, bool trans) {
+    const char uplo = lower_in ? 'L' : 'U';
     std::vector<int2> work;
     for (int i = 0; i < (int)d.size(); ++i) {
         if (d[i].n <= 0 || d[i].nrhs <= 0) continue;
