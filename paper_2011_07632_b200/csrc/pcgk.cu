@@ -18,12 +18,14 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <unordered_map>
 
 namespace cg = cooperative_groups;
 
 namespace spd {
 
 constexpr int PK_MAXPH = 64;
+constexpr int PK_MAXID = 16;       // fused identity levels at most
 #ifndef PCG_CTAS
 #define PCG_CTAS 2                 // CTAs per SM of the all-stored variant
 #endif
@@ -44,10 +46,19 @@ struct PcgPlan {
     const SymGNode* gnodes; int ngnodes, nbig; const SymContrib* gcon; int nbmax;
     SymVecs xin; SymVecsOut yout;
     KernelParams kp; double shift; int d;
+    // identity levels 1..nid (every node keeps all its candidates, T empty): their up passes
+    // are gathers xh_l[k] = p[idb[..]] done in the first up phase together with level
+    // nid + 1 (whose items read p through composed pivots), their down passes one phase
+    // q[o] += yh_1[a_1(o)] + (... + yh_nid[a_nid(o)]) in the order of the level-by-level sums
+    int nid, id_tot;
+    const int* idb; int id_beg[PK_MAXID + 1];
+    const int* ida;                // nid x N, -1: no coefficient
     // HSS solve z = M r
     int nhs;
     const HsNode* hs; const HsItem* hsi; int hs_off[PK_MAXPH + 1];
     unsigned char hs_cta[PK_MAXPH];   // 1: phase of CTA items (dense top operator), 0: warp items
+    double* id_xh[PK_MAXID];
+    double* id_yh[PK_MAXID];
     unsigned long long* trace;     // optional: globaltimer after every phase of iteration 2 (CTA 0)
 };
 
@@ -111,6 +122,12 @@ __global__ void __launch_bounds__(PH_T, EVAL ? 1 : PCG_CTAS) pcg_persistent_kern
         if (P.trace && it == 2 && blockIdx.x == 0 && threadIdx.x == 0) P.trace[nph++] = gtimer();
         // ---------------- q = A p (H2, k = 1)
         for (int l = 0; l < P.nup; ++l) {
+            if (l == 0 && P.nid)
+                for (int64_t e = i0; e < P.id_tot; e += stride) {
+                    int lv = 0;
+                    while (e >= P.id_beg[lv + 1]) ++lv;
+                    P.id_xh[lv][e - P.id_beg[lv]] = ldv(P.p + P.idb[e]);
+                }
             for (int w = P.up_off[l] + blockIdx.x; w < P.up_off[l + 1]; w += gridDim.x) basis_up_item(P.up[w], sm);
             sync(it);
         }
@@ -128,6 +145,21 @@ __global__ void __launch_bounds__(PH_T, EVAL ? 1 : PCG_CTAS) pcg_persistent_kern
         sync(it);
         for (int l = 0; l < P.ndn; ++l) {
             for (int w = P.dn_off[l] + blockIdx.x; w < P.dn_off[l + 1]; w += gridDim.x) basis_down_item(P.dn[w], sm);
+            sync(it);
+        }
+        if (P.nid) {
+            for (int64_t o = i0; o < N; o += stride) {
+                double acc = 0.0;
+                bool has = false;
+                for (int lv = P.nid - 1; lv >= 0; --lv) {
+                    const int a = P.ida[(size_t)lv * N + o];
+                    if (a < 0) continue;
+                    const double v = ldv(P.id_yh[lv] + a);
+                    acc = has ? v + acc : v;
+                    has = true;
+                }
+                if (has) P.q[o] = ldv(P.q + o) + acc;
+            }
             sync(it);
         }
         // ---------------- alpha = rz / p^T q
@@ -253,16 +285,66 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
     std::vector<char> buf;
     std::vector<size_t> fix;
     std::vector<BasisItem> upf, dnf;
+    // ---- identity levels (bitwise-equal fusion of their gathers / scatters; see PcgPlan)
+    int nid = 0;
+    for (int lk = 1; lk < L - 1 && !getenv("SPD_PCG_NOFUSE"); ++lk) {
+        const H2Level& lv = A->lv[lk];
+        bool idl = true;
+        for (int a = 0; a < lv.count && idl; ++a) idl = lv.rank[a] == lv.ncand[a];
+        if (!idl) break;
+        nid = lk;
+    }
+    if (nid > PK_MAXID) nid = PK_MAXID;
+    std::vector<int> idb_h, ida_h, comp_h;
+    std::vector<int64_t> comp_off;
+    if (nid) {
+        std::vector<std::vector<int>> bmap(nid + 1);
+        P.id_beg[0] = 0;
+        for (int lk = 1; lk <= nid + 1; ++lk) {
+            const H2Level& lv = A->lv[lk];
+            const std::vector<int> piv = lv.piv.download(s);
+            if (lk <= nid) bmap[lk].assign(std::max<int64_t>(0, lv.S), -1);
+            if (lk == nid + 1) comp_off.assign(lv.count + 1, 0);
+            for (int a = 0; a < lv.count; ++a) {
+                const int i = lv.first + a, sr = lv.rank[a], nc = lv.ncand[a];
+                auto cand_row = [&](int e) -> int {      // row of x behind candidate e of node a
+                    if (lk == 1) return (int)(t.begin[i] + e);
+                    const H2Level& pv = A->lv[lk - 1];
+                    return bmap[lk - 1][pv.off[2 * i + 1 - pv.first] + e];
+                };
+                if (lk <= nid) {
+                    for (int k = 0; k < sr; ++k) bmap[lk][lv.off[a] + k] = cand_row(piv[lv.piv_off[a] + k]);
+                } else {
+                    comp_off[a + 1] = comp_off[a] + (sr ? nc : 0);
+                    if (sr)
+                        for (int k = 0; k < nc; ++k) comp_h.push_back(cand_row(piv[lv.piv_off[a] + k]));
+                }
+            }
+            if (lk <= nid) {
+                idb_h.insert(idb_h.end(), bmap[lk].begin(), bmap[lk].end());
+                P.id_beg[lk] = (int)idb_h.size();
+                P.id_xh[lk - 1] = xh[lk];
+                P.id_yh[lk - 1] = yh[lk];
+            }
+        }
+        ida_h.assign((size_t)nid * A->N, -1);
+        for (int lk = 1; lk <= nid; ++lk)
+            for (size_t e = 0; e < bmap[lk].size(); ++e)
+                if (bmap[lk][e] >= 0) ida_h[(size_t)(lk - 1) * A->N + bmap[lk][e]] = (int)e;
+    }
+    P.nid = nid;
+    P.id_tot = (int)idb_h.size();
     P.nup = 0;
     P.up_off[0] = 0;
-    for (int lk = 1; lk < L; ++lk) {
+    for (int lk = nid + 1; lk < L; ++lk) {
         if (up[lk].empty()) continue;
         upf.insert(upf.end(), up[lk].begin(), up[lk].end());
         P.up_off[++P.nup] = (int)upf.size();
     }
+    if (nid && P.nup == 0) { P.nup = 1; P.up_off[1] = 0; }   // a phase for the gathers alone
     P.ndn = 0;
     P.dn_off[0] = 0;
-    for (int lk = L - 1; lk >= 1; --lk) {
+    for (int lk = L - 1; lk >= nid + 1; --lk) {
         if (dn[lk].empty()) continue;
         dnf.insert(dnf.end(), dn[lk].begin(), dn[lk].end());
         P.dn_off[++P.ndn] = (int)dnf.size();
@@ -291,13 +373,30 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
         P.hs_cta[P.nhs] = (!hss_phase_uses_warps(ph.mode, ph.items.size(), nsm_dev) || getenv("SPD_HSS_CTA")) ? 1 : 0;
         P.hs_off[++P.nhs] = (int)hsi.size();
     }
+    const int* idb_rel = put(buf, idb_h, fix);
+    const int* ida_rel = put(buf, ida_h, fix);
+    const int* comp_rel = put(buf, comp_h, fix);
     const BasisItem* up_rel = put(buf, upf, fix);
     const BasisItem* dn_rel = put(buf, dnf, fix);
     const HsNode* hs_rel = put(buf, hsf, fix);
     const HsItem* hsi_rel = put(buf, hsi, fix);
     im->arena.alloc(std::max<size_t>(1, buf.size()));
+    if (nid && !up[nid + 1].empty()) {
+        // level nid + 1 reads p directly: its pivots composed with the identity levels' maps
+        const H2Level& lv = A->lv[nid + 1];
+        std::unordered_map<int64_t, int> node_of;
+        for (int a = 0; a < lv.count; ++a) node_of[lv.piv_off[a]] = a;
+        BasisItem* items = (BasisItem*)(buf.data() + (uintptr_t)up_rel);
+        for (int w = 0; w < P.up_off[1]; ++w) {
+            const int a = node_of.at((int64_t)(items[w].piv - lv.piv.p));
+            items[w].in = p;
+            items[w].piv = (const int*)(im->arena.p + (uintptr_t)comp_rel) + comp_off[a];
+        }
+    }
     SPD_CUDA(cudaMemcpyAsync(im->arena.p, buf.data(), buf.size(), cudaMemcpyHostToDevice, s));
     P.up = (const BasisItem*)(im->arena.p + (uintptr_t)up_rel);
+    P.idb = (const int*)(im->arena.p + (uintptr_t)idb_rel);
+    P.ida = (const int*)(im->arena.p + (uintptr_t)ida_rel);
     P.dn = (const BasisItem*)(im->arena.p + (uintptr_t)dn_rel);
     P.hs = (const HsNode*)(im->arena.p + (uintptr_t)hs_rel);
     P.hsi = (const HsItem*)(im->arena.p + (uintptr_t)hsi_rel);
