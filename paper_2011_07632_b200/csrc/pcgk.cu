@@ -147,25 +147,25 @@ __global__ void __launch_bounds__(PH_T, EVAL ? 1 : PCG_CTAS) pcg_persistent_kern
             for (int w = P.dn_off[l] + blockIdx.x; w < P.dn_off[l + 1]; w += gridDim.x) basis_down_item(P.dn[w], sm);
             sync(it);
         }
-        if (P.nid) {
-            for (int64_t o = i0; o < N; o += stride) {
-                double acc = 0.0;
-                bool has = false;
-                for (int lv = P.nid - 1; lv >= 0; --lv) {
-                    const int a = P.ida[(size_t)lv * N + o];
-                    if (a < 0) continue;
-                    const double v = ldv(P.id_yh[lv] + a);
-                    acc = has ? v + acc : v;
-                    has = true;
-                }
-                if (has) P.q[o] = ldv(P.q + o) + acc;
-            }
-            sync(it);
-        }
-        // ---------------- alpha = rz / p^T q
+        // ---------------- identity-level scatters (fused) and alpha = rz / p^T q
         {
             double s = 0.0;
-            for (int64_t i = i0; i < N; i += stride) s += ldv(P.p + i) * ldv(P.q + i);
+            for (int64_t o = i0; o < N; o += stride) {
+                double qo = ldv(P.q + o);
+                if (P.nid) {
+                    double acc = 0.0;
+                    bool has = false;
+                    for (int lv = P.nid - 1; lv >= 0; --lv) {
+                        const int a = P.ida[(size_t)lv * N + o];
+                        if (a < 0) continue;
+                        const double v = ldv(P.id_yh[lv] + a);
+                        acc = has ? v + acc : v;
+                        has = true;
+                    }
+                    if (has) { qo = qo + acc; P.q[o] = qo; }
+                }
+                s += ldv(P.p + o) * qo;
+            }
             s = cta_sum(s, red);
             if (threadIdx.x == 0) part_pq[blockIdx.x] = s;
         }
