@@ -439,9 +439,12 @@ static void build_top_operator(spd_hss_s* H, cudaStream_t s) {
     const int L = H->h2->tree.L;
     H->gt_level = 0;
     if (L < 2 || getenv("SPD_NO_GTOP")) return;
+    // largest dense top operator: one GEMV over R_t x R_t replaces 2 (L - t) latency-bound
+    // solve phases; SPD_GTOP_MAX overrides (measured: 3072 vs 4096 at C2 in DESIGN.md)
+    const int64_t gt_max = getenv("SPD_GTOP_MAX") ? atoll(getenv("SPD_GTOP_MAX")) : 3072;
     int t = 0;
     for (int l = 1; l < L; ++l)
-        if (H->lv[l].R <= 3072) { t = l; break; }
+        if (H->lv[l].R <= gt_max) { t = l; break; }
     if (t == 0 || H->lv[t].R == 0) return;
     const int64_t R = H->lv[t].R;
     const int k = (int)R;
