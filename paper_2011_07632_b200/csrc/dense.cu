@@ -1102,35 +1102,27 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
 
 void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
     if (d.empty()) return;
+    // Panels are taken in pairs A = [p, p + 32), B = [p + 32, p + 64): A is factored, its
+    // reflectors update B's columns only, B is factored, and the rest of the trailing
+    // matrix gets ONE update with the combined 64-column compact-WY factor
+    //   I - [V_A V_B] [T_A, -T_A (V_A^T V_B) T_B; 0, T_B] [V_A V_B]^T
+    // (Schreiber-Van Loan), halving the trailing-matrix traffic of the 32-wide scheme.
+    constexpr int QB2 = 2 * QB;
     int nmax = 0;
     size_t vtot = 0, wtot = 0;
     std::vector<size_t> voff(d.size()), woff(d.size());
     for (size_t i = 0; i < d.size(); ++i) {
         nmax = std::max(nmax, d[i].n);
-        voff[i] = vtot; vtot += (size_t)d[i].m * QB;
-        woff[i] = wtot; wtot += (size_t)QB * d[i].n;
+        voff[i] = vtot; vtot += (size_t)d[i].m * QB2;
+        woff[i] = wtot; wtot += (size_t)QB2 * d[i].n;
     }
-    DBuf<double> V(vtot), T(d.size() * QB * QB), W(wtot), W2(wtot);
+    const size_t nd = d.size();
+    DBuf<double> V(vtot), TA(nd * QB * QB), TB(nd * QB * QB), TAB(nd * QB2 * QB2), S(nd * QB * QB),
+        X(nd * QB * QB), W(wtot), W2(wtot);
     double fl = 0;
     for (auto& q : d) fl += 2.0 * q.m * q.n * q.n - 2.0 / 3.0 * q.n * q.n * q.n;
-    for (int p = 0; p < nmax; p += QB) {
-        std::vector<PanelDesc> pd;
-        std::vector<GemmDesc> g1, g2, g3;
-        for (size_t i = 0; i < d.size(); ++i) {
-            const QrDesc& q = d[i];
-            if (p >= q.n || p >= q.m) continue;
-            const int jb = std::min(QB, std::min(q.n, q.m) - p);
-            PanelDesc pdsc{q.A, q.m, q.n, q.ld, p, jb, V.p + voff[i], q.m, T.p + i * QB * QB};
-            pd.push_back(pdsc);
-            const int nt = q.n - p - jb, L = q.m - p;
-            if (nt > 0) {
-                double* At = q.A + p + (size_t)(p + jb) * q.ld;
-                // W = V^T A_trail ; W2 = T^T W ; A_trail -= V W2
-                g1.push_back({V.p + voff[i], At, W.p + woff[i], jb, nt, L, q.m, q.ld, QB});
-                g2.push_back({T.p + i * QB * QB, W.p + woff[i], W2.p + woff[i], jb, nt, jb, QB, QB, QB});
-                g3.push_back({V.p + voff[i], W2.p + woff[i], At, L, nt, jb, q.m, QB, q.ld});
-            }
-        }
+    auto launch_panels = [&](const std::vector<PanelDesc>& pd, int p) {
+        if (pd.empty()) return;
         {
             DevArray<PanelDesc> dp(s, pd);
             double pb = 0;
@@ -1176,6 +1168,63 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
                 SPD_LAUNCH();
             }
         }
+    };
+    for (int p = 0; p < nmax; p += QB2) {
+        V.zero(s);                                    // V_B's rows above its panel must be 0
+        TAB.zero(s);
+        std::vector<PanelDesc> pa, pb;
+        std::vector<GemmDesc> n1, n2, n3, gs, gx, gt, g1, g2, g3;
+        std::vector<CopyDesc> cp;
+        std::vector<int> jbA(nd, 0), jbB(nd, 0);
+        for (size_t i = 0; i < nd; ++i) {
+            const QrDesc& q = d[i];
+            const int kk = std::min(q.n, q.m);
+            if (p >= kk) continue;
+            jbA[i] = std::min(QB, kk - p);
+            jbB[i] = jbA[i] == QB ? std::max(0, std::min(QB, kk - p - QB)) : 0;
+            pa.push_back({q.A, q.m, q.n, q.ld, p, jbA[i], V.p + voff[i], q.m, TA.p + i * QB * QB});
+            const int L = q.m - p;
+            const int pB = p + jbA[i];
+            const int nbB = std::min(QB, q.n - pB);     // B's columns (also when B is not factored)
+            if (nbB > 0) {                              // B columns -= V_A T_A^T V_A^T B
+                double* Ab = q.A + p + (size_t)pB * q.ld;
+                n1.push_back({V.p + voff[i], Ab, W.p + woff[i], jbA[i], nbB, L, q.m, q.ld, QB2});
+                n2.push_back({TA.p + i * QB * QB, W.p + woff[i], W2.p + woff[i], jbA[i], nbB, jbA[i], QB, QB2, QB2});
+                n3.push_back({V.p + voff[i], W2.p + woff[i], Ab, L, nbB, jbA[i], q.m, QB2, q.ld});
+            }
+            if (jbB[i] > 0)
+                pb.push_back({q.A, q.m, q.n, q.ld, pB, jbB[i], V.p + voff[i] + (size_t)QB * q.m + QB, q.m,
+                              TB.p + i * QB * QB});
+            const int pf = pB + nbB, nt = q.n - pf;     // far columns
+            if (nt <= 0) continue;
+            double* Af = q.A + p + (size_t)pf * q.ld;
+            const int K = jbA[i] + jbB[i];
+            if (jbB[i] > 0) {                           // T_AB from T_A, T_B, V_A^T V_B
+                gs.push_back({V.p + voff[i], V.p + voff[i] + (size_t)QB * q.m, S.p + i * QB * QB, QB, jbB[i], L,
+                              q.m, q.m, QB});
+                gx.push_back({TA.p + i * QB * QB, S.p + i * QB * QB, X.p + i * QB * QB, QB, jbB[i], QB, QB, QB, QB});
+                gt.push_back({X.p + i * QB * QB, TB.p + i * QB * QB, TAB.p + i * QB2 * QB2 + (size_t)QB * QB2, QB,
+                              jbB[i], jbB[i], QB, QB, QB2});
+                cp.push_back({TA.p + i * QB * QB, TAB.p + i * QB2 * QB2, QB, QB, QB, QB2, 0});
+                cp.push_back({TB.p + i * QB * QB, TAB.p + i * QB2 * QB2 + QB + (size_t)QB * QB2, jbB[i], jbB[i], QB,
+                              QB2, 0});
+            } else {
+                cp.push_back({TA.p + i * QB * QB, TAB.p + i * QB2 * QB2, jbA[i], jbA[i], QB, QB2, 0});
+            }
+            // W = V^T A_far ; W2 = T^T W ; A_far -= V W2   (K = 64 combined, or A alone)
+            g1.push_back({V.p + voff[i], Af, W.p + woff[i], K, nt, L, q.m, q.ld, QB2});
+            g2.push_back({TAB.p + i * QB2 * QB2, W.p + woff[i], W2.p + woff[i], K, nt, K, QB2, QB2, QB2});
+            g3.push_back({V.p + voff[i], W2.p + woff[i], Af, L, nt, K, q.m, QB2, q.ld});
+        }
+        launch_panels(pa, p);
+        gemm_batched(s, n1, true, false, 1.0, 0.0);
+        gemm_batched(s, n2, true, false, 1.0, 0.0);
+        gemm_batched(s, n3, false, false, -1.0, 1.0);
+        launch_panels(pb, p + QB);
+        gemm_batched(s, gs, true, false, 1.0, 0.0);
+        gemm_batched(s, gx, false, false, 1.0, 0.0);
+        gemm_batched(s, gt, false, false, -1.0, 0.0);
+        copy_batched(s, cp, 1.0, false);
         gemm_batched(s, g1, true, false, 1.0, 0.0);
         gemm_batched(s, g2, true, false, 1.0, 0.0);
         gemm_batched(s, g3, false, false, -1.0, 1.0);
