@@ -316,7 +316,7 @@ def run_ours(args):
     # ---------------- H2 multi-vector sweep over BASELINE C5's widths k in {1, 16, 64, 256}
     # on this workload's H2 (after the timed region; 3 timed products per k after one warm-up)
     sweep = {}
-    _, h_sw, _ = step(pts, b)
+    _, h_sw, H_sw = step(pts, b)
     fp64_pk = load_peaks().get("fp64_dgemm_tflops_sustained") or load_peaks().get("fp64_dgemm_tflops") or 35.5
     for kk in (1, 16, 64, 256):
         Vk = torch.tensor(np.asfortranarray(synth.multivec(N, kk)).T.copy(), device="cuda").t()
@@ -333,7 +333,44 @@ def run_ours(args):
         sweep[str(kk)] = {"ms": round(ms, 3), "useful_tflops": round(fl / ms / 1e9, 2),
                           "frac_fp64_peak": round(fl / ms / 1e9 / fp64_pk, 3)}
         del Vk
-    del h_sw
+    # HSS error metric (the paper's Fig. 5 quantity P:1196-1206): mean over 10
+    # Gaussian probes of ||H x - A_h2 x|| / ||A_h2 x||, H the SPD-HSS matrix (hss_matvec)
+    Pr = torch.tensor(np.asfortranarray(np.random.default_rng(4000).standard_normal((N, 10))).T.copy(),
+                      device="cuda").t()
+    Ax = spd.h2_matvec(h_sw, Pr)
+    Hx = spd.hss_matvec(H_sw, Pr)
+    hss_err = float(((Hx - Ax).norm(dim=0) / Ax.norm(dim=0)).mean())
+    # single-vector HSS solve (the PCG preconditioner), algorithmic bytes = the factors read
+    # once: sum over nodes of 8 (m^2/2 + m r) (leaf m = n_i, nonleaf m = r_c1 + r_c2)
+    hr = H_sw.ranks().astype(np.int64)
+    nodes = h_sw.nodes()
+    Lh = h_sw.levels
+    hb = 0.0
+    for i in range(len(hr)):
+        depth = int(np.floor(np.log2(i + 1)))
+        lev = Lh - depth
+        if lev == Lh:
+            m = int(hr[1] + hr[2]) if len(hr) > 2 else int(nodes[0, 1] - nodes[0, 0])
+            hb += 8.0 * m * m / 2
+            continue
+        m = int(nodes[i, 1] - nodes[i, 0]) if lev == 1 else int(hr[2 * i + 1] + hr[2 * i + 2])
+        hb += 8.0 * (m * m / 2 + m * int(hr[i]))
+    bt = b.clone()
+    for _ in range(3):
+        spd.hss_solve(H_sw, bt, layout=1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(20):
+        spd.hss_solve(H_sw, bt, layout=1)
+    e1.record(stream)
+    e1.synchronize()
+    hs_us = e0.elapsed_time(e1) / 20 * 1e3
+    hss_solve_info = {"us": round(hs_us, 1), "algorithmic_mb": round(hb / 1e6, 1),
+                      "gbs": round(hb / hs_us / 1e3, 1),
+                      "frac_hbm": round(hb / hs_us / 1e3 / load_peaks().get("hbm_gbs", 6546.2), 3),
+                      "note": "standalone solve (one launch per level); inside PCG the same phases run in the persistent kernel"}
+    del h_sw, H_sw, Pr, Ax, Hx
     # ---------------- profiled pass (same steps, per-kernel-class CUDA events on the
     # launching streams; kept out of the timed region because the per-launch event
     # pairs and their host-side drains perturb the step time)
@@ -406,6 +443,8 @@ def run_ours(args):
                         "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
         "roofline": roof,
         "h2_multivector_sweep": sweep,
+        "hss_error_o11": round(hss_err, 6),
+        "hss_solve": hss_solve_info,
         "h2_multivector": {"k": MV_K, "useful_gflop": round(record_flops["flops"] / 1e9, 2),
                            "gflops": round(record_flops["flops"] / mv / 1e9, 1),
                            "frac_fp64_peak": round(record_flops["flops"] / mv / 1e12 / fp64, 4),

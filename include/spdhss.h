@@ -74,6 +74,7 @@ typedef struct {
     int converged;           /* 1 if ||r_k|| <= tol ||b||                 */
     double relres;           /* recursively updated relative residual     */
     double seconds;          /* wall time of the solve (host clock)       */
+    double relres_true;      /* ||b - A x|| / ||b|| with the H2 operator, after the last iteration */
 } spd_pcg_report;
 
 /* Communicator for multi-GPU runs (NCCL over NVLink/NVSwitch,
@@ -154,6 +155,14 @@ spd_status spdhss_build_adaptive(spd_h2_t h, int r0, int r_max, double rel_tol, 
  * R12 (the "ULV-style" solve of PAPER.md P:1119-1123), nrhs columns. */
 spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, double* X,
                      int64_t ldx, int64_t nrhs, void* stream);
+
+/* hss_matvec: Y = H X with the SPD-HSS matrix itself (the nested representation of
+ * Alg. 4: leaf D_i = A_ii, U_i = S_i V_i, transfers R_i, sibling couplings B),
+ * e.g. for the paper's approximation error ||H x - A x|| / ||A x|| (Fig. 5).
+ *   X, Y  device, n x k column-major (ld >= n), layout as for hss_solve; Y overwritten.
+ * Errors: SPD_EINVAL (bad layout / ld / null), SPD_ECUDA. */
+spd_status hss_matvec(spd_hss_t H, int layout, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t k,
+                      void* stream);
 
 /* pcg_solve: (K + shift I) x = b by PCG with H2 matvecs, preconditioner
  * M = the SPD HSS (hss_solve) or none (M == NULL).  x holds x0 = 0 on output the

@@ -45,7 +45,7 @@ class _H2Opts(ctypes.Structure):
 
 class PcgReport(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int), ("converged", ctypes.c_int),
-                ("relres", ctypes.c_double), ("seconds", ctypes.c_double)]
+                ("relres", ctypes.c_double), ("seconds", ctypes.c_double), ("relres_true", ctypes.c_double)]
 
 
 _lib = None
@@ -72,6 +72,7 @@ def lib():
         "h2_matvec": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
         "spdhss_build": ([vp, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp)], c_int),
         "hss_solve": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
+        "hss_matvec": ([vp, c_int, vp, i64, vp, i64, i64, vp], c_int),
         "pcg_solve": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
         "pcg_solve_bj": ([vp, vp, c_int, vp, vp, c_double, c_int, P(PcgReport), vp], c_int),
         "spdhss_build_adaptive": ([vp, c_int, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp), P(c_int)], c_int),
@@ -100,7 +101,7 @@ def lib():
 
 
 EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_init_host", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
-            "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error"]
+            "hss_matvec", "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error"]
 
 
 def _check(status):
@@ -403,6 +404,16 @@ def hss_solve(hss, B, layout=LAYOUT_ORIGINAL, out=None):
         out = empty_colmajor(hss.h2.n, k) if B.dim() == 2 else B.new_empty(B.shape)
     x, ldx, _ = _mat(out, "out")
     _check(lib().hss_solve(hss.ptr, layout, b, ldb, x, ldx, k, _stream()))
+    return out
+
+
+def hss_matvec(hss, X, layout=LAYOUT_ORIGINAL, out=None):
+    """Y = H X with the SPD-HSS matrix (not its inverse)."""
+    x, ldx, k = _mat(X, "X")
+    if out is None:
+        out = empty_colmajor(hss.h2.n, k) if X.dim() == 2 else X.new_empty(X.shape)
+    y, ldy, _ = _mat(out, "out")
+    _check(lib().hss_matvec(hss.ptr, layout, x, ldx, y, ldy, k, _stream()))
     return out
 
 

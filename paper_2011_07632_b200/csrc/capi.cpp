@@ -184,6 +184,29 @@ spd_status hss_solve(spd_hss_t H, int layout, const double* B, int64_t ldb, doub
     })
 }
 
+spd_status hss_matvec(spd_hss_t H, int layout, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t k,
+                      void* stream) {
+    SPD_TRY({
+        AllocStreamScope alloc_scope_((cudaStream_t)stream);
+        SPD_REQUIRE(H != nullptr, "hss_matvec: null handle");
+        SPD_REQUIRE(layout == SPD_LAYOUT_ORIGINAL || layout == SPD_LAYOUT_TREE, "hss_matvec: bad layout");
+        const int64_t N = H->h2->N;
+        SPD_REQUIRE(k >= 0 && ldx >= N && ldy >= N, "hss_matvec: ld must be >= n");
+        SPD_REQUIRE(k <= (1 << 20), "hss_matvec: k too large");
+        if (k == 0) return SPD_OK;
+        SPD_REQUIRE(X != nullptr && Y != nullptr, "hss_matvec: null X or Y");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (layout == SPD_LAYOUT_TREE) {
+            hss_apply_tree(H, X, ldx, Y, ldy, (int)k, s);
+        } else {
+            DBuf<double> xt((size_t)N * k), yt((size_t)N * k);
+            permute_rows(s, H->h2->perm.p, N, (int)k, X, ldx, xt.p, N, true);
+            hss_apply_tree(H, xt.p, N, yt.p, N, (int)k, s);
+            permute_rows(s, H->h2->perm.p, N, (int)k, yt.p, N, Y, ldy, false);
+        }
+    })
+}
+
 static spd_status pcg_common(spd_h2_t A, spd_hss_t M, int precond, int layout, const double* b, double* x,
                              double tol, int maxit, spd_pcg_report* rep, void* stream) {
     spd_pcg_report local{};

@@ -62,6 +62,8 @@ void hss_build_impl(spd_hss_s* H, const double* omega, uint64_t seed, cudaStream
 void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
                    const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s);
 void hss_solve_tree(spd_hss_s* H, const double* b, int64_t ldb, double* x, int64_t ldx, int k, cudaStream_t s);
+// y = H x, the SPD-HSS matrix itself (tree order; x, y N x k, ld >= N; y overwritten)
+void hss_apply_tree(spd_hss_s* H, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s);
 void hss_query(const spd_hss_s* H, int what, void* buf, size_t bytes);
 // precond: PC_HSS (the SPD-HSS solve), PC_BJ (block Jacobi from its leaf factors); M == nullptr: none
 enum { PC_HSS = 0, PC_BJ = 1 };

@@ -58,6 +58,15 @@ __global__ void __launch_bounds__(RED_THREADS) update_xr_kernel(double* x, doubl
     s = block_reduce(s);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
+__global__ void __launch_bounds__(RED_THREADS) resid_kernel(const double* b, const double* q, int64_t n, double* partial) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < n; i += (int64_t)RED_BLOCKS * RED_THREADS) {
+        const double r = b[i] - q[i];
+        s += r * r;
+    }
+    s = block_reduce(s);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
 __global__ void update_p_kernel(double* p, const double* z, const double* scal, int64_t n) {
     const double beta = scal[S_BETA];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -164,8 +173,20 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
     SPD_CUDA(cudaMemcpyAsync(hs, w.scal.p, sizeof(double) * S_NSCAL, cudaMemcpyDeviceToHost, s));
     SPD_CUDA(cudaStreamSynchronize(s));
     const double nb = std::sqrt(hs[S_RR]);
-    rep->iters = 0; rep->converged = 0; rep->relres = 1.0; rep->seconds = 0.0;
-    if (nb == 0.0) { rep->converged = 1; rep->relres = 0.0; return; }
+    rep->iters = 0; rep->converged = 0; rep->relres = 1.0; rep->seconds = 0.0; rep->relres_true = 1.0;
+    if (nb == 0.0) { rep->converged = 1; rep->relres = 0.0; rep->relres_true = 0.0; return; }
+    // true residual ||b - A x|| / ||b|| after the solve (one more H2 product)
+    auto true_residual = [&]() {
+        h2_apply_tree(A, x, N, w.q.p, N, 1, s, comm_real(A->comm));
+        resid_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(b, w.q.p, N, w.partial.p);
+        SPD_LAUNCH();
+        finish_kernel<<<1, RED_THREADS, 0, s>>>(w.partial.p, w.scal.p, S_PQ, 0);
+        SPD_LAUNCH();
+        double v = 0.0;
+        SPD_CUDA(cudaMemcpyAsync(&v, w.scal.p + S_PQ, sizeof(double), cudaMemcpyDeviceToHost, s));
+        SPD_CUDA(cudaStreamSynchronize(s));
+        rep->relres_true = std::sqrt(v) / nb;
+    };
     // z = M r, p = z, rz = r^T z
     if (M && precond == PC_BJ) hss_solve_tree(M, w.r.p, N, w.z.p, N, 1, s);   // allocates the solve workspace
     apply_precond(M, precond, w, N, s);
@@ -193,6 +214,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
             rep->converged = out[2] != 0.0;
             if (out[3] == 1.0) throw Error(SPD_ENOTPD, "PCG breakdown: p^T A p <= 0");
             if (out[3] == 2.0) throw Error(SPD_ENOTPD, "PCG breakdown: r^T M^{-1} r <= 0");
+            true_residual();
             rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             return;
         }
@@ -244,6 +266,7 @@ void pcg_tree(spd_h2_s* A, spd_hss_s* M, const double* b, double* x, double tol,
         if (rep->relres <= tol) { rep->converged = 1; break; }
         if (!(hs[S_RZNEW] > 0.0)) throw Error(SPD_ENOTPD, "PCG breakdown: r^T M^{-1} r = " + std::to_string(hs[S_RZNEW]));
     }
+    true_residual();
     rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 

@@ -808,6 +808,100 @@ void hss_build_impl(spd_hss_s* H, const double* omega_in, uint64_t seed, cudaStr
     H->timings[3] = now_s() - t0;
 }
 
+// ================================================================= forward product y = H x
+// The HSS matrix of Alg. 4 in nested form (the representation hss_export
+// writes): leaf D_i = S_i S_i^T (= A_ii), U_i = S_i V_i; nonleaf transfer R_i (Rt); sibling
+// couplings B_{c1 c2}.  Up:  t_i = S_i^T x_i, xh_i = V_i^T t_i (leaf), xh_p = R_p^T [xh_c1; xh_c2];
+// couple: yh_c1 += B xh_c2, yh_c2 += B^T xh_c1 (every parent, root included); down:
+// [yh_c1; yh_c2] += R_p yh_p;  leaf: y_i = S_i (t_i + V_i yh_i).  Batched DMMA GEMMs per level.
+void hss_apply_tree(spd_hss_s* H, const double* x, int64_t ldx, double* y, int64_t ldy, int k, cudaStream_t s) {
+    const spd_h2_s* h = H->h2;
+    const TreeH& t = h->tree;
+    const int L = t.L;
+    const int64_t N = h->N;
+    if (L == 1) {                                    // y = S (S^T x)
+        const HssLevel& r = H->lv[1];
+        DBuf<double> tt((size_t)N * k);
+        gemm_batched(s, {{r.F.p, x, tt.p, (int)N, k, (int)N, (int)N, (int)ldx, (int)N}}, true, false, 1.0, 0.0);
+        gemm_batched(s, {{r.F.p, tt.p, y, (int)N, k, (int)N, (int)N, (int)N, (int)ldy}}, false, false, 1.0, 0.0);
+        return;
+    }
+    const HssLevel& l1 = H->lv[1];
+    DBuf<double> tt((size_t)N * k);
+    std::vector<DBuf<double>> xh(L), yh(L);
+    for (int l = 1; l < L; ++l) {
+        xh[l].alloc((size_t)std::max<int64_t>(1, H->lv[l].R) * k);
+        yh[l].alloc((size_t)std::max<int64_t>(1, H->lv[l].R) * k);
+        yh[l].zero(s);
+    }
+    {   // leaves: t = S^T x, xh = V^T t
+        std::vector<GemmDesc> g1, g2;
+        for (int a = 0; a < l1.count; ++a) {
+            const int m = l1.m[a], r = l1.rank[a];
+            if (!m) continue;
+            const int64_t b0 = t.begin[l1.first + a];
+            g1.push_back({l1.F.p + l1.F_off[a], x + b0, tt.p + b0, m, k, m, m, (int)ldx, (int)N});
+            if (r) g2.push_back({l1.V.p + l1.V_off[a], tt.p + b0, xh[1].p + l1.off[a], r, k, m, m, (int)N, (int)l1.R});
+        }
+        gemm_batched(s, g1, true, false, 1.0, 0.0);
+        gemm_batched(s, g2, true, false, 1.0, 0.0);
+    }
+    for (int l = 2; l < L; ++l) {                   // xh_p = R_p^T [xh_c1; xh_c2]
+        const HssLevel& lv = H->lv[l];
+        const HssLevel& pv = H->lv[l - 1];
+        std::vector<GemmDesc> g;
+        for (int a = 0; a < lv.count; ++a) {
+            const int c1 = 2 * (lv.first + a) + 1 - pv.first;
+            if (!lv.rank[a] || !lv.m[a]) continue;
+            g.push_back({lv.Rt.p + lv.V_off[a], xh[l - 1].p + pv.off[c1], xh[l].p + lv.off[a], lv.rank[a], k, lv.m[a],
+                         lv.m[a], (int)pv.R, (int)lv.R});
+        }
+        gemm_batched(s, g, true, false, 1.0, 0.0);
+    }
+    {   // sibling couplings, all levels (children of every parent, root included)
+        std::vector<GemmDesc> gf, gt;
+        for (int l = 2; l <= L; ++l) {
+            const HssLevel& cv = H->lv[l - 1];
+            for (int p = t.first(l); p < t.first(l) + t.count(l); ++p) {
+                const int c1 = 2 * p + 1, c2 = 2 * p + 2;
+                const int a1 = c1 - cv.first, a2 = c2 - cv.first;
+                const int r1 = cv.rank[a1], r2 = cv.rank[a2];
+                if (!r1 || !r2) continue;
+                bool tr;
+                const double* B = find_B(cv, c1, c2, tr);
+                gf.push_back({B, xh[l - 1].p + cv.off[a2], yh[l - 1].p + cv.off[a1], r1, k, r2, r1, (int)cv.R, (int)cv.R});
+                gt.push_back({B, xh[l - 1].p + cv.off[a1], yh[l - 1].p + cv.off[a2], r2, k, r1, r1, (int)cv.R, (int)cv.R});
+            }
+        }
+        gemm_batched(s, gf, false, false, 1.0, 1.0);
+        gemm_batched(s, gt, true, false, 1.0, 1.0);
+    }
+    for (int l = L - 1; l >= 2; --l) {              // [yh_c1; yh_c2] += R_p yh_p
+        const HssLevel& lv = H->lv[l];
+        const HssLevel& pv = H->lv[l - 1];
+        std::vector<GemmDesc> g;
+        for (int a = 0; a < lv.count; ++a) {
+            const int c1 = 2 * (lv.first + a) + 1 - pv.first;
+            if (!lv.rank[a] || !lv.m[a]) continue;
+            g.push_back({lv.Rt.p + lv.V_off[a], yh[l].p + lv.off[a], yh[l - 1].p + pv.off[c1], lv.m[a], k, lv.rank[a],
+                         lv.m[a], (int)lv.R, (int)pv.R});
+        }
+        gemm_batched(s, g, false, false, 1.0, 1.0);
+    }
+    {   // leaves: t += V yh ; y = S t
+        std::vector<GemmDesc> g1, g2;
+        for (int a = 0; a < l1.count; ++a) {
+            const int m = l1.m[a], r = l1.rank[a];
+            if (!m) continue;
+            const int64_t b0 = t.begin[l1.first + a];
+            if (r) g1.push_back({l1.V.p + l1.V_off[a], yh[1].p + l1.off[a], tt.p + b0, m, k, r, m, (int)l1.R, (int)N});
+            g2.push_back({l1.F.p + l1.F_off[a], tt.p + b0, y + b0, m, k, m, m, (int)N, (int)ldy});
+        }
+        gemm_batched(s, g1, false, false, 1.0, 1.0);
+        gemm_batched(s, g2, false, false, 1.0, 0.0);
+    }
+}
+
 // ================================================================= recursive solve (R12)
 static void ensure_solve_ws(spd_hss_s* H, int k) {
     if (H->ws_k >= k && !H->z.empty()) return;

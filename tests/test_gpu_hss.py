@@ -105,6 +105,22 @@ def test_hss_solve_matches_oracle(spd, name):
         assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("name", list(CASES))
+def test_hss_matvec_matches_oracle_and_inverts(spd, name):
+    """hss_matvec (the HSS matrix itself) against the oracle's product on the
+    exported GPU factors, and hss_solve(hss_matvec(x)) = x."""
+    cfg, X, h, ho, H, Ho, om = built(spd, name)
+    x = synth.multivec(cfg.dofs, 3, seed=13)
+    yg = host(spd.hss_matvec(H, cuda(x)))
+    if ho.tree.L > 1:
+        G = gpu_as_oracle_hss(H, ho)
+        perm = ho.tree.perm
+        yo = np.empty_like(x)
+        yo[perm] = oracle.hss_matvec(G, x[perm])
+        assert rel(yg, yo) <= 1e-12
+    assert rel(host(spd.hss_solve(H, cuda(yg))), x) <= 1e-9
+
+
 def test_gpu_hss_is_spd(spd):
     cfg, X, h, ho, H, Ho, om = built(spd, "C1")
     G = gpu_as_oracle_hss(H, ho)
@@ -127,9 +143,10 @@ def test_pcg_iterations_match_oracle(spd, name):
     xo = np.empty_like(b)
     xo[perm] = xo_t
     assert rel(host(xg), xo) <= 1e-6
-    # true residual through the GPU H2 operator
+    # true residual through the GPU H2 operator, and the report's own
     r = b - host(spd.h2_matvec(h, xg))
     assert np.linalg.norm(r) <= 2 * cfg.pcg_tol * np.linalg.norm(b)
+    assert abs(rep.relres_true - np.linalg.norm(r) / np.linalg.norm(b)) <= 1e-3 * cfg.pcg_tol
 
 
 def test_philox_omega_path(spd):
