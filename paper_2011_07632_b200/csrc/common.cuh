@@ -203,6 +203,7 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
 // compact-WY trailing updates on the DMMA GEMM.
 struct QrDesc { double* A; int m, n, ld; };
 void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d);
+void qr_tall_batched(cudaStream_t s, const std::vector<QrDesc>& d);      // + one-level TSQR for very tall m
 // form Q[:, :r] (m x r, ld ldq) from the reflectors left in A by qrcp
 struct FormQDesc { const double* A; const double* beta; const int* rank; double* Q; int m, n, lda, ldq; };
 void formq_batched(cudaStream_t s, const std::vector<FormQDesc>& d);

@@ -1232,6 +1232,46 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
     SPD_CUDA(cudaStreamSynchronize(s));
 }
 
+// R of tall matrices whose panels do not fit the 16-CTA cluster (m > 16 x 720 rows, e.g.
+// the RPY proxy matrices with 3 dofs per proxy point): one level of TSQR -- row blocks
+// factored separately, then the QR of their stacked triangles.  R is unique up to row
+// signs, which neither the column pivots of the following QRCP nor R11^{-1} R12 see.
+void qr_tall_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
+    constexpr int MAXROWS = 16 * ((180 * 1024) / (QB * (int)sizeof(double)));
+    std::vector<QrDesc> direct, blocks, stacks;
+    struct Big { QrDesc q; int nb; int64_t soff; };
+    std::vector<Big> big;
+    int64_t stot = 0;
+    for (const auto& q : d) {
+        const int nb = ceil_div(q.m, MAXROWS);
+        if (nb <= 1 || (int64_t)nb * q.n > MAXROWS || ceil_div(q.m, nb) < q.n) { direct.push_back(q); continue; }
+        big.push_back({q, nb, stot});
+        stot += (int64_t)nb * q.n * q.n;
+    }
+    if (!direct.empty()) qr_unpivoted_batched(s, direct);
+    if (big.empty()) return;
+    DBuf<double> S(std::max<int64_t>(1, stot));
+    S.zero(s);
+    std::vector<CopyDesc> up, back;
+    std::vector<MatDesc> low;
+    for (const auto& b : big) {
+        const int rb = ceil_div(b.q.m, b.nb), n = b.q.n, ls = b.nb * n;
+        for (int k = 0; k < b.nb; ++k) {
+            const int r0 = k * rb, rows = std::min(rb, b.q.m - r0);
+            blocks.push_back({b.q.A + r0, rows, n, b.q.ld});
+            up.push_back({b.q.A + r0, S.p + b.soff + (int64_t)k * n, n, n, b.q.ld, ls, 0});   // block's R
+            low.push_back({S.p + b.soff + (int64_t)k * n, n, n, ls});
+        }
+        stacks.push_back({S.p + b.soff, ls, n, ls});
+        back.push_back({S.p + b.soff, b.q.A, n, n, ls, b.q.ld, 0});
+    }
+    qr_unpivoted_batched(s, blocks);
+    copy_batched(s, up, 1.0, false);
+    zero_lower_batched(s, low);                      // keep the triangles only
+    qr_unpivoted_batched(s, stacks);
+    copy_batched(s, back, 1.0, false);               // R (upper n x n) back into the top rows
+}
+
 // ================================================================= FORM Q
 __global__ void __launch_bounds__(256) formq_kernel(const FormQDesc* descs) {
     const FormQDesc d = descs[blockIdx.x];

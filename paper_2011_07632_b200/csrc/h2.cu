@@ -352,7 +352,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                         qdesc[q].m = nc;               // QRCP on the n_c x n_c triangle
                     }
                 }
-                qr_unpivoted_batched(s, tall);
+                qr_tall_batched(s, tall);
                 zero_lower_batched(s, tri);
             }
             stage_mark(s, "h2 blocked QR", k);
