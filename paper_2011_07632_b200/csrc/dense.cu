@@ -1237,7 +1237,8 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
 // factored separately, then the QR of their stacked triangles.  R is unique up to row
 // signs, which neither the column pivots of the following QRCP nor R11^{-1} R12 see.
 void qr_tall_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
-    constexpr int MAXROWS = 16 * ((180 * 1024) / (QB * (int)sizeof(double)));
+    static const int MAXROWS = getenv("SPD_TSQR_ROWS") ? atoi(getenv("SPD_TSQR_ROWS"))
+                                                        : 16 * ((180 * 1024) / (QB * (int)sizeof(double)));
     std::vector<QrDesc> direct, blocks, stacks;
     struct Big { QrDesc q; int nb; int64_t soff; };
     std::vector<Big> big;
