@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <thread>
 
 namespace spd {
 
@@ -16,6 +17,18 @@ int TreeH::lca_level(int i, int j) const {
     int lv = level(i);
     while (i != j) { i = (i - 1) / 2; j = (j - 1) / 2; ++lv; }
     return lv;
+}
+
+// run fn(i) for i in [b, e) on up to hardware_concurrency threads (independent items)
+template <class F>
+static void parallel_for(int b, int e, int64_t work, F&& fn) {
+    const int nt = (int)std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), (int64_t)(e - b),
+                                           std::max<int64_t>(1, work / 4096)});
+    if (nt <= 1) { for (int i = b; i < e; ++i) fn(i); return; }
+    std::vector<std::thread> th;
+    for (int q = 0; q < nt; ++q)
+        th.emplace_back([&, q] { for (int i = b + q; i < e; i += nt) fn(i); });
+    for (auto& x : th) x.join();
 }
 
 void build_tree(const double* pts, int64_t N, int d, int leaf, TreeH& t) {
@@ -34,33 +47,42 @@ void build_tree(const double* pts, int64_t N, int d, int leaf, TreeH& t) {
     t.hi.assign((size_t)t.nnodes * d, 0.0);
     t.begin[0] = 0;
     t.end[0] = N;
-    for (int i = 0; i < t.nnodes; ++i) {
-        const int64_t b = t.begin[i], e = t.end[i];
-        for (int a = 0; a < d; ++a) {
-            double lo = INFINITY, hi = -INFINITY;
-            for (int64_t p = b; p < e; ++p) {
-                double x = pts[t.perm[p] * d + a];
-                lo = std::min(lo, x);
-                hi = std::max(hi, x);
+    // level by level (the nodes of a level are independent); a node's split only needs
+    // the SET of its ceil(n/2) smallest points by (coordinate, index), so nth_element
+    // suffices except at the last split level, whose full sort fixes the order of the
+    // points inside each leaf -- the permutation is bit-identical to sorting everywhere
+    for (int dl = 0; dl <= depth; ++dl) {
+        const int first = (1 << dl) - 1, count = 1 << dl;
+        parallel_for(first, first + count, N, [&](int i) {
+            const int64_t b = t.begin[i], e = t.end[i];
+            for (int a = 0; a < d; ++a) {
+                double lo = INFINITY, hi = -INFINITY;
+                for (int64_t p = b; p < e; ++p) {
+                    double x = pts[t.perm[p] * d + a];
+                    lo = std::min(lo, x);
+                    hi = std::max(hi, x);
+                }
+                t.lo[(size_t)i * d + a] = lo;
+                t.hi[(size_t)i * d + a] = hi;
             }
-            t.lo[(size_t)i * d + a] = lo;
-            t.hi[(size_t)i * d + a] = hi;
-        }
-        if (floor_log2((int64_t)i + 1) < depth) {
-            int sd = 0;
-            double best = t.hi[(size_t)i * d] - t.lo[(size_t)i * d];
-            for (int a = 1; a < d; ++a) {
-                double ext = t.hi[(size_t)i * d + a] - t.lo[(size_t)i * d + a];
-                if (ext > best) { best = ext; sd = a; }
+            if (dl < depth) {
+                int sd = 0;
+                double best = t.hi[(size_t)i * d] - t.lo[(size_t)i * d];
+                for (int a = 1; a < d; ++a) {
+                    double ext = t.hi[(size_t)i * d + a] - t.lo[(size_t)i * d + a];
+                    if (ext > best) { best = ext; sd = a; }
+                }
+                auto less = [&](int64_t x, int64_t y) {
+                    double cx = pts[x * d + sd], cy = pts[y * d + sd];
+                    return cx < cy || (cx == cy && x < y);
+                };
+                const int64_t mid = b + (e - b + 1) / 2;
+                if (dl == depth - 1) std::sort(t.perm.begin() + b, t.perm.begin() + e, less);
+                else if (mid < e) std::nth_element(t.perm.begin() + b, t.perm.begin() + mid, t.perm.begin() + e, less);
+                t.begin[2 * i + 1] = b; t.end[2 * i + 1] = mid;
+                t.begin[2 * i + 2] = mid; t.end[2 * i + 2] = e;
             }
-            std::sort(t.perm.begin() + b, t.perm.begin() + e, [&](int64_t x, int64_t y) {
-                double cx = pts[x * d + sd], cy = pts[y * d + sd];
-                return cx < cy || (cx == cy && x < y);
-            });
-            const int64_t mid = b + (e - b + 1) / 2;
-            t.begin[2 * i + 1] = b; t.end[2 * i + 1] = mid;
-            t.begin[2 * i + 2] = mid; t.end[2 * i + 2] = e;
-        }
+        });
     }
 }
 
@@ -89,16 +111,51 @@ void build_lists(const TreeH& t, ListsH& l) {
     l.near.clear();
     l.type1.assign(t.L + 1, {});
     l.type3.assign(t.L + 1, {});
-    std::vector<Pair> stack{{0, 0}};
-    while (!stack.empty()) {
-        auto [i, j] = stack.back();
-        stack.pop_back();
-        const int k = t.level(i);
-        if (i != j && is_far(t, i, j)) { l.type3[k].push_back({i, j}); continue; }
-        if (i != j) l.type1[k].push_back({i, j});
-        if (k == 1) { l.near.push_back({i, j}); continue; }
-        for (int ci = 2 * i + 1; ci <= 2 * i + 2; ++ci)
-            for (int cj = 2 * j + 1; cj <= 2 * j + 2; ++cj) stack.push_back({ci, cj});
+    // breadth-first until there are enough independent pairs, then the subtree
+    // traversals in parallel; every list is sorted at the end, so the visiting order
+    // does not matter (bit-identical lists)
+    struct Out { std::vector<Pair> near; std::vector<std::vector<Pair>> t1, t3; };
+    auto visit = [&](std::vector<Pair> stack, Out& o, size_t stop_at) {
+        std::vector<Pair> frontier;
+        while (!stack.empty()) {
+            auto [i, j] = stack.back();
+            stack.pop_back();
+            const int k = t.level(i);
+            if (i != j && is_far(t, i, j)) { o.t3[k].push_back({i, j}); continue; }
+            if (i != j) o.t1[k].push_back({i, j});
+            if (k == 1) { o.near.push_back({i, j}); continue; }
+            for (int ci = 2 * i + 1; ci <= 2 * i + 2; ++ci)
+                for (int cj = 2 * j + 1; cj <= 2 * j + 2; ++cj) {
+                    if (stop_at && k - 1 <= (int)stop_at) frontier.push_back({ci, cj});
+                    else stack.push_back({ci, cj});
+                }
+        }
+        return frontier;
+    };
+    Out top{{}, std::vector<std::vector<Pair>>(t.L + 1), std::vector<std::vector<Pair>>(t.L + 1)};
+    // pairs below level split_k are handed to the threads
+    const int split_k = std::max(1, t.L - 4);
+    std::vector<Pair> frontier = t.L > 5 ? visit({{0, 0}}, top, (size_t)split_k) : std::vector<Pair>{};
+    if (t.L <= 5) visit({{0, 0}}, top, 0);
+    const int nt = (int)std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), frontier.size()));
+    std::vector<Out> outs(nt, Out{{}, std::vector<std::vector<Pair>>(t.L + 1), std::vector<std::vector<Pair>>(t.L + 1)});
+    {
+        std::vector<std::thread> th;
+        for (int q = 0; q < nt; ++q)
+            th.emplace_back([&, q] {
+                std::vector<Pair> st;
+                for (size_t f = q; f < frontier.size(); f += nt) st.push_back(frontier[f]);
+                visit(std::move(st), outs[q], 0);
+            });
+        for (auto& x : th) x.join();
+    }
+    outs.push_back(std::move(top));
+    for (auto& o : outs) {
+        l.near.insert(l.near.end(), o.near.begin(), o.near.end());
+        for (int k = 0; k <= t.L; ++k) {
+            l.type1[k].insert(l.type1[k].end(), o.t1[k].begin(), o.t1[k].end());
+            l.type3[k].insert(l.type3[k].end(), o.t3[k].begin(), o.t3[k].end());
+        }
     }
     std::sort(l.near.begin(), l.near.end());
     for (int k = 0; k <= t.L; ++k) {
