@@ -192,6 +192,12 @@ static void expand_dofs(TreeH& t, int m) {
     t.N *= m;
 }
 
+struct IntCopy { const int* src; int* dst; int n; };
+__global__ void int_copy_kernel(const IntCopy* __restrict__ d) {
+    const IntCopy c = d[blockIdx.x];
+    for (int i = threadIdx.x; i < c.n; i += blockDim.x) c.dst[i] = c.src[i];
+}
+
 // ================================================================= build
 static double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -427,16 +433,26 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         lv.piv = std::move(piv_d);
         lv.skel.alloc(std::max<int64_t>(1, lv.S));
         lv.skelX.alloc(std::max<int64_t>(1, lv.S * d));
-        for (auto& pe : pend) {
-            const int a = pe.a, sr = lv.rank[a];
-            if (sr == 0) continue;
-            SPD_CUDA(cudaMemcpyAsync(lv.E.p + lv.E_off[a], pe.E.p, sizeof(double) * lv.ncand[a] * sr, cudaMemcpyDeviceToDevice, s));
-            if (lv.ncand[a] > sr)
-                SPD_CUDA(cudaMemcpyAsync(lv.T.p + lv.T_off[a], pe.T.p, sizeof(double) * (lv.ncand[a] - sr) * sr,
-                                         cudaMemcpyDeviceToDevice, s));
-            SPD_CUDA(cudaMemcpyAsync(lv.skel.p + lv.off[a], pe.skel.p, sizeof(int) * sr, cudaMemcpyDeviceToDevice, s));
-            SPD_CUDA(cudaMemcpy2DAsync(lv.skelX.p + lv.off[a], sizeof(double) * lv.S, pe.sx.p, sizeof(double) * sr,
-                                       sizeof(double) * sr, d, cudaMemcpyDeviceToDevice, s));
+        {   // per-node temporaries -> level arrays: two batched launches (not 4 copies per node)
+            std::vector<CopyDesc> cd;
+            std::vector<IntCopy> ic;
+            for (auto& pe : pend) {
+                const int a = pe.a, sr = lv.rank[a];
+                if (sr == 0) continue;
+                const int ne = lv.ncand[a] * sr, nt = (lv.ncand[a] - sr) * sr;
+                cd.push_back({pe.E.p, lv.E.p + lv.E_off[a], ne, 1, ne, ne, 0});
+                if (nt > 0) cd.push_back({pe.T.p, lv.T.p + lv.T_off[a], nt, 1, nt, nt, 0});
+                cd.push_back({pe.sx.p, lv.skelX.p + lv.off[a], sr, d, sr, (int)lv.S, 0});
+                ic.push_back({pe.skel.p, lv.skel.p + lv.off[a], sr});
+            }
+            copy_batched(s, cd, 1.0, false);
+            if (!ic.empty()) {
+                DevArray<IntCopy> di(s, ic);
+                for (size_t off = 0; off < ic.size(); off += 65535) {
+                    int_copy_kernel<<<(unsigned)std::min<size_t>(65535, ic.size() - off), 128, 0, s>>>(di.p + off);
+                    SPD_LAUNCH();
+                }
+            }
         }
         // sharded level: the owners' contiguous node ranges of every level array are
         // broadcast (one NCCL group = an all-gather of variable-size ranges)
