@@ -795,8 +795,114 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
     }
 }
 
+// Small matrices (m n <= ~24k doubles: the SPD-HSS sketches 200 x 110, the leaf-level H2
+// triangles 128 x 128): one CTA per matrix with the matrix in shared memory -- the same
+// Businger-Golub steps (recomputed norms, lowest index on ties), but every step is
+// separated by CTA barriers only, not by group barriers through global memory.
+__global__ void __launch_bounds__(256) qrcp_smem_kernel(const QrcpDesc* __restrict__ descs, double rel_tol) {
+    extern __shared__ double smq[];
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    const QrcpDesc d = descs[blockIdx.x];
+    const int m = d.m, n = d.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double* As = smq;                                // m x n, ld m
+    double* nrm = smq + (size_t)m * n;
+    int* pv = (int*)(nrm + n);
+    for (int e = tid; e < m * n; e += blockDim.x) As[e] = d.A[e % m + (size_t)(e / m) * d.ld];
+    for (int j = tid; j < n; j += blockDim.x) pv[j] = j;
+    __syncthreads();
+    for (int j = warp; j < n; j += nw) {
+        double sacc = 0.0;
+        for (int i = lane; i < m; i += 32) { const double x = As[i + (size_t)j * m]; sacc += x * x; }
+        sacc = warp_sum(sacc);
+        if (lane == 0) nrm[j] = sacc;
+    }
+    __syncthreads();
+    const int kmax = min(min(m, n), d.max_rank);
+    double nu0 = 0.0;
+    int rank = kmax;
+    for (int t = 0; t < kmax; ++t) {
+        double v = -1.0;
+        int idx = 0x7fffffff;
+        for (int j = t + tid; j < n; j += blockDim.x) {
+            const double x = nrm[j];
+            if (x > v) { v = x; idx = j; }             // ascending j: lowest index on ties
+        }
+        double bv;
+        int bi;
+        block_argmax(v, idx, sv, si, bv, bi);
+        const double nu = bv > 0.0 ? sqrt(bv) : 0.0;
+        if (t == 0) nu0 = nu;
+        if (nu == 0.0 || nu <= rel_tol * nu0) { rank = t; break; }
+        const int p = bi;
+        if (p != t) {
+            for (int i = tid; i < m; i += blockDim.x) {
+                const double a = As[i + (size_t)t * m];
+                As[i + (size_t)t * m] = As[i + (size_t)p * m];
+                As[i + (size_t)p * m] = a;
+            }
+            if (tid == 0) {
+                const int tp = pv[t]; pv[t] = pv[p]; pv[p] = tp;
+                const double tn = nrm[t]; nrm[t] = nrm[p]; nrm[p] = tn;
+            }
+        }
+        __syncthreads();
+        double* ct = As + (size_t)t * m;
+        double sig = 0.0;
+        for (int i = t + 1 + tid; i < m; i += blockDim.x) { const double x = ct[i]; sig += x * x; }
+        sig = block_sum(sig, sv);
+        const double x0 = ct[t];
+        double beta, mu, v0;
+        if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
+        else {
+            mu = sqrt(x0 * x0 + sig);
+            v0 = (x0 <= 0.0) ? x0 - mu : -sig / (x0 + mu);
+            beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+        }
+        const double inv0 = 1.0 / v0;
+        for (int i = t + 1 + tid; i < m; i += blockDim.x) ct[i] = (sig == 0.0) ? 0.0 : ct[i] * inv0;
+        __syncthreads();
+        if (tid == 0) { ct[t] = mu; d.beta[t] = beta; }
+        // columns j > t: w = beta v^T a_j (v_t = 1), a_j -= w v, norms over rows > t
+        for (int j = t + 1 + warp; j < n; j += nw) {
+            double* cj = As + (size_t)j * m;
+            double sacc = lane == 0 ? cj[t] : 0.0;
+            for (int i = t + 1 + lane; i < m; i += 32) sacc += ct[i] * cj[i];
+            const double w = beta * warp_sum(sacc);
+            double nn = 0.0;
+            for (int i = t + 1 + lane; i < m; i += 32) { const double a = cj[i] - w * ct[i]; cj[i] = a; nn += a * a; }
+            nn = warp_sum(nn);
+            if (lane == 0) { cj[t] -= w; nrm[j] = nn; }
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < m * n; e += blockDim.x) d.A[e % m + (size_t)(e / m) * d.ld] = As[e];
+    for (int j = tid; j < n; j += blockDim.x) { d.piv[j] = pv[j]; d.norms[j] = nrm[j]; }
+    if (tid == 0) d.rank[0] = rank;
+}
+
 void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol) {
     if (d.empty()) return;
+    {
+        size_t need = 0;
+        for (auto& q : d) need = std::max(need, sizeof(double) * ((size_t)q.m * q.n + q.n) + sizeof(int) * q.n);
+        if (need <= 200 * 1024 && !getenv("SPD_QRCP_GROUP")) {
+            static size_t set = 0;
+            if (need > 48 * 1024 && need > set) {
+                SPD_CUDA(cudaFuncSetAttribute(qrcp_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                set = 200 * 1024;
+            }
+            double fl = 0;
+            for (auto& q : d) fl += 4.0 * q.m * q.n * std::min(std::min(q.m, q.n), q.max_rank);
+            DevArray<QrcpDesc> dd(s, d);
+            ProfScope prof(s, "qrcp", fl, 0);
+            for (size_t off = 0; off < d.size(); off += 65535) {
+                qrcp_smem_kernel<<<(unsigned)std::min<size_t>(65535, d.size() - off), 256, need, s>>>(dd.p + off, rel_tol);
+                SPD_LAUNCH();
+            }
+            return;
+        }
+    }
     int dev = 0;
     SPD_CUDA(cudaGetDevice(&dev));
     int nsm = 0, per_sm = 0;
