@@ -99,7 +99,7 @@ class ClockSampler:
 # ------------------------------------------------------------------ helpers
 def load_traffic(kernel):
     """DRAM traffic of the dominant kernel from the committed ncu capture (or None)."""
-    path = os.path.join(ROOT, "profiles", "r01f_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r01g_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get(kernel)
@@ -419,7 +419,7 @@ def run_ours(args):
         tr = load_traffic(nm)
         if tr and nm == "pcg_persistent":        # per launch: ncu's bytes per PCG iteration x this launch's iterations
             roof["traffic"] = round(tr["bytes_per_iteration"] * statistics.mean(r["pcg_iters"] for r in recs) / 1e9, 2)
-            roof["traffic_unit"] = "GB per launch (ncu dram read+write, profiles/r01f_traffic.json)"
+            roof["traffic_unit"] = "GB per launch (ncu dram read+write, profiles/r01g_traffic.json)"
             roof["algorithmic_gb_per_launch"] = round(p["bytes"] / max(1.0, p["launches"]) / 1e9, 2)
         roof["share_of_step"] = round(p["ms"] * 1e-3 / sum(prof_s), 4)
         roof["measured_in"] = "profiled pass (same steps as the timed region)"
