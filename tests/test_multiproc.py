@@ -42,3 +42,22 @@ def test_max_over_ranks_without_group():
     sys.path.insert(0, ROOT)
     import bench
     assert bench.max_over_ranks(3.0, device="cpu") == 3.0
+
+
+def test_reference_arm_json_contract():
+    """bench.py --impl reference (the CPU oracle timed on a bounded sample): one JSON
+    line with impl, the same metric/unit/direction as our arm, cpu_baseline and an
+    e2e block with zero host<->device bytes (CPU only)."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "s" and d["higher_is_better"] is False
+    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
