@@ -540,6 +540,13 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
 // Multi-vector products read the kernel blocks from the symmetric k = 1 store when it
 // holds them (built on demand like the k = 1 product's; env SPD_MV_EVAL=1: evaluate):
 // no kernel evaluation, the blocks stream from HBM and the DMMA contraction is unchanged.
+// largest store built on demand for products, as a fraction of the free memory (env
+// SPD_STORE_FRAC); the SPD-HSS build that usually follows needs its own workspaces
+static double store_frac_limit() {
+    static const double f = getenv("SPD_STORE_FRAC") ? atof(getenv("SPD_STORE_FRAC")) : 0.5;
+    return f;
+}
+
 bool h2_store_for_products(spd_h2_s* h, cudaStream_t s, bool build) {
     static const bool eval = getenv("SPD_MV_EVAL") != nullptr;
     if (eval || h->tree.L < 2) return false;
@@ -547,7 +554,7 @@ bool h2_store_for_products(spd_h2_s* h, cudaStream_t s, bool build) {
     // built here only when it is small next to the free memory (the SPD-HSS build that
     // usually follows needs its workspaces; PCG builds it within its own budget anyway)
     if (h->sym_need < 0.0) h->sym_need = (double)h2sym_bytes(h);
-    if (!build || h->sym_need > 0.25 * (double)device_free_bytes()) return false;
+    if (!build || h->sym_need > store_frac_limit() * (double)device_free_bytes()) return false;
     if (h->stored_mode == -1) h2_prepare(h, 1, s);
     if (h->stored_mode != 1) return false;
     h2sym_build(h, h->sym_budget, s);
