@@ -63,6 +63,14 @@ typedef enum { SPD_LAYOUT_ORIGINAL = 0, SPD_LAYOUT_TREE = 1 } spd_layout;
 typedef struct {
     int n_proxy;        /* proxy points per node; 0 = 4096 (2D) / 6144 (3D) (reading R3) */
     int reserved;
+    /* Parity hook of the certified-tie protocol (reading R19):
+     * host, nullable.  For every heap node at levels 1..L-1 in heap order: s_i, then the
+     * s_i skeleton TREE POSITIONS in pivot order (s_i = 0 for inactive nodes).  The ID
+     * QRCP of each node then takes these pivots instead of its own (Alg. 2 step 3,
+     * P:827) and stops after s_i steps, so later stages can be compared with another
+     * implementation's (the oracle's) skeletons.  Read during h2_build only.
+     * SPD_EINVAL if a count or position does not fit the tree and the candidates. */
+    const int32_t* inject_skeletons;
 } spd_h2_opts;
 
 typedef struct spd_comm_s* spd_comm_t;

@@ -25,6 +25,9 @@ spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int
 /* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major
  * (d = spatial dimension; for RPY the points, not their 3 dofs each) */
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
+/* the device Omega generator of spdhss_build (Philox4x32-10 + Box-Muller, reading R29):
+ * out (device) n x w column-major, ld n, tree-order element e = row + col n */
+spd_status spd_test_philox_normal(double* out, int64_t n, int w, uint64_t seed, void* stream);
 /* subtree-sharding plan (host logic only, no GPU): owner rank of node a of a level
  * with `count` nodes for nranks ranks, -1 when the level is computed redundantly */
 int spd_test_shard_owner(int nranks, int count, int a);

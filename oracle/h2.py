@@ -113,6 +113,17 @@ class H2:
     E: dict = field(default_factory=dict)      # node -> leaf U_i or nonleaf R_i
     piv: dict = field(default_factory=dict)    # node -> QRCP pivots over candidates
     rank: dict = field(default_factory=dict)
+    blocks: dict = field(default_factory=dict)  # cache of evaluated near / coupling blocks (R21)
+
+    def block(self, key, rows, cols, shift=True):
+        """K(rows, cols) of a near block (key ("n", a, b)) or coupling (("c", i, j)),
+        evaluated once and kept: reading R21 lets the oracle store what the device
+        evaluates on the fly; the entries are the same function of the same points."""
+        B = self.blocks.get(key)
+        if B is None:
+            B = self.K(rows, cols, shift)
+            self.blocks[key] = B
+        return B
 
     def K(self, rows, cols, shift=True):
         return kernel_matrix(self.kid, self.ell, self.Xt[rows], self.Xt[cols],
@@ -177,7 +188,7 @@ def h2_build(X, kid, ell, shift, leaf, tol, n_proxy=0):
     return h
 
 
-def h2_matvec(h: H2, x, exclude_level=0):
+def h2_matvec(h: H2, x, exclude_level=0, reverse=False):
     """y = A x for the H2 matrix A (tree order), x: (N, w).
 
     exclude_level = k > 0 gives the literal Y^(k) = (A - blockdiag_k(A)) x of
@@ -185,6 +196,8 @@ def h2_matvec(h: H2, x, exclude_level=0):
     level-k ancestor (LCA level <= k) is skipped, "just neglecting the block
     diagonal parts during multiplication".
     Up pass / coupling / down pass follow eqn:uniformbasis_h2 + eqn:nested.
+    reverse=True accumulates the near blocks and the couplings in the reverse list
+    order: the same sum in another order (the drift evidence of reading R24).
     """
     t, lists = h.tree, h.lists
     x = np.asarray(x, dtype=np.float64)
@@ -196,11 +209,11 @@ def h2_matvec(h: H2, x, exclude_level=0):
     keep = (lambda i, j: True) if exclude_level <= 0 else \
         (lambda i, j: lists.lca[(i, j)] > exclude_level)
     # near field (dense leaf blocks, shift on the diagonal)
-    for (a, b) in lists.near:
+    for (a, b) in (reversed(lists.near) if reverse else lists.near):
         if keep(a, b):
             ra = np.arange(t.begin[a], t.end[a])
             rb = np.arange(t.begin[b], t.end[b])
-            y[ra] += h.K(ra, rb) @ x[rb]
+            y[ra] += h.block(("n", a, b), ra, rb) @ x[rb]
     # up pass: xh_i = U_i^T x_i (leaf), R_i^T [xh_c1; xh_c2] (nonleaf)
     xh = {}
     for k in range(1, t.L):
@@ -215,9 +228,9 @@ def h2_matvec(h: H2, x, exclude_level=0):
     # coupling: yh_i += K(J_i, J_j) xh_j over Type-3 pairs
     yh = {i: np.zeros((h.rank[i], w)) for i in xh}
     for k in range(1, t.L):
-        for (i, j) in lists.type3[k]:
+        for (i, j) in (reversed(lists.type3[k]) if reverse else lists.type3[k]):
             if keep(i, j):
-                yh[i] += h.K(h.skel[i], h.skel[j], shift=False) @ xh[j]
+                yh[i] += h.block(("c", i, j), h.skel[i], h.skel[j], shift=False) @ xh[j]
     # down pass
     for k in range(t.L - 1, 0, -1):
         for i in t.nodes_at(k):

@@ -91,6 +91,12 @@ def _lib():
                                     ctypes.c_int, ctypes.c_double, P(ctypes.c_int),
                                     P(ctypes.c_double)]
         lib.oracle_qrcp.restype = ctypes.c_int
+        lib.oracle_qrcp_follow.argtypes = [ctypes.c_int, ctypes.c_int, P(ctypes.c_double),
+                                           ctypes.c_int, ctypes.c_double, P(ctypes.c_int),
+                                           P(ctypes.c_double), P(ctypes.c_int), ctypes.c_int,
+                                           P(ctypes.c_double), P(ctypes.c_double),
+                                           P(ctypes.c_double), P(ctypes.c_int)]
+        lib.oracle_qrcp_follow.restype = ctypes.c_int
         _LIB = lib
     return _LIB
 
@@ -120,3 +126,42 @@ def qrcp(A, max_rank, rel_tol, want_q=True):
             v = np.concatenate([[1.0], A[t + 1:, t]])
             Q[t:, :] -= beta[t] * np.outer(v, v @ Q[t:, :])
     return Q, R, piv.astype(np.int64), r
+
+
+def qrcp_trace(A, max_rank, rel_tol, follow=None, runner_up=False):
+    """The QRCP of `qrcp` with its per-step norms recorded (reading R19).
+
+    follow=None: the oracle's own Businger-Golub run.  follow = a pivot sequence of
+    ORIGINAL column indices (another implementation's pivots, length s): step t takes
+    column follow[t] instead of the argmax and the run stops after s steps.
+    Returns (R_r, piv, r, numax, nuf): numax[t] = largest residual column norm at step t
+    (t < r, plus t = r when the run stopped before min(m, n, max_rank) in own mode, or
+    when s < min(m, n, max_rank) in follow mode), nuf[t] = the norm of the column taken.
+    r = -1 if a followed index is not a remaining column."""
+    import ctypes
+    A = np.array(A, dtype=np.float64, order="F", copy=True)
+    m, n = A.shape
+    kmax = max(0, min(m, n, int(max_rank)))
+    piv = np.zeros(n, dtype=np.int32)
+    beta = np.zeros(max(min(m, n), 1))
+    numax = np.full(kmax + 1, np.nan)
+    nuf = np.full(kmax + 1, np.nan)
+    P = ctypes.POINTER
+    if follow is not None:
+        fo = np.ascontiguousarray(np.asarray(follow, dtype=np.int32))
+        fptr, nf = fo.ctypes.data_as(P(ctypes.c_int)), int(fo.size)
+    else:
+        fptr, nf = None, 0
+    nu2 = np.full(kmax + 1, np.nan)
+    idx2 = np.full(kmax + 1, -1, dtype=np.int32)
+    r = _lib().oracle_qrcp_follow(m, n, A.ctypes.data_as(P(ctypes.c_double)), int(max_rank),
+                                  float(rel_tol), piv.ctypes.data_as(P(ctypes.c_int)),
+                                  beta.ctypes.data_as(P(ctypes.c_double)), fptr, nf,
+                                  numax.ctypes.data_as(P(ctypes.c_double)),
+                                  nuf.ctypes.data_as(P(ctypes.c_double)),
+                                  nu2.ctypes.data_as(P(ctypes.c_double)) if runner_up else None,
+                                  idx2.ctypes.data_as(P(ctypes.c_int)) if runner_up else None)
+    R = np.triu(A[:max(r, 0), :])
+    if runner_up:
+        return R, piv.astype(np.int64), r, numax, nuf, nu2, idx2.astype(np.int64)
+    return R, piv.astype(np.int64), r, numax, nuf

@@ -35,8 +35,17 @@ static void house(int len, double *x, double *beta)
     x[0] = mu;
 }
 
-int oracle_qrcp(int m, int n, double *A, int max_rank, double rel_tol,
-                int *piv, double *beta)
+/* Follow mode (certified-tie protocol, reading R19): when follow != NULL the pivot
+ * of step t < nfollow is the column whose ORIGINAL index is follow[t] (the pivots of
+ * another implementation) instead of the argmax, and the factorization stops after
+ * nfollow steps.  In both modes numax[t] (t <= rank, nullable) receives the largest
+ * residual column norm at step t, nuf[t] (nullable) the norm of the column taken, and
+ * nu2[t] / idx2[t] (nullable) the runner-up norm and its original column index;
+ * the arithmetic of a step is the same.  Returns -1 if follow[t] is not a remaining
+ * column. */
+int oracle_qrcp_follow(int m, int n, double *A, int max_rank, double rel_tol,
+                       int *piv, double *beta, const int *follow, int nfollow,
+                       double *numax, double *nuf, double *nu2, int *idx2)
 {
     int kmax = m < n ? m : n;
     if (max_rank < kmax) kmax = max_rank;
@@ -58,7 +67,26 @@ int oracle_qrcp(int m, int n, double *A, int max_rank, double rel_tol,
             if (norms[j] > norms[p]) p = j;          /* strict: lowest index wins ties */
         double nu = norms[p];
         if (t == 0) nu0 = nu;
-        if (nu == 0.0 || nu <= rel_tol * nu0) break;
+        if (numax) numax[t] = nu;
+        if (nu2) {                                   /* runner-up (lowest index on ties) */
+            int q2 = -1;
+            for (int j = t; j < n; ++j)
+                if (j != p && (q2 < 0 || norms[j] > norms[q2])) q2 = j;
+            nu2[t] = q2 < 0 ? -1.0 : norms[q2];
+            if (idx2) idx2[t] = q2 < 0 ? -1 : piv[q2];
+        }
+        if (follow) {
+            if (t >= nfollow) break;
+            int q = -1;
+            for (int j = t; j < n; ++j)
+                if (piv[j] == follow[t]) { q = j; break; }
+            if (q < 0) { r = -1; break; }
+            p = q;
+            if (nuf) nuf[t] = norms[p];
+        } else {
+            if (nuf) nuf[t] = nu;
+            if (nu == 0.0 || nu <= rel_tol * nu0) break;
+        }
         if (p != t) {
             double *a = A + (size_t)t * m, *b = A + (size_t)p * m;
             for (int i = 0; i < m; ++i) { double tmp = a[i]; a[i] = b[i]; b[i] = tmp; }
@@ -83,4 +111,10 @@ int oracle_qrcp(int m, int n, double *A, int max_rank, double rel_tol,
     free(norms);
     free(v);
     return r;
+}
+
+int oracle_qrcp(int m, int n, double *A, int max_rank, double rel_tol,
+                int *piv, double *beta)
+{
+    return oracle_qrcp_follow(m, n, A, max_rank, rel_tol, piv, beta, NULL, 0, NULL, NULL, NULL, NULL);
 }

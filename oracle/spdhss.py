@@ -46,6 +46,7 @@ class HSS:
     PhiU: dict = field(default_factory=dict)     # node -> Phi_i U_i^{H2}
     Phi_leaf: dict = field(default_factory=dict)
     piv: dict = field(default_factory=dict)
+    Lam: dict = field(default_factory=dict)      # node -> the sketch QRCP factored (keep_sketch)
     sketch_widths: list = field(default_factory=list)   # instrumentation
 
     def Bij(self, i, j):
@@ -109,8 +110,10 @@ def special_products(hss: HSS, Yk, k):
     return out
 
 
-def spdhss_build(h2: H2, rank_cap, rel_tol, omega, form="eig"):
-    """Alg. 4.  omega: N x (r+p) in tree order (one for all k, R8)."""
+def spdhss_build(h2: H2, rank_cap, rel_tol, omega, form="eig", keep_sketch=False):
+    """Alg. 4.  omega: N x (r+p) in tree order (one for all k, R8).
+    keep_sketch: keep every node's sketch Lambda (the matrix its QRCP factors) in
+    hss.Lam, for the certified-tie records of reading R19."""
     t, lists = h2.tree, h2.lists
     L = t.L
     hss = HSS(h2, form)
@@ -133,6 +136,8 @@ def spdhss_build(h2: H2, rank_cap, rel_tol, omega, form="eig"):
         Lam = solve_triangular(S, Y[1][rows], lower=True) if len(rows) else Y[1][rows]
         V, _, piv, r = qrcp(Lam, rank_cap, rel_tol)    # Alg. 2 step 3
         hss.V[i], hss.piv[i], hss.rank[i] = V, piv, r
+        if keep_sketch:
+            hss.Lam[i] = Lam
         Phi = solve_triangular(S, V, lower=True, trans='T').T if len(rows) else V.T   # V^T S^{-1}
         hss.Phi_leaf[i] = Phi
         if h2.active[i]:
@@ -164,6 +169,8 @@ def spdhss_build(h2: H2, rank_cap, rel_tol, omega, form="eig"):
         for i in t.nodes_at(k):
             Vb, _, piv, r = qrcp(Lam[i], rank_cap, rel_tol)
             hss.V[i], hss.piv[i], hss.rank[i] = Vb, piv, r
+            if keep_sketch:
+                hss.Lam[i] = Lam[i]
             left = Vb.T @ hss.Finv[i]                  # Vbar^T (I+B)^{-1/2}
             if h2.active[i]:
                 c1, c2 = t.children(i)

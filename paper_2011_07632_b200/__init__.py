@@ -40,7 +40,8 @@ class _Kernel(ctypes.Structure):
 
 
 class _H2Opts(ctypes.Structure):
-    _fields_ = [("n_proxy", ctypes.c_int), ("reserved", ctypes.c_int)]
+    _fields_ = [("n_proxy", ctypes.c_int), ("reserved", ctypes.c_int),
+                ("inject_skeletons", ctypes.POINTER(ctypes.c_int32))]
 
 
 class PcgReport(ctypes.Structure):
@@ -86,6 +87,7 @@ def lib():
         "spd_test_qrcp": ([c_int, vp, c_int, c_int, c_int, i64, c_int, c_double, vp, vp, vp, i64, vp], c_int),
         "spd_test_proxies": ([vp, c_int, vp, vp], c_int),
         "spd_test_qr_unpivoted": ([c_int, vp, c_int, c_int, c_int, i64, vp], c_int),
+        "spd_test_philox_normal": ([vp, i64, c_int, ctypes.c_uint64, vp], c_int),
         "spd_launch_count": ([], ctypes.c_longlong),
         "spd_prof_enable": ([c_int], None),
         "spd_prof_reset": ([], None),
@@ -314,20 +316,41 @@ def shard_owner(nranks, count, a):
     return int(lib().spd_test_shard_owner(int(nranks), int(count), int(a)))
 
 
-def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0, comm=None):
+def h2_build(points, kernel_id, ell, shift, leaf, tol, n_proxy=0, comm=None, inject_skeletons=None):
     """points: CUDA float64 (n, d) row-major, original order.  comm: optional Comm
-    (subtree-sharded build; every rank ends with the full H2)."""
+    (subtree-sharded build; every rank ends with the full H2).  inject_skeletons:
+    optional dict node -> skeleton tree positions in pivot order for every node at
+    levels 1..L-1 (missing nodes: 0), the parity hook of reading R19."""
     if points.dim() != 2 or not points.is_contiguous():
         raise ValueError("points must be a contiguous (n, d) tensor")
     n, d = points.shape
     out = ctypes.c_void_p()
-    opts = _H2Opts(int(n_proxy), 0)
+    opts = _H2Opts(int(n_proxy), 0, None)
+    if inject_skeletons is not None:
+        flat = []
+        depth = 0                                  # tree depth of reading R1
+        while int(leaf) << depth < n:
+            depth += 1
+        L = depth + 1
+        for i in range((1 << L) - 1):
+            if _node_level(i, L) >= L:
+                continue
+            s = [int(v) for v in inject_skeletons.get(i, [])]
+            flat.append(len(s))
+            flat.extend(s)
+        inj = np.ascontiguousarray(np.array(flat + [0], dtype=np.int32))
+        opts.inject_skeletons = inj.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     _check(lib().h2_build(_dptr(points, "points"), n, d, _Kernel(int(kernel_id), float(ell), float(shift)),
                           int(leaf), float(tol), ctypes.byref(opts), comm.ptr if comm is not None else None,
                           _stream(), ctypes.byref(out)))
     h = H2(out, n * (3 if int(kernel_id) == K_RPY else 1), d)      # operator rows (RPY: 3 dofs per point)
     h._comm = comm            # keep the communicator alive as long as the handle
     return h
+
+
+def _node_level(i, L):
+    """Paper level of heap node i in a perfect tree of depth L (root = L, leaves = 1)."""
+    return L - ((i + 1).bit_length() - 1)
 
 
 def h2_matvec(h2, X, layout=LAYOUT_ORIGINAL, out=None):
@@ -365,6 +388,14 @@ class HSS:
 
     def timings(self):
         return self.query(Q_TIMINGS, np.float64, 16)
+
+    def pivots(self, w):
+        """QRCP pivots of every node at levels 1..L-1 in heap order: dict node -> (w,)."""
+        L, nn = self.h2.levels, self.h2.nnodes
+        nodes = [i for i in range(nn) if _node_level(i, L) < L]
+        flat = self.query(Q_HSS_PIVOTS, np.int32, max(1, len(nodes) * w))
+        order = [i for k in range(1, L) for i in nodes if _node_level(i, L) == k]
+        return {i: flat[a * w:(a + 1) * w].astype(np.int64) for a, i in enumerate(order)}
 
     def shard_work(self):
         """(nodes whose per-node work this process computed, nodes with per-node work)."""
@@ -420,10 +451,23 @@ def hss_matvec(hss, X, layout=LAYOUT_ORIGINAL, out=None):
 def pcg_solve(h2, hss, b, tol=1e-8, maxit=3000, layout=LAYOUT_ORIGINAL, x=None, precond="hss"):
     """Returns (x, PcgReport).  hss=None: unpreconditioned CG.  precond="bj": block
     Jacobi from the SPD-HSS leaf factors (the paper's BJ baseline)."""
+    n = h2.n
+    if b.dim() != 1 or not b.is_contiguous() or b.numel() != n:
+        raise ValueError(f"b must be a contiguous 1-D tensor of length n = {n}")
     if x is None:
         x = b.new_zeros(b.shape)
+    if x.dim() != 1 or not x.is_contiguous() or x.numel() != n:
+        raise ValueError(f"x must be a contiguous 1-D tensor of length n = {n}")
     rep = PcgReport()
     fn = lib().pcg_solve_bj if precond == "bj" else lib().pcg_solve
     _check(fn(h2.ptr, hss.ptr if hss is not None else None, layout, _dptr(b, "b"),
               _dptr(x, "x"), float(tol), int(maxit), ctypes.byref(rep), _stream()))
     return x, rep
+
+
+def philox_normal(n, w, seed):
+    """Test export: the device Omega generator of spdhss_build (n x w column-major)."""
+    import torch
+    out = torch.empty((w, n), dtype=torch.float64, device="cuda").t()
+    _check(lib().spd_test_philox_normal(ctypes.c_void_p(out.data_ptr()), int(n), int(w), int(seed), _stream()))
+    return out

@@ -77,6 +77,7 @@ spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf,
         h->kern = k; h->kp = make_kernel(k); h->tol = tol; h->leaf = leaf;
         h->n_proxy = (opts && opts->n_proxy > 0) ? opts->n_proxy : (d == 2 ? 4096 : 6144);
         h->comm = c;
+        h->inject = opts ? opts->inject_skeletons : nullptr;
         try { h2_build_impl(h, pts, (cudaStream_t)stream); }
         catch (...) { delete h; throw; }
         *out = h;
@@ -258,6 +259,7 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
     SPD_TRY({
         SPD_REQUIRE(handle != nullptr && buf != nullptr, "spd_query: null argument");
         if (what >= SPD_Q_HSS_RANKS && what < SPD_Q_TIMINGS) {
+            SPD_REQUIRE(hss_if_hss(handle) != nullptr, "spd_query: HSS query on a non-HSS handle");
             hss_query((const spd_hss_s*)handle, what, buf, bytes);
             return SPD_OK;
         }
@@ -284,7 +286,9 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
             std::memcpy(buf, tm, 16 * sizeof(double));
             return SPD_OK;
         }
+        SPD_REQUIRE(hss_if_hss(handle) == nullptr, "spd_query: H2 query on an HSS handle");
         const spd_h2_s* h = (const spd_h2_s*)handle;
+        SPD_REQUIRE(h->magic == 0x48324832u, "spd_query: not an H2 handle");
         const TreeH& t = h->tree;
         switch (what) {
         case SPD_Q_N: { int64_t v = h->N; std::memcpy(buf, &v, need(bytes, 8)); break; }
@@ -430,6 +434,13 @@ spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) 
         std::vector<double> v = P.download(s);
         for (int p = 0; p < h->n_proxy; ++p)                // the proxy points (first dof of each)
             for (int a = 0; a < h->dim; ++a) P_host[(size_t)p * h->dim + a] = v[(size_t)a * np + (size_t)h->m * p];
+    })
+}
+
+spd_status spd_test_philox_normal(double* out, int64_t n, int w, uint64_t seed, void* stream) {
+    SPD_TRY({
+        SPD_REQUIRE(out != nullptr && n >= 0 && w >= 0, "spd_test_philox_normal: bad argument");
+        philox_normal((cudaStream_t)stream, out, n, w, seed);
     })
 }
 

@@ -188,6 +188,11 @@ struct QrcpDesc {          // pivoted QR of A (m x n) in place
     double* beta;          // min(m, n)
     int* rank;             // out (device)
     double* norms;         // scratch n
+    // forced pivots (injection hook of reading R19, spd_h2_opts.inject_skeletons):
+    // when non-null, step t < nforce takes the column whose ORIGINAL index is force[t]
+    // (device) instead of the argmax, and the factorization stops after nforce steps
+    const int* force = nullptr;
+    int nforce = 0;
 };
 
 // host launchers (dense.cu)

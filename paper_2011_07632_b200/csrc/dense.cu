@@ -680,6 +680,18 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
                     s_stop = (t >= kmax || nu == 0.0 || nu <= rel_tol * s_nu0) ? 1 : 0;
                 }
                 __syncthreads();
+                if (d.force) {                          // injected pivots (R19 hook)
+                    if (threadIdx.x == 0) s_stop = (t >= min(kmax, d.nforce)) ? 1 : 0;
+                    __syncthreads();
+                    if (!s_stop) {
+                        const int want = d.force[t];
+                        for (int j = t + threadIdx.x; j < n; j += QR_THREADS)
+                            if (__ldcg(d.piv + j) == want) si[0] = j;
+                    }
+                    __syncthreads();
+                    bi = si[0];
+                    __syncthreads();
+                }
                 if (!s_stop) {
                     const int p = bi;
                     if (p != t) {
@@ -833,7 +845,15 @@ __global__ void __launch_bounds__(256) qrcp_smem_kernel(const QrcpDesc* __restri
         block_argmax(v, idx, sv, si, bv, bi);
         const double nu = bv > 0.0 ? sqrt(bv) : 0.0;
         if (t == 0) nu0 = nu;
-        if (nu == 0.0 || nu <= rel_tol * nu0) { rank = t; break; }
+        if (d.force) {                                  // injected pivots (R19 hook)
+            if (t >= d.nforce) { rank = t; break; }
+            const int want = d.force[t];
+            for (int j = t + tid; j < n; j += blockDim.x)
+                if (pv[j] == want) si[0] = j;
+            __syncthreads();
+            bi = si[0];
+            __syncthreads();
+        } else if (nu == 0.0 || nu <= rel_tol * nu0) { rank = t; break; }
         const int p = bi;
         if (p != t) {
             for (int i = tid; i < m; i += blockDim.x) {

@@ -225,6 +225,22 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
     for (int i = 1; i < t.nnodes; ++i)
         if (h->active[(i - 1) / 2]) h->active[i] = 1;
     h->active[0] = 0;
+    // injected skeletons (reading R19 hook): per node at levels 1..L-1 in heap order,
+    // s_i then s_i tree positions; turned into forced QRCP pivots (candidate indices)
+    std::vector<std::vector<int>> inj;
+    if (h->inject) {
+        inj.assign(t.nnodes, {});
+        const int32_t* q = h->inject;
+        for (int i = 0; i < t.nnodes; ++i) {
+            if (t.level(i) >= L) continue;
+            const int si = *q++;
+            SPD_REQUIRE(si >= 0 && si <= t.size(i) && (si == 0 || h->active[i]),
+                        "h2_build: inject_skeletons: bad skeleton count");
+            inj[i].assign(q, q + si);
+            q += si;
+        }
+        h->inject = nullptr;
+    }
     double t1 = now_s();
     h->timings[0] = t1 - t0;
     stage_mark(s, nullptr);
@@ -269,6 +285,27 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         rank_d.zero(s);
         DBuf<double> beta_d(std::max<int64_t>(1, piv_off[lv.count]));
         DBuf<double> norms_d(std::max<int64_t>(1, piv_off[lv.count]));
+        DBuf<int> force_d;
+        if (!inj.empty()) {                      // forced pivots = candidate indices
+            std::vector<int> f(std::max<int64_t>(1, piv_off[lv.count]), -1);
+            for (int a : nodes) {
+                const int i = lv.first + a;
+                std::vector<int> cand;
+                if (k == 1) for (int64_t p = t.begin[i]; p < t.end[i]; ++p) cand.push_back((int)p);
+                else {
+                    const int c1 = 2 * i + 1;
+                    cand = inj[c1];
+                    cand.insert(cand.end(), inj[c1 + 1].begin(), inj[c1 + 1].end());
+                }
+                SPD_REQUIRE((int)cand.size() == lv.ncand[a], "h2_build: inject_skeletons: candidate mismatch");
+                for (size_t c = 0; c < inj[i].size(); ++c) {
+                    auto it = std::find(cand.begin(), cand.end(), inj[i][c]);
+                    SPD_REQUIRE(it != cand.end(), "h2_build: inject_skeletons: skeleton not a candidate");
+                    f[piv_off[a] + c] = (int)(it - cand.begin());
+                }
+            }
+            force_d.upload(f, s);
+        }
         // subtree sharding (comm.cpp): a rank computes the nodes of its subtree at levels
         // with >= P nodes (all nodes at the redundant top levels); a virtual communicator
         // computes every virtual rank's share in turn in this process
@@ -329,6 +366,11 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 qd.beta = beta_d.p + piv_off[a];
                 qd.rank = rank_d.p + a;
                 qd.norms = norms_d.p + piv_off[a];
+                if (!inj.empty()) {
+                    qd.force = force_d.p + piv_off[a];
+                    qd.nforce = (int)inj[i].size();
+                    SPD_REQUIRE(qd.nforce <= qd.max_rank, "h2_build: inject_skeletons: too many skeletons");
+                }
                 qdesc.push_back(qd);
             }
             stage_mark(s, "h2 alloc/desc", k);

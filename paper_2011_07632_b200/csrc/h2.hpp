@@ -85,6 +85,7 @@ struct spd_h2_s {
     spd::DBuf<double> xt, yt;
     std::vector<spd::DBuf<double>> xh, yh;
     spd_comm_t comm = nullptr;
+    const int32_t* inject = nullptr;   // spd_h2_opts.inject_skeletons during h2_build only (host)
     // symmetric k = 1 product (near field + Type-3 couplings, h2sym.cu): blocks stored
     // up to sym_budget bytes, the rest evaluated on the fly
     int stored_mode = -1;          // -1 undecided, 0 old per-level path (tests), 1 symmetric

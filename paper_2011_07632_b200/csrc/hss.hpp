@@ -81,6 +81,7 @@ bool pcg_persistent_prepare(PcgPersistent& pk, spd_h2_s* A, spd_hss_s* M, double
 // out: ||r||^2, iterations, converged, error (1: p^T A p <= 0, 2: r^T M r <= 0)
 void pcg_persistent_run(PcgPersistent& pk, double rz, double nb, double tol, int maxit, double out[4], cudaStream_t s);
 const spd_hss_s* hss_if_hss(const void* handle);      // nullptr when handle is not an HSS
+void philox_normal(cudaStream_t s, double* out, int64_t n, int w, uint64_t seed);   // Omega (R29)
 const double* hss_timings(const spd_hss_s* H);
 const int64_t* hss_shard_work(const spd_hss_s* H);
 inline uint64_t pair_key(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uint32_t)j; }

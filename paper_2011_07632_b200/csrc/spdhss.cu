@@ -56,6 +56,12 @@ __global__ void philox_normal_kernel(double* out, int64_t n, int w, uint64_t see
     }
 }
 
+void philox_normal(cudaStream_t s, double* out, int64_t n, int w, uint64_t seed) {
+    if (n == 0 || w == 0) return;
+    philox_normal_kernel<<<148 * 8, 256, 0, s>>>(out, n, w, seed);
+    SPD_LAUNCH();
+}
+
 // ================================================================= dense kernel blocks A_ii
 struct DenseKDesc { const double* x; int64_t ds; int n; int64_t id0; double* A; int ld; };
 __global__ void dense_kernel_blocks(const DenseKDesc* descs, KernelParams kp, double shift, int d) {

@@ -6,6 +6,7 @@ import pytest
 import oracle
 import synth
 from gpu_util import cuda, host, rel
+from parity_util import TreeInfo, certify_h2
 
 pytestmark = pytest.mark.gpu
 
@@ -74,17 +75,40 @@ def test_proxies_bit_exact(spd, name):
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_skeletons(spd, name):
+    """Every node's skeleton sequence is the oracle's or a certified tie (R19): replayed
+    in the oracle's QRCP, each deviating pivot within 16 sqrt(m) eps nu_0 of the largest
+    residual norm and the rank within that band of the threshold.  No percentage window."""
     cfg, X, h, ho = built(spd, name)
-    rg = h.ranks()
-    sk = h.skeletons()
-    n_nodes = n_same = 0
-    for i, s in ho.rank.items():
-        n_nodes += 1
-        assert abs(int(rg[i]) - s) <= 1, f"node {i}: rank {rg[i]} vs {s}"
-        if rg[i] == s and (s == 0 or np.array_equal(sk.get(i, []), ho.skel[i])):
-            n_same += 1
-    # certified ties (R19) may flip tail pivots; most nodes must agree exactly
-    assert n_same >= 0.9 * n_nodes, f"{n_same}/{n_nodes} skeleton sets identical"
+    info = TreeInfo(X, cfg.kernel, cfg.leaf)
+    nodes, same, ties, fails = certify_h2(info, cfg.kernel, cfg.ell, cfg.h2_tol, h.ranks(), h.skeletons(),
+                                          oracle_skel=ho.skel, n_proxy=ho.n_proxy)
+    print(f"{name}: {nodes} active nodes, {same} identical, {ties} certified ties")
+    assert not fails, fails[:5]
+    assert same + ties == nodes
+
+
+def test_injected_skeletons(spd):
+    """The parity hook spd_h2_opts.inject_skeletons (R19): the GPU ID takes the oracle's
+    pivots, so its skeletons are the oracle's and its products match to <= 1e-9."""
+    import torch
+    cfg, X, h, ho = built(spd, "C2s")
+    inj = {i: s for i, s in ho.skel.items()}
+    hi = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol,
+                      inject_skeletons=inj)
+    sk = hi.skeletons()
+    for i, s in ho.skel.items():
+        np.testing.assert_array_equal(sk.get(i, np.zeros(0, np.int64)), s)
+    x = synth.multivec(cfg.n, 3)
+    yo = np.empty_like(x)
+    yo[ho.tree.perm] = oracle.h2_matvec(ho, x[ho.tree.perm])
+    assert rel(host(spd.h2_matvec(hi, cuda(x))), yo) <= 1e-9
+    # a skeleton that is not a candidate of its node is rejected
+    bad = dict(inj)
+    leaf = ho.tree.nodes_at(1)[0]
+    bad[leaf] = np.array([ho.tree.N - 1])
+    with pytest.raises(spd.SpdError):
+        spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol,
+                     inject_skeletons=bad)
 
 
 @pytest.mark.parametrize("name", list(CASES))
