@@ -1,19 +1,23 @@
 #!/usr/bin/env python
 """bench.py -- the driver's benchmark contract for the SPD-HSS-from-H2 hot path.
 
-One STEP = one pass of the whole hot path of arXiv 2011.07632 on BASELINE.json
-configs[1] (C2: N=32768 points uniform in [0,1]^3, Matern-3/2 l=0.2 + 1e-4 I,
-leaf 128, H2 tol 1e-10, HSS cap 100 / tol 1e-3, p = 10, PCG to 1e-8):
-    h2_build -> spdhss_build (Alg. 4) -> pcg_solve (H2 matvec + HSS solve)
-    -> one H2 multi-vector product of width 64 (the "H2 multi-vector GFLOP/s" line)
-`value` = seconds per step (max over ranks), lower is better.  Inputs are
-resident in HBM when the timed region starts; L2 (126 MB) is flushed between
-steps by writing a 256 MB buffer.  Multi-GPU (torchrun): independent replicas,
-weak scaling; with --shard one problem whose H2 build, SPD-HSS build and H2 products
-(PCG's included) are sharded by subtrees over NCCL, strong scaling.
+BASELINE.json's metric is "SPD-HSS build s & H2 multi-vector GFLOP/s (fp64)"; its
+single-GPU configurations at N = 2^20 are C4 (full build) and C5 (multi-vector
+product sweep).  One STEP = one pass of the hot path on those configs:
+    h2_build(C4) -> spdhss_build(C4, Alg. 4)  +  h2_matvec(C5's H2, X of width 64)
+(C5's H2 is built once before the timed region; its product evaluates the kernel
+blocks on the fly).  `value` = seconds per step (max over ranks), lower is better.
+Inputs are resident in HBM when the timed region starts; they are larger than L2
+(126 MB) and L2 is also flushed between steps (256 MB write).  Outside the timed
+region: the C5 sweep k in {1, 16, 64, 256} (evaluated, then with the symmetric block
+store, whose build time is reported), C4 PCG time-to-1e-8 once, the HSS solve
+bandwidth, the O11 HSS error, a profiled pass (per-kernel-class CUDA events) for the
+roofline, and the end-to-end pass through host buffers.
+Multi-GPU (torchrun): independent replicas (weak scaling); --shard: one problem whose
+builds and products are sharded by subtrees over NCCL (strong scaling).
 
---impl reference: the CPU oracle (test infrastructure) timed on a bounded
-sample of the same workload; prints the same JSON line with "impl": "reference".
+--impl reference: the CPU oracle (test infrastructure) timed on a bounded sample of
+the same workload (the C4 and C5 recipes at N = 4096), not extrapolated.
 """
 import argparse
 import json
@@ -33,16 +37,17 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "SPD-HSS build s & H2 multi-vector GFLOP/s (fp64) vs FP64 roofline"
-CFG = synth.C2
-WORKLOAD = ("C2 (BASELINE configs[1]): N=32768 uniform [0,1]^3, Matern-3/2 (1+sqrt3 r/0.2)exp(-sqrt3 r/0.2) "
-            "+ 1e-4 I, KD leaf 128, H2 proxy-ID tol 1e-10, SPD-HSS cap 100 / tol 1e-3, p=10, PCG b~N(0,1) to 1e-8; "
-            "step = h2_build + spdhss_build + pcg_solve + h2_matvec(k=64)")
+CFG = synth.C4                 # the full build (BASELINE configs[3])
+CFG_MV = synth.C5              # the multi-vector product (BASELINE configs[4])
 MV_K = 64
+WORKLOAD = ("C4 full build + C5 product at N=2^20 (BASELINE configs[3], configs[4]): "
+            "h2_build + spdhss_build of C4 (N=1048576 uniform [0,1]^3, IMQ 1/sqrt(r^2+0.01) + 1e-2 I, KD leaf 256, "
+            "H2 proxy-ID tol 1e-10, SPD-HSS cap 150 / tol 1e-3, p=10, device Philox Omega) + one k=64 H2 product "
+            "on C5's H2 (N=1048576 uniform [0,1]^3, Gaussian exp(-r^2/0.2^2), leaf 256, tol 1e-10, X~N(0,1), "
+            "kernel blocks evaluated on the fly; C5's H2 built once before the timed region)")
 # roofline class of each kernel family
 TENSOR_BOUND = {"kblock_dmma", "gemm_dmma"}
-REF_SAMPLE_N = 2048      # oracle sample (same kernel / leaf / cap / tolerances)
-
-
+REF_SAMPLE_N = 4096      # oracle sample per reference-arm step (C4 / C5 recipes, same leaf / cap / tolerances)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -50,11 +55,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
+    ap.add_argument("--no-pcg", action="store_true", help="skip the C4 PCG time-to-tolerance measurement")
+    ap.add_argument("--n", type=int, default=0, help="override N of both configs (testing only)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: ONE problem, H2/HSS builds and all H2 products sharded by subtrees over NCCL "
-                         "(strong scaling); "
-                         "default: independent replicas (weak scaling)")
+                         "(strong scaling); default: independent replicas (weak scaling)")
     return ap.parse_args()
 
 
@@ -99,7 +104,7 @@ class ClockSampler:
 # ------------------------------------------------------------------ helpers
 def load_traffic(kernel):
     """DRAM traffic of the dominant kernel from the committed ncu capture (or None)."""
-    path = os.path.join(ROOT, "profiles", "r01g_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get(kernel)
@@ -141,9 +146,9 @@ def max_over_ranks(v, device="cuda"):
 
 
 def replica_config(rank):
-    """Replicas (weak scaling): every rank solves its own C2 problem.  All ranks
-    use the same recipe and seeds, so every replica does identical work."""
-    return CFG
+    """Replicas (weak scaling): every rank solves its own C4 build + C5 product.  All
+    ranks use the same recipe and seeds, so every replica does identical work."""
+    return CFG, CFG_MV
 
 
 def h2_useful_flops(h, k):
@@ -167,28 +172,36 @@ def h2_useful_flops(h, k):
 
 
 def oracle_step(n):
-    """One oracle pass (h2_build + Alg. 4 + PCG) on the C2 recipe at size n."""
+    """One oracle pass of the step on the C4 / C5 recipes at size n: h2_build +
+    spdhss_build (Alg. 4, Philox Omega of reading R29) of the C4 recipe and one k=64
+    product on the C5 recipe's H2 (built outside the timed part, like the GPU arm).
+    Returns (seconds of the timed part, phase seconds)."""
     import oracle
-    cfg = CFG.scaled(n)
-    X = synth.points(cfg)
-    h = oracle.h2_build(X, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
-    H = oracle.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, synth.omega(cfg), form="chol")
-    b = synth.rhs(cfg)[h.tree.perm]
-    _, it, conv, _ = oracle.pcg(lambda v: oracle.h2_matvec(h, v), lambda v: oracle.hss_solve(H, v),
-                                b, cfg.pcg_tol, cfg.maxit)
-    return it
-
-
-def cpu_baseline(n_full):
-    """The oracle timed on a bounded sample (N=REF_SAMPLE_N), extrapolated by N log N."""
+    from oracle.omega import philox_normal
+    c4, c5 = CFG.scaled(n), CFG_MV.scaled(n)
+    h5 = oracle.h2_build(synth.points(c5), c5.kernel, c5.ell, c5.shift, c5.leaf, c5.h2_tol)
+    V = synth.multivec(n, MV_K)[h5.tree.perm]
     t0 = time.time()
-    it = oracle_step(REF_SAMPLE_N)
-    dt = time.time() - t0
-    scale = (n_full * math.log2(n_full / CFG.leaf)) / (REF_SAMPLE_N * math.log2(REF_SAMPLE_N / CFG.leaf))
-    return {"value": round(dt * scale, 3), "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"oracle h2_build+spdhss_build+pcg on the C2 recipe at N={REF_SAMPLE_N} "
-                      f"({dt:.2f} s, {it} PCG its), extrapolated x{scale:.1f} by N log N to N={n_full}; "
-                      "the oracle's C QRCP uses OpenMP over the host cores"}
+    X = synth.points(c4)
+    h = oracle.h2_build(X, c4.kernel, c4.ell, c4.shift, c4.leaf, c4.h2_tol)
+    t1 = time.time()
+    oracle.spdhss_build(h, c4.rank_cap, c4.hss_tol, philox_normal(n, c4.w, 1234), form="chol")
+    t2 = time.time()
+    h5.blocks.clear()                          # evaluated on the fly, like the GPU step
+    oracle.h2_matvec(h5, V)
+    t3 = time.time()
+    return t3 - t0, {"h2_build_s": round(t1 - t0, 3), "spdhss_build_s": round(t2 - t1, 3),
+                     "c5_mv_s": round(t3 - t2, 3)}
+
+
+def cpu_baseline():
+    """The oracle as it stands, timed once on a bounded sample of the step (no scaling)."""
+    dt, ph = oracle_step(REF_SAMPLE_N)
+    return {"value": round(dt, 3), "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"one step of the workload at N={REF_SAMPLE_N} instead of 2^20 (C4 recipe h2_build + "
+                      f"spdhss_build, C5 recipe k={MV_K} product; leaf 256, caps and tolerances as configured), "
+                      f"not extrapolated; phases {ph}; numpy/OpenMP over the host cores",
+            "points_per_s": round(REF_SAMPLE_N / dt, 1)}
 
 
 # ------------------------------------------------------------------ reference arm
@@ -198,25 +211,62 @@ def run_reference(args):
         return
     for _ in range(args.warmup):
         oracle_step(1024)                       # small warm-up (imports, C build)
-    times = []
+    times, phases = [], None
     for _ in range(args.steps):
-        t0 = time.time()
-        oracle_step(REF_SAMPLE_N)
-        times.append(time.time() - t0)
-    scale = (CFG.n * math.log2(CFG.n / CFG.leaf)) / (REF_SAMPLE_N * math.log2(REF_SAMPLE_N / CFG.leaf))
-    v = statistics.mean(times) * scale
+        dt, phases = oracle_step(REF_SAMPLE_N)
+        times.append(dt)
+    v = statistics.mean(times)
+    sample = (f"each step: the workload at N={REF_SAMPLE_N} instead of 2^20 (C4 recipe h2_build + spdhss_build, "
+              f"C5 recipe k={MV_K} product), mean {v:.2f} s, not extrapolated; last phases {phases}")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "parallelism": "cpu oracle (rank 0 only)"},
+            "config": {"workload": WORKLOAD, "parallelism": "cpu oracle (rank 0 only)", "N": REF_SAMPLE_N},
             "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": f"each step: oracle on the C2 recipe at N={REF_SAMPLE_N} "
-                                       f"(mean {statistics.mean(times):.2f} s), x{scale:.1f} by N log N"},
+                             "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
+def colmajor(a):
+    import torch
+    return torch.tensor(np.asfortranarray(a).T.copy(), device="cuda").t()
+
+
+def timed_products(spd, h, V, reps=3):
+    """ms per product (one warm-up, then `reps` products between two events)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    spd.h2_matvec(h, V)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        spd.h2_matvec(h, V)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def hss_solve_bytes(h, H):
+    """Algorithmic bytes of one single-vector HSS solve: the factors read once,
+    sum over nodes of 8 (m^2/2 + m r) (leaf m = n_i, nonleaf m = r_c1 + r_c2, root m^2/2)."""
+    hr = H.ranks().astype(np.int64)
+    nodes = h.nodes()
+    Lh = h.levels
+    hb = 0.0
+    for i in range(len(hr)):
+        lev = Lh - int(np.floor(np.log2(i + 1)))
+        if lev == Lh:
+            m = int(hr[1] + hr[2]) if len(hr) > 2 else int(nodes[0, 1] - nodes[0, 0])
+            hb += 8.0 * m * m / 2
+            continue
+        m = int(nodes[i, 1] - nodes[i, 0]) if lev == 1 else int(hr[2 * i + 1] + hr[2 * i + 2])
+        hb += 8.0 * (m * m / 2 + m * int(hr[i]))
+    return hb
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -235,43 +285,45 @@ def run_ours(args):
         uid = [spd.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = spd.Comm(world, rank, uid[0])
-    cfg = replica_config(rank) if not args.n else CFG.scaled(args.n)
-    N = cfg.n
-    X_h = synth.points(cfg)
-    b_h = synth.rhs(cfg)
+    c4, c5 = replica_config(rank)
+    if args.n:
+        c4, c5 = c4.scaled(args.n), c5.scaled(args.n)
+    N = c4.n
+    X4_h, X5_h = synth.points(c4), synth.points(c5)
     V_h = synth.multivec(N, MV_K)
-    pts = torch.tensor(X_h, device="cuda")
-    b = torch.tensor(b_h, device="cuda")
-    V = torch.tensor(np.asfortranarray(V_h).T.copy(), device="cuda").t()
+    pts4 = torch.tensor(X4_h, device="cuda")
+    pts5 = torch.tensor(X5_h, device="cuda")
+    V = colmajor(V_h)
     flush = torch.empty(256 << 20 >> 3, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
+    # C5's H2, once, outside the timed region
+    t5 = time.time()
+    h5 = spd.h2_build(pts5, c5.kernel, c5.ell, c5.shift, c5.leaf, c5.h2_tol, comm=comm)
+    torch.cuda.synchronize()
+    h5_build_s = time.time() - t5
+    mv_flops, mv_counts = h2_useful_flops(h5, MV_K)
 
-    record_flops = {}
-
-    def step(points, rhs, record=None):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    def step(points, X, record=None):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(stream)
-        h = spd.h2_build(points, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol, comm=comm)
+        h = spd.h2_build(points, c4.kernel, c4.ell, c4.shift, c4.leaf, c4.h2_tol, comm=comm)
         ev[1].record(stream)
-        H = spd.spdhss_build(h, cfg.rank_cap, cfg.hss_tol, cfg.oversample, seed=1234)
+        H = spd.spdhss_build(h, c4.rank_cap, c4.hss_tol, c4.oversample, seed=1234)
         ev[2].record(stream)
-        x, rep = spd.pcg_solve(h, H, rhs, tol=cfg.pcg_tol, maxit=cfg.maxit)
+        Y = spd.h2_matvec(h5, X)
         ev[3].record(stream)
-        spd.h2_matvec(h, V)
-        ev[4].record(stream)
-        ev[4].synchronize()
-        t = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(4)]
-        if record is not None and not record:
-            record_flops.update(zip(("flops", "counts"), h2_useful_flops(h, MV_K)))
+        ev[3].synchronize()
+        t = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(3)]
         if record is not None:
-            record.append({"h2_build_s": t[0], "spdhss_build_s": t[1], "pcg_s": t[2], "h2_mv_s": t[3],
-                           "pcg_iters": rep.iters, "pcg_relres": rep.relres, "converged": rep.converged,
-                           "h2_ranks_max": int(h.ranks().max()), "hss_rank_max": int(H.ranks().max()),
+            record.append({"h2_build_s": t[0], "spdhss_build_s": t[1], "c5_mv_s": t[2],
+                           "h2_rank_max": int(h.ranks().max()), "hss_rank_max": int(H.ranks().max()),
                            "h2_timings": list(h.timings()[:2]), "hss_timings": list(H.timings()[:4])})
-        return x, h, H
+        return h, H, Y
 
+    os.environ["SPD_STORE_FRAC"] = "0"       # the step's product evaluates its kernel blocks (north star)
     for _ in range(args.warmup):
-        step(pts, b)
+        out = step(pts4, V)
+        out = None
         flush.fill_(1.0)
     torch.cuda.synchronize()
     if world > 1:
@@ -281,13 +333,15 @@ def run_ours(args):
     sampler.start()
     l0 = lib.spd_launch_count()
     recs, step_s = [], []
+    last = None
     torch.cuda.nvtx.range_push("timed")
     for _ in range(args.steps):
+        last = None                          # free the previous step's H2 / HSS / product
         flush.fill_(1.0)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        step(pts, b, recs)
+        last = step(pts4, V, recs)
         s1.record(stream)
         s1.synchronize()
         step_s.append(s0.elapsed_time(s1) * 1e-3)
@@ -296,171 +350,198 @@ def run_ours(args):
     launches = lib.spd_launch_count() - l0
     clocks = sampler.stop()
     t_step = max_over_ranks(statistics.mean(step_s))
-    # ---------------- end-to-end: host (pinned) inputs, H2D inside, result D2H inside
-    pts_pin = torch.tensor(X_h).pin_memory()
-    b_pin = torch.tensor(b_h).pin_memory()
-    x_pin = torch.empty(N, dtype=torch.float64).pin_memory()
+    h4, H4, _ = last
+    last = None
+    # ---------------- end-to-end: host (pinned) inputs, H2D inside, results D2H inside
+    pts_pin = torch.tensor(X4_h).pin_memory()
+    V_pin = torch.tensor(np.ascontiguousarray(V_h.T)).pin_memory()          # k x N = column-major N x k
+    Y_pin = torch.empty((MV_K, N), dtype=torch.float64).pin_memory()
     e2e = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, min(args.steps, 2))):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         p_d = pts_pin.to("cuda", non_blocking=True)
-        b_d = b_pin.to("cuda", non_blocking=True)
-        x, _, _ = step(p_d, b_d)
-        x_pin.copy_(x, non_blocking=True)
+        V_d = V_pin.to("cuda", non_blocking=True).t()
+        h, H, Y = step(p_d, V_d)
+        Y_pin.copy_(Y.t(), non_blocking=True)
+        ranks = H.ranks()                    # the build's result read back (host query)
         e1.record(stream)
         e1.synchronize()
         e2e.append(e0.elapsed_time(e1) * 1e-3)
-    # ---------------- H2 multi-vector sweep over BASELINE C5's widths k in {1, 16, 64, 256}
-    # on this workload's H2 (after the timed region; 3 timed products per k after one warm-up)
-    sweep = {}
-    _, h_sw, H_sw = step(pts, b)
+        h = H = Y = p_d = V_d = None
+    e2e_v = max_over_ranks(statistics.mean(e2e))
+    # ---------------- C5 multi-vector sweep k in {1, 16, 64, 256} (BASELINE configs[4])
     fp64_pk = load_peaks().get("fp64_dgemm_tflops_sustained") or load_peaks().get("fp64_dgemm_tflops") or 35.5
-    for kk in (1, 16, 64, 256):
-        Vk = torch.tensor(np.asfortranarray(synth.multivec(N, kk)).T.copy(), device="cuda").t()
-        spd.h2_matvec(h_sw, Vk)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(3):
-            spd.h2_matvec(h_sw, Vk)
-        e1.record(stream)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / 3
-        fl = h2_useful_flops(h_sw, kk)[0]
-        sweep[str(kk)] = {"ms": round(ms, 3), "useful_tflops": round(fl / ms / 1e9, 2),
-                          "frac_fp64_peak": round(fl / ms / 1e9 / fp64_pk, 3)}
+    sweep = {}
+    for kk in (16, 64, 256, 1):
+        Vk = colmajor(synth.multivec(N, kk))
+        fl = h2_useful_flops(h5, kk)[0]
+        ent = {}
+        if kk == 1:                           # the first k = 1 product builds the symmetric store
+            os.environ["SPD_STORE_FRAC"] = "0.25"
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            spd.h2_matvec(h5, Vk)
+            e1.record(stream)
+            e1.synchronize()
+            ent["first_call_ms_incl_store_build"] = round(e0.elapsed_time(e1), 1)
+            ent["store_gb"] = round(h5.sym_store()[0] / 1e9, 2)
+        ms = timed_products(spd, h5, Vk)
+        ent.update({"ms": round(ms, 3), "useful_tflops": round(fl / ms / 1e9, 2),
+                    "frac_fp64_peak": round(fl / ms / 1e9 / fp64_pk, 3),
+                    "blocks": "stored symmetric k=1 store" if kk == 1 else "evaluated on the fly"})
+        sweep[str(kk)] = ent
         del Vk
-    # HSS error metric (the paper's Fig. 5 quantity P:1196-1206): mean over 10
-    # Gaussian probes of ||H x - A_h2 x|| / ||A_h2 x||, H the SPD-HSS matrix (hss_matvec)
-    Pr = torch.tensor(np.asfortranarray(np.random.default_rng(4000).standard_normal((N, 10))).T.copy(),
-                      device="cuda").t()
-    Ax = spd.h2_matvec(h_sw, Pr)
-    Hx = spd.hss_matvec(H_sw, Pr)
+    stored = {}
+    if h5.sym_store()[0] > 0:                 # multi-vector products reading the store instead
+        for kk in (64, 256):
+            Vk = colmajor(synth.multivec(N, kk))
+            ms = timed_products(spd, h5, Vk)
+            fl = h2_useful_flops(h5, kk)[0]
+            stored[str(kk)] = {"ms": round(ms, 3), "useful_tflops": round(fl / ms / 1e9, 2),
+                               "frac_fp64_peak": round(fl / ms / 1e9 / fp64_pk, 3)}
+            del Vk
+        stored["store_build_included_in"] = "sweep['1'].first_call_ms_incl_store_build"
+    h5.release_store()
+    os.environ["SPD_STORE_FRAC"] = "0"
+    # ---------------- O11 HSS error and the standalone HSS solve on the last C4 build
+    Pr = colmajor(np.random.default_rng(4000).standard_normal((N, 10)))
+    Ax = spd.h2_matvec(h4, Pr)
+    Hx = spd.hss_matvec(H4, Pr)
     hss_err = float(((Hx - Ax).norm(dim=0) / Ax.norm(dim=0)).mean())
-    # single-vector HSS solve (the PCG preconditioner), algorithmic bytes = the factors read
-    # once: sum over nodes of 8 (m^2/2 + m r) (leaf m = n_i, nonleaf m = r_c1 + r_c2)
-    hr = H_sw.ranks().astype(np.int64)
-    nodes = h_sw.nodes()
-    Lh = h_sw.levels
-    hb = 0.0
-    for i in range(len(hr)):
-        depth = int(np.floor(np.log2(i + 1)))
-        lev = Lh - depth
-        if lev == Lh:
-            m = int(hr[1] + hr[2]) if len(hr) > 2 else int(nodes[0, 1] - nodes[0, 0])
-            hb += 8.0 * m * m / 2
-            continue
-        m = int(nodes[i, 1] - nodes[i, 0]) if lev == 1 else int(hr[2 * i + 1] + hr[2 * i + 2])
-        hb += 8.0 * (m * m / 2 + m * int(hr[i]))
-    bt = b.clone()
+    del Pr, Ax, Hx
+    hb = hss_solve_bytes(h4, H4)
+    b4 = torch.tensor(synth.rhs(c4), device="cuda")
+    bt = b4.clone()
     for _ in range(3):
-        spd.hss_solve(H_sw, bt, layout=1)
+        spd.hss_solve(H4, bt, layout=1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(20):
-        spd.hss_solve(H_sw, bt, layout=1)
+        spd.hss_solve(H4, bt, layout=1)
     e1.record(stream)
     e1.synchronize()
     hs_us = e0.elapsed_time(e1) / 20 * 1e3
     hss_solve_info = {"us": round(hs_us, 1), "algorithmic_mb": round(hb / 1e6, 1),
                       "gbs": round(hb / hs_us / 1e3, 1),
                       "frac_hbm": round(hb / hs_us / 1e3 / load_peaks().get("hbm_gbs", 6546.2), 3),
-                      "note": "standalone solve (one launch per level); inside PCG the same phases run in the persistent kernel"}
-    del h_sw, H_sw, Pr, Ax, Hx
-    # ---------------- profiled pass (same steps, per-kernel-class CUDA events on the
+                      "note": "standalone C4 solve (one launch per level); inside PCG the same phases run in "
+                              "the persistent kernel or the per-iteration graph"}
+    # ---------------- C4 PCG time-to-1e-8, once (maxit 10000, reading R25)
+    pcg_info = None
+    if not args.no_pcg:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = spd.pcg_solve(h4, H4, b4, tol=c4.pcg_tol, maxit=10000)
+        e1.record(stream)
+        e1.synchronize()
+        pcg_info = {"s": round(e0.elapsed_time(e1) * 1e-3, 3), "iters": rep.iters, "converged": bool(rep.converged),
+                    "relres_true": rep.relres_true, "ms_per_iter": round(e0.elapsed_time(e1) / max(1, rep.iters), 3),
+                    "note": "includes building the symmetric k=1 block store (within 40% of free memory)"}
+    h4 = H4 = b4 = bt = None
+    # ---------------- profiled pass (same step, per-kernel-class CUDA events on the
     # launching streams; kept out of the timed region because the per-launch event
     # pairs and their host-side drains perturb the step time)
     lib.spd_prof_reset()
     lib.spd_prof_enable(1)
     prof_s = []
-    for _ in range(args.steps):
+    for _ in range(1):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        step(pts, b)
+        out = step(pts4, V)
         s1.record(stream)
         s1.synchronize()
+        out = None
         prof_s.append(s0.elapsed_time(s1) * 1e-3)
     torch.cuda.synchronize()
     lib.spd_prof_enable(0)
     prof = prof_table(lib)
-    e2e_v = max_over_ranks(statistics.mean(e2e))
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
-    # ---------------- roofline of the dominant kernel class
+    line = {
+        "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 2), "higher_is_better": False,
+        "scaling": "strong" if comm is not None else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N": N, "l2_flush": "256 MB write between steps; inputs > L2",
+                   "parallelism": ("h2_build, spdhss_build and every H2 product sharded by subtrees over NCCL"
+                                   if comm is not None else "replicas") if world > 1 else "single GPU"},
+        "breakdown": dict({k: round(statistics.mean(r[k] for r in recs), 4)
+                           for k in ("h2_build_s", "spdhss_build_s", "c5_mv_s")},
+                          h2_tree_lists_s=round(statistics.mean(r["h2_timings"][0] for r in recs), 4)),
+        "full_build_s": round(statistics.mean(r["h2_build_s"] + r["spdhss_build_s"] for r in recs), 4),
+        "h2_rank_max": recs[-1]["h2_rank_max"], "hss_rank_max": recs[-1]["hss_rank_max"],
+        "c5_h2_build_s": round(h5_build_s, 3),
+        "h2_multivector": {"k": MV_K, "useful_gflop": round(mv_flops / 1e9, 2),
+                           "gflops": round(mv_flops / statistics.mean(r["c5_mv_s"] for r in recs) / 1e9, 1),
+                           "frac_fp64_peak": round(mv_flops / statistics.mean(r["c5_mv_s"] for r in recs)
+                                                   / 1e12 / fp64_pk, 4),
+                           "counts": mv_counts},
+        "h2_multivector_sweep": sweep,
+        "h2_multivector_stored": stored,
+        "pcg_c4": pcg_info,
+        "hss_error_o11": round(hss_err, 6),
+        "hss_solve": hss_solve_info,
+        "kernels": {k: {"launches": int(v["launches"]), "ms": round(v["ms"], 2),
+                        "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3),
+                        "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
+        "roofline": roofline(prof, sum(prof_s)),
+        "e2e": {"value": round(e2e_v, 4), "unit": "s",
+                "h2d_bytes_per_step": int(8 * N * (c4.d + MV_K)), "d2h_bytes_per_step": int(8 * N * MV_K)},
+        "gpu_launches": int(launches // max(1, args.steps)),
+        "profiled_pass_s_per_step": round(statistics.mean(prof_s), 4),
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def roofline(prof, prof_total_s):
+    """Roofline of the dominant kernel class of the profiled step: achieved = its
+    algorithmic flops (tensor) or bytes (hbm) per launch / its mean launch duration."""
     peaks = load_peaks()
     fp64 = peaks.get("fp64_dgemm_tflops_sustained") or peaks.get("fp64_dgemm_tflops")
     fp64_src = "measured cuBLAS DGEMM sustained (profiles/fp64_peak.json)" if fp64 else \
         "bf16 measured x nominal fp64/bf16 ratio (40/2250)"
     if not fp64:
         fp64 = peaks.get("bf16_tflops_sustained", 1345.0) * 40.0 / 2250.0
-    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else (None, None)
-    roof = None
-    if top[0]:
-        nm, p = top
-        avg_s = p["ms"] * 1e-3 / max(1.0, p["launches"])
-        if nm in TENSOR_BOUND:
-            ach = p["flops"] / max(1.0, p["launches"]) / avg_s / 1e12
-            roof = {"kernel": nm, "bound": "tensor", "achieved": round(ach, 3), "peak": round(fp64, 2),
-                    "unit": "TFLOP/s", "frac": round(ach / fp64, 4), "traffic": None, "peak_source": fp64_src}
-        else:
-            ach = p["bytes"] / max(1.0, p["launches"]) / avg_s / 1e9
-            roof = {"kernel": nm, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs", 6550.7),
-                    "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6550.7), 4), "traffic": None,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        tr = load_traffic(nm)
-        if tr and nm == "pcg_persistent":        # per launch: ncu's bytes per PCG iteration x this launch's iterations
-            roof["traffic"] = round(tr["bytes_per_iteration"] * statistics.mean(r["pcg_iters"] for r in recs) / 1e9, 2)
-            roof["traffic_unit"] = "GB per launch (ncu dram read+write, profiles/r01g_traffic.json)"
-            roof["algorithmic_gb_per_launch"] = round(p["bytes"] / max(1.0, p["launches"]) / 1e9, 2)
-        roof["share_of_step"] = round(p["ms"] * 1e-3 / sum(prof_s), 4)
-        roof["measured_in"] = "profiled pass (same steps as the timed region)"
-    mv = statistics.mean(r["h2_mv_s"] for r in recs)
-    mv_flops = prof.get("kblock_dmma", {}).get("flops", 0)
-    line = {
-        "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 2), "higher_is_better": False,
-        "scaling": "strong" if comm is not None else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "l2_flush": "256 MB write between steps",
-                   "parallelism": ("h2_build, spdhss_build and every H2 product (PCG's k=1 too) sharded by subtrees over NCCL; "
-                                   "PCG vectors and HSS solve replicated"
-                                   if comm is not None else "replicas") if world > 1 else "single GPU", "N": N},
-        "breakdown": {k: round(statistics.mean(r[k] for r in recs), 4)
-                      for k in ("h2_build_s", "spdhss_build_s", "pcg_s", "h2_mv_s")},
-        "full_build_s": round(statistics.mean(r["h2_build_s"] + r["spdhss_build_s"] for r in recs), 4),
-        "pcg_iters": recs[-1]["pcg_iters"], "pcg_converged": bool(recs[-1]["converged"]),
-        "h2_rank_max": recs[-1]["h2_ranks_max"], "hss_rank_max": recs[-1]["hss_rank_max"],
-        "kernels": {k: {"launches": int(v["launches"]), "ms": round(v["ms"], 2),
-                        "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)} for k, v in prof.items()},
-        "roofline": roof,
-        "h2_multivector_sweep": sweep,
-        "hss_error_o11": round(hss_err, 6),
-        "hss_solve": hss_solve_info,
-        "h2_multivector": {"k": MV_K, "useful_gflop": round(record_flops["flops"] / 1e9, 2),
-                           "gflops": round(record_flops["flops"] / mv / 1e9, 1),
-                           "frac_fp64_peak": round(record_flops["flops"] / mv / 1e12 / fp64, 4),
-                           "counts": record_flops["counts"]},
-        "e2e": {"value": round(e2e_v, 4), "unit": "s", "h2d_bytes_per_step": int(8 * N * (CFG.d + 1)),
-                "d2h_bytes_per_step": int(8 * N)},
-        "gpu_launches": int(launches // max(1, args.steps)),
-        "profiled_pass_s_per_step": round(statistics.mean(prof_s), 4),
-        "clocks": clocks,
-    }
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(N)
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    if not prof:
+        return None
+    nm, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    avg_s = p["ms"] * 1e-3 / max(1.0, p["launches"])
+    if nm in TENSOR_BOUND or p["flops"] > 5.7 * max(p["bytes"], 1.0):
+        ach = p["flops"] / max(1.0, p["launches"]) / avg_s / 1e12
+        roof = {"kernel": nm, "bound": "tensor", "achieved": round(ach, 3), "peak": round(fp64, 2),
+                "unit": "TFLOP/s", "frac": round(ach / fp64, 4), "traffic": None, "peak_source": fp64_src}
+    else:
+        ach = p["bytes"] / max(1.0, p["launches"]) / avg_s / 1e9
+        roof = {"kernel": nm, "bound": "hbm", "achieved": round(ach, 1), "peak": peaks.get("hbm_gbs", 6550.7),
+                "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6550.7), 4), "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    tr = load_traffic(nm)
+    if tr:
+        roof["traffic"] = tr.get("gb_per_launch")
+        roof["traffic_unit"] = f"GB per launch (ncu dram read+write, {tr.get('source')})"
+    roof["algorithmic_per_launch"] = {"gflop": round(p["flops"] / max(1.0, p["launches"]) / 1e9, 3),
+                                      "gb": round(p["bytes"] / max(1.0, p["launches"]) / 1e9, 4)}
+    roof["launches"] = int(p["launches"])
+    roof["share_of_step"] = round(p["ms"] * 1e-3 / prof_total_s, 4)
+    roof["measured_in"] = "profiled pass (one step, per-launch CUDA events on the launching stream)"
+    return roof
 
 
 def main():

@@ -211,9 +211,11 @@ enum {
     SPD_Q_SHARD_WORK = 31,  /* int64[2]: nodes whose per-node work (H2: proxy ID; HSS:
                                factorisation, QRCP, bases) this process computed, and
                                the number of such nodes; equal unless sharded (§8(e)) */
-    SPD_Q_SYM_STORE = 32    /* int64[2] (H2 handle): bytes of stored symmetric k = 1 blocks on
-                               this process and their number of pieces (0 before the first
-                               k = 1 product / PCG); sharded: the blocks touching owned nodes */
+    SPD_Q_SYM_STORE = 32    /* int64[2] (H2 handle): bytes of stored symmetric blocks on this
+                               process and their number of pieces (0 before the first k = 1
+                               product / PCG, or before the first multi-vector product when
+                               the store fits SPD_STORE_FRAC = 0.25 of the free memory, and
+                               after h2_release_store); sharded: the blocks touching owned nodes */
 };
 spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
 
@@ -227,6 +229,12 @@ int spd_prof_count(void);
 /* out4 = {launches, total ms, total flops, total bytes}; returns 0 if idx valid */
 int spd_prof_get(int idx, char* name, int name_len, double* out4);
 
+/* h2_release_store: free the stored symmetric kernel blocks of h (built by the first
+ * k = 1 product / PCG within 40 % of the free memory, or on demand for multi-vector
+ * products within SPD_STORE_FRAC = 0.25 of it); products evaluate the blocks on the fly
+ * again until a later k = 1 product rebuilds it.  Synchronizes the device.
+ * SPD_EINVAL on a null handle. */
+spd_status h2_release_store(spd_h2_t h);
 void h2_free(spd_h2_t h);
 void hss_free(spd_hss_t H);
 const char* spd_last_error(void);

@@ -25,6 +25,12 @@ spd_status spd_test_qr_unpivoted(int batch, double* A, int m, int n, int ld, int
 /* proxy points of heap node `node` of an H2 handle: P host, n_proxy x d row-major
  * (d = spatial dimension; for RPY the points, not their 3 dofs each) */
 spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream);
+/* the HOST tree / list builder (tree.cpp, kept for leaves beyond the device sort) on host
+ * points: perm[n] (tree position -> original index), boxes[nnodes * 2 * d] (lo, hi per
+ * node) and list_counts[1 + 2L] (near pairs, then type1[k], type3[k] for k = 1..L), the
+ * layouts of SPD_Q_PERM / SPD_Q_BOXES / SPD_Q_LIST_COUNTS -- to check the device builder */
+spd_status spd_test_tree_host(const double* pts, int64_t n, int d, int leaf, int64_t* perm, double* boxes,
+                              int64_t* list_counts);
 /* the device Omega generator of spdhss_build (Philox4x32-10 + Box-Muller, reading R29):
  * out (device) n x w column-major, ld n, tree-order element e = row + col n */
 spd_status spd_test_philox_normal(double* out, int64_t n, int w, uint64_t seed, void* stream);

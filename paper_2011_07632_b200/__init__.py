@@ -79,6 +79,7 @@ def lib():
         "spdhss_build_adaptive": ([vp, c_int, c_int, c_double, c_int, ctypes.c_uint64, vp, vp, P(vp), P(c_int)], c_int),
         "spd_query": ([vp, c_int, vp, ctypes.c_size_t], c_int),
         "h2_free": ([vp], None),
+        "h2_release_store": ([vp], c_int),
         "hss_free": ([vp], None),
         "spd_test_gemm": ([c_int, c_int, c_int, c_int, c_int, c_double, vp, c_int, vp, c_int, c_double,
                            vp, c_int, vp], c_int),
@@ -88,6 +89,7 @@ def lib():
         "spd_test_proxies": ([vp, c_int, vp, vp], c_int),
         "spd_test_qr_unpivoted": ([c_int, vp, c_int, c_int, c_int, i64, vp], c_int),
         "spd_test_philox_normal": ([vp, i64, c_int, ctypes.c_uint64, vp], c_int),
+        "spd_test_tree_host": ([vp, i64, c_int, c_int, vp, vp, vp], c_int),
         "spd_launch_count": ([], ctypes.c_longlong),
         "spd_prof_enable": ([c_int], None),
         "spd_prof_reset": ([], None),
@@ -103,7 +105,8 @@ def lib():
 
 
 EXPORTED = ["spd_comm_unique_id", "spd_comm_init", "spd_comm_init_host", "spd_comm_free", "h2_build", "h2_matvec", "spdhss_build", "hss_solve",
-            "hss_matvec", "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error"]
+            "hss_matvec", "pcg_solve", "pcg_solve_bj", "spdhss_build_adaptive", "spd_query", "h2_free", "hss_free", "spd_last_error",
+            "h2_release_store"]
 
 
 def _check(status):
@@ -215,6 +218,10 @@ class H2:
     def shard_work(self):
         """(nodes whose per-node work this process computed, nodes with per-node work)."""
         return tuple(int(v) for v in self.query(Q_SHARD_WORK, np.int64, 2))
+
+    def release_store(self):
+        """Free the stored symmetric kernel blocks (h2_release_store)."""
+        _check(lib().h2_release_store(self.ptr))
 
     def sym_store(self):
         """(bytes, pieces) of the stored symmetric k = 1 blocks on this process."""
@@ -471,3 +478,21 @@ def philox_normal(n, w, seed):
     out = torch.empty((w, n), dtype=torch.float64, device="cuda").t()
     _check(lib().spd_test_philox_normal(ctypes.c_void_p(out.data_ptr()), int(n), int(w), int(seed), _stream()))
     return out
+
+
+def tree_host(points, leaf):
+    """Test export: the host tree / list builder on host points (n, d):
+    (perm, boxes (nnodes, 2, d), list counts (1 + 2L))."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    n, d = pts.shape
+    depth = 0
+    while int(leaf) << depth < n:
+        depth += 1
+    L, nn = depth + 1, (1 << (depth + 1)) - 1
+    perm = np.zeros(n, np.int64)
+    boxes = np.zeros((nn, 2, d))
+    counts = np.zeros(1 + 2 * L, np.int64)
+    vp = ctypes.c_void_p
+    _check(lib().spd_test_tree_host(vp(pts.ctypes.data), n, d, int(leaf), vp(perm.ctypes.data),
+                                    vp(boxes.ctypes.data), vp(counts.ctypes.data)))
+    return perm, boxes, counts

@@ -86,6 +86,16 @@ spd_status h2_build(const double* pts, int64_t n, int d, spd_kernel k, int leaf,
 
 void h2_free(spd_h2_t h) { if (h) { cudaDeviceSynchronize(); delete h; } }
 
+spd_status h2_release_store(spd_h2_t h) {
+    SPD_TRY({
+        SPD_REQUIRE(h != nullptr, "h2_release_store: null handle");
+        SPD_CUDA(cudaDeviceSynchronize());
+        h->sym = spd::H2SymStore();
+        h->stored_mode = -1;
+        h->sym_budget = 0.0;
+    })
+}
+
 spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t k,
                      void* stream) {
     SPD_TRY({
@@ -434,6 +444,29 @@ spd_status spd_test_proxies(spd_h2_t h, int node, double* P_host, void* stream) 
         std::vector<double> v = P.download(s);
         for (int p = 0; p < h->n_proxy; ++p)                // the proxy points (first dof of each)
             for (int a = 0; a < h->dim; ++a) P_host[(size_t)p * h->dim + a] = v[(size_t)a * np + (size_t)h->m * p];
+    })
+}
+
+spd_status spd_test_tree_host(const double* pts, int64_t n, int d, int leaf, int64_t* perm, double* boxes,
+                              int64_t* list_counts) {
+    SPD_TRY({
+        SPD_REQUIRE(pts && perm && boxes && list_counts && n >= 1 && (d == 2 || d == 3) && leaf >= 1,
+                    "spd_test_tree_host: bad argument");
+        TreeH t;
+        ListsH l;
+        build_tree(pts, n, d, leaf, t);
+        build_lists(t, l);
+        std::memcpy(perm, t.perm.data(), sizeof(int64_t) * n);
+        for (int i = 0; i < t.nnodes; ++i)
+            for (int a = 0; a < d; ++a) {
+                boxes[((size_t)i * 2) * d + a] = t.lo[(size_t)i * d + a];
+                boxes[((size_t)i * 2 + 1) * d + a] = t.hi[(size_t)i * d + a];
+            }
+        list_counts[0] = (int64_t)l.near.size();
+        for (int k = 1; k <= t.L; ++k) {
+            list_counts[k] = (int64_t)l.type1[k].size();
+            list_counts[t.L + k] = (int64_t)l.type3[k].size();
+        }
     })
 }
 

@@ -49,6 +49,7 @@ struct ProfCaptured;
 ProfCaptured* prof_capture_take(size_t first);   // records [first, end) of the list
 size_t prof_mark();
 void prof_update_last(const char* name, double flops, double bytes);   // latest record of that name
+bool prof_on();                                   // the per-kernel-class profiler is enabled
 void prof_accumulate(ProfCaptured* c);            // after a (synchronized) replay
 void prof_release(ProfCaptured* c);
 

@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
                 for (int j = threadIdx.x; j < n; j += QR_THREADS) d.piv[j] = j;
         }
         if (threadIdx.x == 0) { s_stop = 0; s_nu0 = 0.0; }
+        if (g == 0 && threadIdx.x == 0) d.rank[0] = -1;     // "running" (published by the barrier)
         group_barrier(bar, G);
         for (int t = 0;; ++t) {
             const bool trc = (item.desc == 0 && g == 0 && t == 100 && threadIdx.x == 0);
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
                     for (int i = t + 1 + threadIdx.x; i < m; i += QR_THREADS) ct[i] = (sig == 0.0) ? 0.0 : ct[i] * inv0;
                     if (threadIdx.x == 0) { ct[t] = mu; d.beta[t] = beta; }
                 } else if (threadIdx.x == 0) {
-                    d.rank[0] = t;                  // stop: publish the rank (host set -1)
+                    d.rank[0] = t;                  // stop: publish the rank (-1 while running)
                 }
                 __syncthreads();
             }
@@ -901,6 +902,29 @@ __global__ void __launch_bounds__(256) qrcp_smem_kernel(const QrcpDesc* __restri
     if (tid == 0) d.rank[0] = rank;
 }
 
+__global__ void gather_ranks_kernel(const QrcpDesc* __restrict__ d, int n, int* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = *d[i].rank;
+}
+
+// algorithmic work of the QRCPs just enqueued (profiling only; ranks read back): with
+// recomputed norms (R4) step t must read every entry of the trailing (m-t) x (n-t)
+// block once -- 8 B per entry (the minimal traffic) and 6 flops (norm, dot, update)
+static void qrcp_prof_exact(cudaStream_t s, const std::vector<QrcpDesc>& d, const QrcpDesc* dd) {
+    if (!prof_on()) return;
+    DBuf<int> rk(d.size());
+    gather_ranks_kernel<<<ceil_div((int64_t)d.size(), 256), 256, 0, s>>>(dd, (int)d.size(), rk.p);
+    std::vector<int> r = rk.download(s);
+    double by = 0.0, fl = 0.0;
+    for (size_t i = 0; i < d.size(); ++i)
+        for (int t = 0; t <= std::min(r[i], std::min(d[i].m, d[i].n) - 1); ++t) {   // + the stopping step's norms
+            const double e = (double)(d[i].m - t) * (d[i].n - t);
+            by += 8.0 * e;
+            fl += 6.0 * e;
+        }
+    prof_update_last("qrcp", fl, by);
+}
+
 void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol) {
     if (d.empty()) return;
     {
@@ -915,11 +939,14 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
             double fl = 0;
             for (auto& q : d) fl += 4.0 * q.m * q.n * std::min(std::min(q.m, q.n), q.max_rank);
             DevArray<QrcpDesc> dd(s, d);
-            ProfScope prof(s, "qrcp", fl, 0);
-            for (size_t off = 0; off < d.size(); off += 65535) {
-                qrcp_smem_kernel<<<(unsigned)std::min<size_t>(65535, d.size() - off), 256, need, s>>>(dd.p + off, rel_tol);
-                SPD_LAUNCH();
+            {
+                ProfScope prof(s, "qrcp", fl, 0);
+                for (size_t off = 0; off < d.size(); off += 65535) {
+                    qrcp_smem_kernel<<<(unsigned)std::min<size_t>(65535, d.size() - off), 256, need, s>>>(dd.p + off, rel_tol);
+                    SPD_LAUNCH();
+                }
             }
+            qrcp_prof_exact(s, d, dd.p);
             return;
         }
     }
@@ -946,70 +973,92 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
         work[i] = (double)std::max(d[i].m, 1) * std::max(d[i].n, 1) * k;
         total += work[i];
     }
-    std::vector<QrItem> items;
-    std::vector<int2> cta;
-    if ((int)d.size() >= cap) {
-        // one CTA per matrix, CTAs loop over matrices (largest first, greedy balance)
-        std::vector<int> order(d.size());
-        for (size_t i = 0; i < d.size(); ++i) order[i] = (int)i;
-        std::sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-        std::vector<std::vector<int>> bins(cap);
-        std::vector<double> load(cap, 0.0);
-        for (int i : order) {
-            int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-            bins[b].push_back(i);
-            load[b] += work[i];
-        }
-        for (int b = 0; b < cap; ++b) {
-            int begin = (int)items.size();
-            for (int i : bins[b]) items.push_back({i, 0, 1});
-            cta.push_back(make_int2(begin, (int)items.size()));
-        }
-    } else {
-        int spare = cap - (int)d.size();
-        std::vector<int> G(d.size(), 1);
-        for (size_t i = 0; i < d.size(); ++i) {
-            int extra = (int)(spare * (work[i] / total));
-            int maxg = std::max(1, std::min(d[i].n, 64));
-            G[i] = std::min(maxg, 1 + extra);
-        }
-        for (size_t i = 0; i < d.size(); ++i)
-            for (int g = 0; g < G[i]; ++g) {
-                cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
-                items.push_back({(int)i, g, G[i]});
-            }
-    }
-    double fl = 0, by = 0;
-    for (size_t i = 0; i < d.size(); ++i) { fl += 4.0 * work[i]; by += 8.0 * d[i].m * d[i].n; }
     DevArray<QrcpDesc> dd(s, d);
-    DevArray<QrItem> di(s, items);
-    DevArray<int2> dc(s, cta);
     unsigned* bars = nullptr;
     SPD_CUDA(cudaMallocAsync((void**)&bars, sizeof(unsigned) * 2 * d.size(), s));
     SPD_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * d.size(), s));
-    // rank = -1 marks "running"
-    std::vector<int> minus1(1, -1);
-    for (auto& q : d) SPD_CUDA(cudaMemcpyAsync(q.rank, minus1.data(), sizeof(int), cudaMemcpyHostToDevice, s));
-    SPD_CUDA(cudaStreamSynchronize(s));
-    const QrcpDesc* a0 = dd.p;
-    const QrItem* a1 = di.p;
-    const int2* a2 = dc.p;
-    double tol = rel_tol;
-    void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
-    ProfScope prof(s, "qrcp", fl, by);     // flops: upper bound 4 m n kmax (rank unknown at launch)
-    SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
-                                         args, qsmem, s));
+    // L2-resident rounds (env SPD_QRCP_L2MB = budget in MB, 0 = one round): matrices in
+    // rounds whose working sets fit the budget, each round with all CTAs, so the per-step
+    // re-reads of the trailing matrices hit L2 instead of HBM
+    const char* l2e = getenv("SPD_QRCP_L2MB");
+    const double l2b = l2e ? atof(l2e) * 1e6 : 0.0;
+    std::vector<std::vector<int>> rounds;
+    if (l2b > 0.0) {
+        std::vector<int> order(d.size());
+        for (size_t i = 0; i < d.size(); ++i) order[i] = (int)i;
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+        double acc = 0.0;
+        for (int i : order) {
+            const double b = 8.0 * d[i].m * d[i].n;
+            if (rounds.empty() || acc + b > l2b || (int)rounds.back().size() >= cap) { rounds.push_back({}); acc = 0.0; }
+            rounds.back().push_back(i);
+            acc += b;
+        }
+    } else {
+        rounds.push_back({});
+        for (size_t i = 0; i < d.size(); ++i) rounds.back().push_back((int)i);
+    }
+    double fl = 0, by = 0;
+    for (size_t i = 0; i < d.size(); ++i) { fl += 4.0 * work[i]; by += 8.0 * d[i].m * d[i].n; }
+    {
+        ProfScope prof(s, "qrcp", fl, by);     // exact counts filled in by qrcp_prof_exact (profiling)
+        for (const auto& rd : rounds) {
+        double rtotal = 0.0;
+        for (int i : rd) rtotal += work[i];
+        std::vector<QrItem> items;
+        std::vector<int2> cta;
+        if ((int)rd.size() >= cap) {
+            // one CTA per matrix, CTAs loop over matrices (largest first, greedy balance)
+            std::vector<int> order(rd);
+            std::sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+            std::vector<std::vector<int>> bins(cap);
+            std::vector<double> load(cap, 0.0);
+            for (int i : order) {
+                int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+                bins[b].push_back(i);
+                load[b] += work[i];
+            }
+            for (int b = 0; b < cap; ++b) {
+                int begin = (int)items.size();
+                for (int i : bins[b]) items.push_back({i, 0, 1});
+                cta.push_back(make_int2(begin, (int)items.size()));
+            }
+        } else {
+            int spare = cap - (int)rd.size();
+            const int gmax = l2b > 0.0 ? 128 : 64;
+            for (int i : rd) {
+                int extra = (int)(spare * (work[i] / rtotal));
+                int maxg = std::max(1, std::min(d[i].n, gmax));
+                const int G = std::min(maxg, 1 + extra);
+                for (int g = 0; g < G; ++g) {
+                    cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
+                    items.push_back({i, g, G});
+                }
+            }
+        }
+        DevArray<QrItem> di(s, items);
+        DevArray<int2> dc(s, cta);
+        const QrcpDesc* a0 = dd.p;
+        const QrItem* a1 = di.p;
+        const int2* a2 = dc.p;
+        double tol = rel_tol;
+        void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
+        SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
+                                             args, qsmem, s));
+        count_launch();
+        }
+    }
     static const bool trace = getenv("SPD_QR_TRACE") != nullptr;
     if (trace) {
         unsigned long long tr[16];
         SPD_CUDA(cudaStreamSynchronize(s));
         SPD_CUDA(cudaMemcpyFromSymbol(tr, g_qr_trace, sizeof(tr), 10 * sizeof(unsigned long long)));
-        fprintf(stderr, "[qrcp trace] %zu mats, %zu CTAs, m %d n %d: leader %.2f bar1 %.2f update %.2f bar2 %.2f us\n",
-                d.size(), cta.size(), d[0].m, d[0].n, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3,
+        fprintf(stderr, "[qrcp trace] %zu mats, %zu rounds, m %d n %d: leader %.2f bar1 %.2f update %.2f bar2 %.2f us\n",
+                d.size(), rounds.size(), d[0].m, d[0].n, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3,
                 (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3);
     }
-    count_launch();
     SPD_CUDA(cudaFreeAsync(bars, s));
+    qrcp_prof_exact(s, d, dd.p);
 }
 
 // ================================================================= unpivoted blocked QR

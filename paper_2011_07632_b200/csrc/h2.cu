@@ -198,6 +198,11 @@ __global__ void int_copy_kernel(const IntCopy* __restrict__ d) {
     for (int i = threadIdx.x; i < c.n; i += blockDim.x) c.dst[i] = c.src[i];
 }
 
+__global__ void check_finite_kernel(const double* x, int64_t n, int* bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[e])) *bad = 1;
+}
+
 // ================================================================= build
 static double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -208,13 +213,22 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
     const int64_t npts = N / h->m;
     const int d = h->d, dim = h->dim, m = h->m;
     double t0 = now_s();
-    // --- tree + lists (host metadata; R1, R2) on the points, then over dofs (R28)
-    std::vector<double> pts((size_t)npts * dim);
-    SPD_CUDA(cudaMemcpyAsync(pts.data(), pts_dev, sizeof(double) * npts * dim, cudaMemcpyDeviceToHost, s));
-    SPD_CUDA(cudaStreamSynchronize(s));
-    for (double v : pts) SPD_REQUIRE(std::isfinite(v), "h2_build: non-finite point coordinate");
-    build_tree(pts.data(), npts, dim, h->leaf, h->tree);
-    build_lists(h->tree, h->lists);
+    // --- tree + lists (R1, R2) on the points, built on the device (tree_dev.cu), then
+    // over dofs (R28); the host builder only for leaves beyond the shared-memory sort
+    {
+        DBuf<int> bad(1);
+        bad.zero(s);
+        check_finite_kernel<<<148 * 4, 256, 0, s>>>(pts_dev, npts * dim, bad.p);
+        SPD_LAUNCH();
+        SPD_REQUIRE(bad.download(s)[0] == 0, "h2_build: non-finite point coordinate");
+    }
+    if (!build_tree_device(pts_dev, npts, dim, h->leaf, h->tree, s)) {
+        std::vector<double> pts((size_t)npts * dim);
+        SPD_CUDA(cudaMemcpyAsync(pts.data(), pts_dev, sizeof(double) * npts * dim, cudaMemcpyDeviceToHost, s));
+        SPD_CUDA(cudaStreamSynchronize(s));
+        build_tree(pts.data(), npts, dim, h->leaf, h->tree);
+    }
+    build_lists_device(h->tree, h->lists, s);
     expand_dofs(h->tree, m);
     const TreeH& t = h->tree;
     const int L = t.L;
@@ -584,13 +598,14 @@ void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {
 // no kernel evaluation, the blocks stream from HBM and the DMMA contraction is unchanged.
 // largest store built on demand for products, as a fraction of the free memory (env
 // SPD_STORE_FRAC); the SPD-HSS build that usually follows needs its own workspaces
+// (read on every call, so tests and tools can switch it per product)
 static double store_frac_limit() {
-    static const double f = getenv("SPD_STORE_FRAC") ? atof(getenv("SPD_STORE_FRAC")) : 0.5;
-    return f;
+    const char* e = getenv("SPD_STORE_FRAC");
+    return e ? atof(e) : 0.25;
 }
 
 bool h2_store_for_products(spd_h2_s* h, cudaStream_t s, bool build) {
-    static const bool eval = getenv("SPD_MV_EVAL") != nullptr;
+    const bool eval = getenv("SPD_MV_EVAL") != nullptr;
     if (eval || h->tree.L < 2) return false;
     if (h->sym.built) return !h->sym.base.empty();
     // built here only when it is small next to the free memory (the SPD-HSS build that

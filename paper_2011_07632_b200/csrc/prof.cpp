@@ -135,6 +135,8 @@ ProfScope::~ProfScope() {
     if (!ext && g_recs.size() > 20000) drain();
 }
 
+bool prof_on() { return g_on; }
+
 void prof_update_last(const char* name, double flops, double bytes) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t i = g_recs.size(); i-- > 0;)

@@ -39,5 +39,12 @@ struct ListsH {
 void build_tree(const double* pts, int64_t N, int d, int leaf, TreeH& t);
 bool is_far(const TreeH& t, int i, int j);
 void build_lists(const TreeH& t, ListsH& l);
+#ifdef __CUDACC__
+// device builders (tree_dev.cu): pts = DEVICE N x d row-major; same
+// result as build_tree / build_lists.  build_tree_device returns false (nothing built)
+// when a last-level node exceeds the shared-memory sort (leaf > 2048): use the host one.
+bool build_tree_device(const double* pts, int64_t N, int d, int leaf, TreeH& t, cudaStream_t s);
+void build_lists_device(const TreeH& t, ListsH& l, cudaStream_t s);
+#endif
 
 }  // namespace spd

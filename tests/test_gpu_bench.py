@@ -14,8 +14,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_bench_json_contract():
+    # the step's workload at N = 2^16 (the C4 / C5 recipes scaled down) to keep the test short
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "3",
-                          "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+                          "--no-cpu-baseline", "--n", "65536"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -35,7 +37,9 @@ def test_bench_json_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["clocks"]["samples"] > 0 and d["clocks"]["sm_max_mhz"] > 0
-    assert d["pcg_converged"] is True
+    assert d["pcg_c4"]["converged"] is True and d["pcg_c4"]["iters"] > 0
+    assert d["config"]["N"] == 65536 and set(d["breakdown"]) == {"h2_build_s", "spdhss_build_s", "c5_mv_s", "h2_tree_lists_s"}
     sw = d["h2_multivector_sweep"]
     assert set(sw) == {"1", "16", "64", "256"} and all(v["useful_tflops"] > 0 for v in sw.values())
+    assert sw["1"]["first_call_ms_incl_store_build"] >= sw["1"]["ms"]
     assert 0.0 < d["hss_error_o11"] < 1.0

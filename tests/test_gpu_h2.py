@@ -150,3 +150,16 @@ def test_h2_full_c2_sampled_rows(spd):
     err = np.linalg.norm(y[rows] - ref) / np.linalg.norm(ref)
     print("C2 sampled-row H2 error", err, "ranks", np.bincount(h.ranks())[:0], h.timings()[:2])
     assert err <= 10 * cfg.h2_tol
+
+
+@pytest.mark.parametrize("cfg", [synth.C4, synth.C3, synth.C1.scaled(3001, leaf=40)], ids=["C4", "C3", "ragged2D"])
+def test_device_tree_lists_equal_host_builder_full_size(spd, cfg):
+    """K12: the device tree and dual-tree lists (tree_dev.cu) at full size (N = 2^20 for
+    C4/C5) equal the host builder (tree.cpp), itself bit-exact with the oracle above."""
+    import torch
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, 1e-3)
+    perm, boxes, counts = spd.tree_host(X, cfg.leaf)
+    np.testing.assert_array_equal(h.perm, perm)
+    np.testing.assert_array_equal(h.boxes(), boxes)
+    np.testing.assert_array_equal(h.list_counts(), counts)
