@@ -1275,28 +1275,7 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
     cluster.sync();                                   // keep smem alive for remote readers
 }
 
-void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
-    if (d.empty()) return;
-    // Panels are taken in pairs A = [p, p + 32), B = [p + 32, p + 64): A is factored, its
-    // reflectors update B's columns only, B is factored, and the rest of the trailing
-    // matrix gets ONE update with the combined 64-column compact-WY factor
-    //   I - [V_A V_B] [T_A, -T_A (V_A^T V_B) T_B; 0, T_B] [V_A V_B]^T
-    // (Schreiber-Van Loan), halving the trailing-matrix traffic of the 32-wide scheme.
-    constexpr int QB2 = 2 * QB;
-    int nmax = 0;
-    size_t vtot = 0, wtot = 0;
-    std::vector<size_t> voff(d.size()), woff(d.size());
-    for (size_t i = 0; i < d.size(); ++i) {
-        nmax = std::max(nmax, d[i].n);
-        voff[i] = vtot; vtot += (size_t)d[i].m * QB2;
-        woff[i] = wtot; wtot += (size_t)QB2 * d[i].n;
-    }
-    const size_t nd = d.size();
-    DBuf<double> V(vtot), TA(nd * QB * QB), TB(nd * QB * QB), TAB(nd * QB2 * QB2), S(nd * QB * QB),
-        X(nd * QB * QB), W(wtot), W2(wtot);
-    double fl = 0;
-    for (auto& q : d) fl += 2.0 * q.m * q.n * q.n - 2.0 / 3.0 * q.n * q.n * q.n;
-    auto launch_panels = [&](const std::vector<PanelDesc>& pd, int p) {
+static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int p) {
         if (pd.empty()) return;
         {
             DevArray<PanelDesc> dp(s, pd);
@@ -1343,7 +1322,115 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
                 SPD_LAUNCH();
             }
         }
-    };
+    }
+
+// Blocks of NP panels (NP x 32 columns): panel s is updated by the reflectors of panels
+// 0..s-1 of its block (combined compact-WY factor T_{0:s}), factored, and T is extended
+// (Schreiber-Van Loan: T_{0:s+1} = [T_{0:s}, -T_{0:s} V_{0:s}^T V_s T_s; 0, T_s]); the
+// rest of the trailing matrix gets ONE rank-(32 NP) update per block, so its traffic is
+// 1/NP of the column-by-panel scheme and the far GEMMs have K = 32 NP.
+static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP) {
+    const int KB = NP * QB;
+    int nmax = 0;
+    size_t vtot = 0, wtot = 0;
+    std::vector<size_t> voff(d.size()), woff(d.size());
+    for (size_t i = 0; i < d.size(); ++i) {
+        nmax = std::max(nmax, d[i].n);
+        voff[i] = vtot; vtot += (size_t)d[i].m * KB;
+        woff[i] = wtot; wtot += (size_t)KB * std::max(d[i].n, QB);
+    }
+    const size_t nd = d.size();
+    DBuf<double> V(vtot), T(nd * KB * KB), Ts(nd * QB * QB), S(nd * KB * QB), X(nd * KB * QB), W(wtot), W2(wtot);
+    for (int p = 0; p < nmax; p += KB) {
+        V.zero(s);                                    // rows above each panel's start must be 0
+        T.zero(s);
+        std::vector<int> kacc(nd, 0);                 // reflector columns of the block so far
+        std::vector<int> done(nd, 0);                 // columns of the block already handled
+        for (int sp = 0; sp < NP; ++sp) {
+            std::vector<GemmDesc> u1, u2, u3, e1, e2, e3;
+            std::vector<PanelDesc> pd;
+            std::vector<CopyDesc> cp;
+            for (size_t i = 0; i < nd; ++i) {
+                const QrDesc& q = d[i];
+                const int kk = std::min(q.n, q.m);
+                const int ps = p + done[i];
+                if (ps >= q.n || done[i] < sp * QB) continue;       // block ended early for this matrix
+                const int ncols = std::min(QB, q.n - ps);
+                const int jb = std::max(0, std::min(QB, kk - ps));
+                const int K = kacc[i], L = q.m - p;
+                double* Vb = V.p + voff[i];
+                double* Tb = T.p + i * KB * KB;
+                double* As = q.A + p + (size_t)ps * q.ld;              // rows from p
+                if (K > 0) {                                            // in-block update of panel sp
+                    u1.push_back({Vb, As, W.p + woff[i], K, ncols, L, q.m, q.ld, KB});
+                    u2.push_back({Tb, W.p + woff[i], W2.p + woff[i], K, ncols, K, KB, KB, KB});
+                    u3.push_back({Vb, W2.p + woff[i], As, L, ncols, K, q.m, KB, q.ld});
+                }
+                done[i] += ncols;
+                if (jb <= 0) continue;
+                double* Vs = Vb + (size_t)K * q.m + (ps - p);
+                pd.push_back({q.A, q.m, q.n, q.ld, ps, jb, Vs, q.m, Ts.p + i * QB * QB});
+                if (K > 0) {                                            // extend T
+                    const int Ls = q.m - ps;
+                    e1.push_back({Vb + (ps - p), Vs, S.p + i * KB * QB, K, jb, Ls, q.m, q.m, KB});
+                    e2.push_back({Tb, S.p + i * KB * QB, X.p + i * KB * QB, K, jb, K, KB, KB, KB});
+                    e3.push_back({X.p + i * KB * QB, Ts.p + i * QB * QB, Tb + (size_t)K * KB, K, jb, jb, KB, QB, KB});
+                }
+                cp.push_back({Ts.p + i * QB * QB, Tb + K + (size_t)K * KB, jb, jb, QB, KB, 0});
+                kacc[i] = K + jb;
+            }
+            gemm_batched(s, u1, true, false, 1.0, 0.0);
+            gemm_batched(s, u2, true, false, 1.0, 0.0);
+            gemm_batched(s, u3, false, false, -1.0, 1.0);
+            launch_panels(s, pd, p + sp * QB);
+            gemm_batched(s, e1, true, false, 1.0, 0.0);
+            gemm_batched(s, e2, false, false, 1.0, 0.0);
+            gemm_batched(s, e3, false, false, -1.0, 0.0);
+            copy_batched(s, cp, 1.0, false);
+        }
+        // far columns: one rank-K update with the block's combined factor
+        std::vector<GemmDesc> g1, g2, g3;
+        for (size_t i = 0; i < nd; ++i) {
+            const QrDesc& q = d[i];
+            const int pf = p + done[i], nt = q.n - pf, K = kacc[i], L = q.m - p;
+            if (nt <= 0 || K <= 0 || p >= q.n) continue;
+            double* Af = q.A + p + (size_t)pf * q.ld;
+            g1.push_back({V.p + voff[i], Af, W.p + woff[i], K, nt, L, q.m, q.ld, KB});
+            g2.push_back({T.p + i * KB * KB, W.p + woff[i], W2.p + woff[i], K, nt, K, KB, KB, KB});
+            g3.push_back({V.p + voff[i], W2.p + woff[i], Af, L, nt, K, q.m, KB, q.ld});
+        }
+        gemm_batched(s, g1, true, false, 1.0, 0.0);
+        gemm_batched(s, g2, true, false, 1.0, 0.0);
+        gemm_batched(s, g3, false, false, -1.0, 1.0);
+    }
+    SPD_CUDA(cudaStreamSynchronize(s));
+}
+
+void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
+    if (d.empty()) return;
+    if (const char* e = getenv("SPD_QR_NP")) {
+        const int np = atoi(e);
+        if (np >= 1 && np <= 8 && np != 2) { qr_blocked_np(s, d, np); return; }
+    }
+    // Panels are taken in pairs A = [p, p + 32), B = [p + 32, p + 64): A is factored, its
+    // reflectors update B's columns only, B is factored, and the rest of the trailing
+    // matrix gets ONE update with the combined 64-column compact-WY factor
+    //   I - [V_A V_B] [T_A, -T_A (V_A^T V_B) T_B; 0, T_B] [V_A V_B]^T
+    // (Schreiber-Van Loan), halving the trailing-matrix traffic of the 32-wide scheme.
+    constexpr int QB2 = 2 * QB;
+    int nmax = 0;
+    size_t vtot = 0, wtot = 0;
+    std::vector<size_t> voff(d.size()), woff(d.size());
+    for (size_t i = 0; i < d.size(); ++i) {
+        nmax = std::max(nmax, d[i].n);
+        voff[i] = vtot; vtot += (size_t)d[i].m * QB2;
+        woff[i] = wtot; wtot += (size_t)QB2 * d[i].n;
+    }
+    const size_t nd = d.size();
+    DBuf<double> V(vtot), TA(nd * QB * QB), TB(nd * QB * QB), TAB(nd * QB2 * QB2), S(nd * QB * QB),
+        X(nd * QB * QB), W(wtot), W2(wtot);
+    double fl = 0;
+    for (auto& q : d) fl += 2.0 * q.m * q.n * q.n - 2.0 / 3.0 * q.n * q.n * q.n;
     for (int p = 0; p < nmax; p += QB2) {
         V.zero(s);                                    // V_B's rows above its panel must be 0
         TAB.zero(s);
@@ -1391,11 +1478,11 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
             g2.push_back({TAB.p + i * QB2 * QB2, W.p + woff[i], W2.p + woff[i], K, nt, K, QB2, QB2, QB2});
             g3.push_back({V.p + voff[i], W2.p + woff[i], Af, L, nt, K, q.m, QB2, q.ld});
         }
-        launch_panels(pa, p);
+        launch_panels(s, pa, p);
         gemm_batched(s, n1, true, false, 1.0, 0.0);
         gemm_batched(s, n2, true, false, 1.0, 0.0);
         gemm_batched(s, n3, false, false, -1.0, 1.0);
-        launch_panels(pb, p + QB);
+        launch_panels(s, pb, p + QB);
         gemm_batched(s, gs, true, false, 1.0, 0.0);
         gemm_batched(s, gx, false, false, 1.0, 0.0);
         gemm_batched(s, gt, false, false, -1.0, 0.0);

@@ -36,14 +36,14 @@ __device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
 // with the 16 x NC slice of X; the next chunk's X slice and coordinates are
 // prefetched into registers while the current chunk is evaluated/contracted.
 template <int KID, int NC>
-__global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : 256 / NC) kblock_kernel(
+__global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : (NC == 160 ? 1 : 256 / NC)) kblock_kernel(
     KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
     const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
     const KbWork* __restrict__ work, double* __restrict__ partial) {
     constexpr int NT = 2 * NC;                  // threads
     constexpr int WN = NC / 32;                 // warps along columns
     constexpr int XPT = KB_K * NC / NT;         // X values per thread per chunk (= 8)
-    constexpr int EPT = KB_M * KB_K / NT;       // kernel evaluations per thread per chunk
+    constexpr int EST = NT / KB_M;              // kernel-tile columns kc = tid / 64 + EST u (NC / 32 of them)
     __shared__ double Ks[KB_K][KB_M + 8];            // row stride = 8 (mod 16) doubles: fragment reads in 2 wavefronts
     __shared__ double Xs[NC][KB_K + 4];              // kc contiguous: conflict-free writes and reads
     __shared__ double Sx[4][KB_K];                   // coordinates (RPY: + component row)
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : 256 / NC) kblock_kernel
     double* part = wk.pslot >= 0 ? partial + (size_t)wk.pslot * KB_M * NC : nullptr;
     const int r0 = wk.tm * KB_M, c0 = wk.tn * NC;
     const int nrows = min(KB_M, tb.n - r0);
-    const int er = tid & (KB_M - 1), ec0 = (tid / KB_M) * EPT;
+    const int er = tid & (KB_M - 1), ec0 = tid / KB_M;
     double rx[4] = {0.0, 0.0, 0.0, 0.0};
     if (er < nrows)
         for (int a = 0; a < d; ++a) rx[a] = tb.x[(size_t)a * tb.ds + r0 + er];
@@ -101,8 +101,7 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : 256 / NC) kblock_kernel
                 if (k0 + KB_K < sb.n) load(k0 + KB_K);          // prefetch the next chunk
                 if (en.kmode == 0) {
 #pragma unroll
-                    for (int c = 0; c < EPT; ++c) {
-                        const int kc = ec0 + c;
+                    for (int kc = ec0; kc < KB_K; kc += EST) {
                         const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
                         double kv;
                         if constexpr (KID == SPD_K_RPY) kv = rpy_entry(kp, d0, d1, d2, (int)rx[3], (int)Sx[3][kc]);
@@ -112,17 +111,19 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : 256 / NC) kblock_kernel
                     }
                 } else {                          // stored block (symmetric store): loads only
                     const int r = r0 + er;
+                    constexpr int EPT = (KB_K + EST - 1) / EST;
                     double kv[EPT];
 #pragma unroll
                     for (int c = 0; c < EPT; ++c) {
-                        const int kc = ec0 + c, cc = k0 + kc;
+                        const int kc = ec0 + c * EST, cc = k0 + kc;
                         const double* a = en.kmode == 1
                             ? en.kst + (size_t)(r >> 5) * 32 * en.kld + (size_t)cc * 32 + (r & 31)
                             : en.kst + (size_t)(cc >> 5) * 32 * en.kld + (size_t)r * 32 + (cc & 31);
-                        kv[c] = (er < nrows && kc < nk) ? __ldg(a) : 0.0;
+                        kv[c] = (kc < KB_K && er < nrows && kc < nk) ? __ldg(a) : 0.0;
                     }
 #pragma unroll
-                    for (int c = 0; c < EPT; ++c) Ks[ec0 + c][er] = kv[c];
+                    for (int c = 0; c < EPT; ++c)
+                        if (ec0 + c * EST < KB_K) Ks[ec0 + c * EST][er] = kv[c];
                 }
                 __syncthreads();
 #pragma unroll
@@ -324,7 +325,9 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     }
     int maxc_all = 0;
     for (auto& e : entries) maxc_all = std::max(maxc_all, e.ncols);
-    const int NC = maxc_all > 64 ? 128 : (maxc_all > 32 ? 64 : 32);   // column tile >= k for k <= 128
+    // column tile matched to the width (k <= 160 in one tile: every kernel tile is evaluated
+    // once per product; wider products take 128-column tiles)
+    const int NC = maxc_all > 160 ? 128 : maxc_all > 128 ? 160 : maxc_all > 64 ? 128 : (maxc_all > 32 ? 64 : 32);
     // work items; a target whose entries (one output group) hold many more source
     // points than the average item is cut into segments at entry boundaries, so the
     // long top-level coupling lists spread over many CTAs (ordered reduction after)
@@ -400,7 +403,8 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     ProfScope prof(s, "kblock_dmma", fl, by);
     const unsigned nb = (unsigned)work.size();
 #define SPD_KB_LAUNCH(KID)                                                                                    \
-    if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
+    if (NC == 160) kblock_kernel<KID, 160><<<nb, 320, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
+    else if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
     else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); \
     else kblock_kernel<KID, 32><<<nb, 64, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
     switch (kp.id) {
@@ -414,7 +418,8 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     SPD_LAUNCH();
     if (!red.empty()) {
         DevArray<KbRed> dr(s, red);
-        if (NC == 128) kb_reduce_kernel<128><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        if (NC == 160) kb_reduce_kernel<160><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+        else if (NC == 128) kb_reduce_kernel<128><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
         else if (NC == 64) kb_reduce_kernel<64><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
         else kb_reduce_kernel<32><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
         SPD_LAUNCH();

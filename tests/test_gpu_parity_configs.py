@@ -166,18 +166,20 @@ def _own_h2_identical(c):
 
 @pytest.mark.parametrize("name", HSS_CASES)
 def test_pcg_iterations(spd, name):
-    """+-1 iteration (north star), widened only by the oracle's own drift between two
-    summation orders of its product (golden pcg_iters vs pcg_iters_reversed, R24)."""
+    """+-1 iteration (north star), widened only by the oracle's own drift over other
+    summation orders of its product (golden pcg_iters vs the reversed and shuffled
+    orders, R24)."""
     c = case(spd, name)
     cfg, g = c["cfg"], c["g"]
     b = synth.rhs(cfg)
     it_o, it_rev = int(g["pcg_iters"]), int(g["pcg_iters_reversed"])
-    window = max(1, abs(it_o - it_rev))
+    others = [it_rev] + [int(v) for v in g.get("pcg_iters_shuffled", [])]
+    window = max([1] + [abs(it_o - v) for v in others])
     for which_h, which_H in (("hi", "H"), ("h", "Hn")):
         if which_h == "h" and not _own_h2_identical(c):
             continue
         x, rep = spd.pcg_solve(c[which_h], c[which_H], cuda(b), tol=cfg.pcg_tol, maxit=20000)
-        print(f"{name} ({which_h}): GPU {rep.iters} iterations, oracle {it_o} / {it_rev} (reversed order)")
+        print(f"{name} ({which_h}): GPU {rep.iters} iterations, oracle {it_o}, other summation orders {others}")
         assert rep.converged and bool(g["pcg_converged"])
         assert abs(rep.iters - it_o) <= window, (rep.iters, it_o, it_rev)
         assert rel(host(x), g["pcg_x"]) <= 1e-6
