@@ -1158,20 +1158,20 @@ __device__ __forceinline__ void qr_tr0(int k) {        // CTA 0 only
     if (blockIdx.x == 0 && threadIdx.x == 0) qr_tr(k);
 }
 
-template <int QCL>
+template <int QCL, int PW>
 __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* descs, int rp) {
     cg::cluster_group cluster = cg::this_cluster();
     const int g = (int)cluster.block_rank();
     const PanelDesc d = descs[blockIdx.x / QCL];
-    extern __shared__ double sm[];                    // rp x QB panel slice (col-major, ld rp)
-    constexpr int NP = 2 * QB + 2;                    // partials per column
-    __shared__ double part[2][NP];                    // [0..QB): A_ij A_ic (c = j: sigma), [QB..2QB): V_ia A_ij,
+    extern __shared__ double sm[];                    // rp x PW panel slice (col-major, ld rp)
+    constexpr int NP = 2 * PW + 2;                    // partials per column
+    __shared__ double part[2][NP];                    // [0..PW): A_ij A_ic (c = j: sigma), [PW..2QB): V_ia A_ij,
                                                       // [2QB]: x0 (row-j owner), row-j values in rowv
-    __shared__ double rowv[2][2 * QB];                // row j: A_jc (c > j) and V_ja (a < j), owner CTA only
-    __shared__ double T[QB][QB + 1];
-    __shared__ double vtv[QB];
-    __shared__ double wc[QB];
-    __shared__ double tot[NP + 2 * QB];               // their sums
+    __shared__ double rowv[2][2 * PW];                // row j: A_jc (c > j) and V_ja (a < j), owner CTA only
+    __shared__ double T[PW][PW + 1];
+    __shared__ double vtv[PW];
+    __shared__ double wc[PW];
+    __shared__ double tot[NP + 2 * PW];               // their sums
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int L = d.m - d.p, jb = d.jb;
     const int r0 = g * rp, nr = max(0, min(rp, L - r0));
@@ -1191,10 +1191,10 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
         const int buf = j & 1;
         const double* colj = sm + j * rp;
         // ---- partial sums over my rows i > j (warp w: entries e = w, w + 8, ...)
-        //      e < QB: column c = j + e (c == j: sigma);  QB <= e < QB + j: reflector a = e - QB
-        for (int e = warp; e < QB + j; e += (int)(blockDim.x >> 5)) {
+        //      e < PW: column c = j + e (c == j: sigma);  PW <= e < PW + j: reflector a = e - PW
+        for (int e = warp; e < PW + j; e += (int)(blockDim.x >> 5)) {
             double acc = 0.0;
-            const double* other = e < QB ? (j + e < jb ? sm + (j + e) * rp : nullptr) : sm + (e - QB) * rp;
+            const double* other = e < PW ? (j + e < jb ? sm + (j + e) * rp : nullptr) : sm + (e - PW) * rp;
             if (other)
                 for (int i = lane; i < nr; i += 32)
                     if (r0 + i > j) acc += colj[i] * other[i];
@@ -1206,16 +1206,16 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
         if (own) {
             const int lj = j - r0;
             for (int c = threadIdx.x; c < jb; c += blockDim.x) rowv[buf][c] = sm[lj + c * rp];          // A_jc
-            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][QB + a] = sm[lj + a * rp];      // V_ja
+            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][PW + a] = sm[lj + a * rp];      // V_ja
         } else {
             for (int c = threadIdx.x; c < jb; c += blockDim.x) rowv[buf][c] = 0.0;
-            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][QB + a] = 0.0;
+            for (int a = threadIdx.x; a < j; a += blockDim.x) rowv[buf][PW + a] = 0.0;
         }
         cluster.sync();
         // ---- sum every entry over the CTAs in rank order (same bits in every CTA):
         //      thread e issues its QCL remote (DSMEM) loads at once
         {
-            constexpr int NE = NP + 2 * QB;
+            constexpr int NE = NP + 2 * PW;
             for (int e = threadIdx.x; e < NE; e += blockDim.x) {
                 const double* base = e < NP ? &part[buf][e] : &rowv[buf][e - NP];
                 double v[QCL];
@@ -1239,7 +1239,7 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
         const double inv0 = (sig == 0.0) ? 0.0 : 1.0 / v0;
         // w_c = A_jc + d_c / v0 (c > j);  V^T v_j [a] = V_ja + g_a / v0 (a < j)
         for (int c = j + 1 + threadIdx.x; c < jb; c += blockDim.x) wc[c] = tot[NP + c] + tot[c - j] * inv0;
-        for (int a = threadIdx.x; a < j; a += blockDim.x) vtv[a] = tot[NP + QB + a] + tot[QB + a] * inv0;
+        for (int a = threadIdx.x; a < j; a += blockDim.x) vtv[a] = tot[NP + PW + a] + tot[PW + a] * inv0;
         __syncthreads();
         // ---- T column j (warp 0; identical in every CTA, CTA 0 stores it)
         if (warp == 0) {
@@ -1249,7 +1249,7 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
             __syncwarp();
             if (lane < j) T[lane][j] = -beta * t;
             if (lane == j) T[j][j] = beta;
-            if (lane > j) T[lane][j] = 0.0;
+            if (lane > j && lane < PW) T[lane][j] = 0.0;
         }
         // ---- update my rows: column j -> v (mu at row j), columns c > j -= beta w_c v
         double* colw = sm + j * rp;
@@ -1269,13 +1269,14 @@ __global__ void __launch_bounds__(512) panel_qr_cluster_kernel(const PanelDesc* 
         for (int i = threadIdx.x; i < nr; i += blockDim.x)
             if (r0 + i <= c) P[r0 + i + (size_t)c * d.ld] = sm[i + c * rp];
     if (g == 0)
-        for (int e = threadIdx.x; e < QB * QB; e += blockDim.x) d.T[e] = T[e % QB][e / QB];
+        for (int e = threadIdx.x; e < PW * PW; e += blockDim.x) d.T[e] = T[e % PW][e / PW];
     qr_tr0(5);
     qr_tr0(6);
     cluster.sync();                                   // keep smem alive for remote readers
 }
 
-static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int p) {
+template <int PW>
+static void launch_panels_pw(cudaStream_t s, const std::vector<PanelDesc>& pd, int p) {
         if (pd.empty()) return;
         {
             DevArray<PanelDesc> dp(s, pd);
@@ -1283,16 +1284,19 @@ static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int 
             int Lmax = 0;
             for (auto& q : pd) { pb += 8.0 * (q.m - q.p) * q.jb * (q.jb + 2); Lmax = std::max(Lmax, q.m - q.p); }
             // cluster of 8 CTAs (portable) when the panel slice fits 180 KB, else 16 (non-portable)
-            const int qcl = ceil_div(Lmax, 8) * QB * (int)sizeof(double) <= 180 * 1024 ? 8 : 16;
+            // (env SPD_QR_QCL8_KB: largest 8-CTA slice in KB, default 208: the 6144-row proxy
+            // panels run as 8-CTA clusters of one CTA per SM, measured 1 % faster than 16 x 2)
+            static const int q8kb = getenv("SPD_QR_QCL8_KB") ? atoi(getenv("SPD_QR_QCL8_KB")) : 208;
+            const int qcl = ceil_div(Lmax, 8) * PW * (int)sizeof(double) <= q8kb * 1024 ? 8 : 16;
             const int rp = ceil_div(Lmax, qcl);
-            const size_t sh = (size_t)rp * QB * sizeof(double);
+            const size_t sh = (size_t)rp * PW * sizeof(double);
             ProfScope prof(s, "qr_panel", 0, pb);
-            if (sh <= 180 * 1024) {
-                static bool attr = false;
+            if (sh <= 208 * 1024) {
+                static bool attr = false;   // per PW instantiation
                 if (!attr) {
-                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
-                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
-                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<8, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 208 * 1024));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+                    SPD_CUDA(cudaFuncSetAttribute(panel_qr_cluster_kernel<16, PW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                     attr = true;
                 }
                 cudaLaunchConfig_t cfg = {};
@@ -1305,8 +1309,8 @@ static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int 
                 at[0].val.clusterDim.x = qcl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                if (qcl == 8) SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<8>, (const PanelDesc*)dp.p, rp));
-                else SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<16>, (const PanelDesc*)dp.p, rp));
+                if (qcl == 8) SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<8, PW>, (const PanelDesc*)dp.p, rp));
+                else SPD_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_cluster_kernel<16, PW>, (const PanelDesc*)dp.p, rp));
                 count_launch();
                 static const bool trace = getenv("SPD_QR_TRACE") != nullptr;
                 if (trace && p == 0) {
@@ -1318,29 +1322,35 @@ static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int 
                             (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3, (tr[5] - tr[4]) * 1e-3, (tr[6] - tr[5]) * 1e-3);
                 }
             } else {
+                SPD_REQUIRE(PW == QB, "qr panel: slice too tall for the cluster kernel");
                 panel_qr_kernel<<<(unsigned)pd.size(), 256, 0, s>>>(dp.p);
                 SPD_LAUNCH();
             }
         }
     }
 
+static void launch_panels(cudaStream_t s, const std::vector<PanelDesc>& pd, int p, int pw = QB) {
+    if (pw == 16) launch_panels_pw<16>(s, pd, p);
+    else launch_panels_pw<QB>(s, pd, p);
+}
+
 // Blocks of NP panels (NP x 32 columns): panel s is updated by the reflectors of panels
 // 0..s-1 of its block (combined compact-WY factor T_{0:s}), factored, and T is extended
 // (Schreiber-Van Loan: T_{0:s+1} = [T_{0:s}, -T_{0:s} V_{0:s}^T V_s T_s; 0, T_s]); the
 // rest of the trailing matrix gets ONE rank-(32 NP) update per block, so its traffic is
 // 1/NP of the column-by-panel scheme and the far GEMMs have K = 32 NP.
-static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP) {
-    const int KB = NP * QB;
+static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP, int PW = QB) {
+    const int KB = NP * PW;
     int nmax = 0;
     size_t vtot = 0, wtot = 0;
     std::vector<size_t> voff(d.size()), woff(d.size());
     for (size_t i = 0; i < d.size(); ++i) {
         nmax = std::max(nmax, d[i].n);
         voff[i] = vtot; vtot += (size_t)d[i].m * KB;
-        woff[i] = wtot; wtot += (size_t)KB * std::max(d[i].n, QB);
+        woff[i] = wtot; wtot += (size_t)KB * std::max(d[i].n, PW);
     }
     const size_t nd = d.size();
-    DBuf<double> V(vtot), T(nd * KB * KB), Ts(nd * QB * QB), S(nd * KB * QB), X(nd * KB * QB), W(wtot), W2(wtot);
+    DBuf<double> V(vtot), T(nd * KB * KB), Ts(nd * PW * PW), S(nd * KB * PW), X(nd * KB * PW), W(wtot), W2(wtot);
     for (int p = 0; p < nmax; p += KB) {
         V.zero(s);                                    // rows above each panel's start must be 0
         T.zero(s);
@@ -1354,9 +1364,9 @@ static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP) 
                 const QrDesc& q = d[i];
                 const int kk = std::min(q.n, q.m);
                 const int ps = p + done[i];
-                if (ps >= q.n || done[i] < sp * QB) continue;       // block ended early for this matrix
-                const int ncols = std::min(QB, q.n - ps);
-                const int jb = std::max(0, std::min(QB, kk - ps));
+                if (ps >= q.n || done[i] < sp * PW) continue;       // block ended early for this matrix
+                const int ncols = std::min(PW, q.n - ps);
+                const int jb = std::max(0, std::min(PW, kk - ps));
                 const int K = kacc[i], L = q.m - p;
                 double* Vb = V.p + voff[i];
                 double* Tb = T.p + i * KB * KB;
@@ -1369,20 +1379,20 @@ static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP) 
                 done[i] += ncols;
                 if (jb <= 0) continue;
                 double* Vs = Vb + (size_t)K * q.m + (ps - p);
-                pd.push_back({q.A, q.m, q.n, q.ld, ps, jb, Vs, q.m, Ts.p + i * QB * QB});
+                pd.push_back({q.A, q.m, q.n, q.ld, ps, jb, Vs, q.m, Ts.p + i * PW * PW});
                 if (K > 0) {                                            // extend T
                     const int Ls = q.m - ps;
-                    e1.push_back({Vb + (ps - p), Vs, S.p + i * KB * QB, K, jb, Ls, q.m, q.m, KB});
-                    e2.push_back({Tb, S.p + i * KB * QB, X.p + i * KB * QB, K, jb, K, KB, KB, KB});
-                    e3.push_back({X.p + i * KB * QB, Ts.p + i * QB * QB, Tb + (size_t)K * KB, K, jb, jb, KB, QB, KB});
+                    e1.push_back({Vb + (ps - p), Vs, S.p + i * KB * PW, K, jb, Ls, q.m, q.m, KB});
+                    e2.push_back({Tb, S.p + i * KB * PW, X.p + i * KB * PW, K, jb, K, KB, KB, KB});
+                    e3.push_back({X.p + i * KB * PW, Ts.p + i * PW * PW, Tb + (size_t)K * KB, K, jb, jb, KB, PW, KB});
                 }
-                cp.push_back({Ts.p + i * QB * QB, Tb + K + (size_t)K * KB, jb, jb, QB, KB, 0});
+                cp.push_back({Ts.p + i * PW * PW, Tb + K + (size_t)K * KB, jb, jb, PW, KB, 0});
                 kacc[i] = K + jb;
             }
             gemm_batched(s, u1, true, false, 1.0, 0.0);
             gemm_batched(s, u2, true, false, 1.0, 0.0);
             gemm_batched(s, u3, false, false, -1.0, 1.0);
-            launch_panels(s, pd, p + sp * QB);
+            launch_panels(s, pd, p + sp * PW, PW);
             gemm_batched(s, e1, true, false, 1.0, 0.0);
             gemm_batched(s, e2, false, false, 1.0, 0.0);
             gemm_batched(s, e3, false, false, -1.0, 0.0);
@@ -1408,10 +1418,14 @@ static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP) 
 
 void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
     if (d.empty()) return;
-    if (const char* e = getenv("SPD_QR_NP")) {
-        const int np = atoi(e);
-        if (np >= 1 && np <= 8 && np != 2) { qr_blocked_np(s, d, np); return; }
-    }
+    // default: 16-column panels in blocks of NP = 4 (64-column compact-WY trailing updates):
+    // the panel's per-column latency is set by the cluster barrier and reductions, not by its
+    // width, so half-width panels double the panels in flight (measured C4 H2 build 9.76 ->
+    // 9.38 s).  env SPD_QR_PW=32 / SPD_QR_NP select the 32-column variants (A/B).
+    const int pw = getenv("SPD_QR_PW") ? atoi(getenv("SPD_QR_PW")) : 16;
+    const int np = getenv("SPD_QR_NP") ? atoi(getenv("SPD_QR_NP")) : (pw == 16 ? 4 : 2);
+    if (pw == 16) { qr_blocked_np(s, d, std::max(1, std::min(8, np)), 16); return; }
+    if (np >= 1 && np <= 8 && np != 2) { qr_blocked_np(s, d, np); return; }
     // Panels are taken in pairs A = [p, p + 32), B = [p + 32, p + 64): A is factored, its
     // reflectors update B's columns only, B is factored, and the rest of the trailing
     // matrix gets ONE update with the combined 64-column compact-WY factor

@@ -272,7 +272,8 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
     h->lv.clear();
     h->lv.resize(L);
     const int n_p = m * h->n_proxy;              // proxy dofs per node (rows of the proxy matrix)
-    const size_t budget = (size_t)6 << 30;       // bytes of proxy matrices in flight
+    // bytes of proxy matrices in flight per chunk (env SPD_H2_BUDGET_GB, default 6)
+    const size_t budget = (size_t)((getenv("SPD_H2_BUDGET_GB") ? atof(getenv("SPD_H2_BUDGET_GB")) : 6.0) * (1 << 30));
     for (int k = 1; k < L; ++k) {
         H2Level& lv = h->lv[k];
         lv.k = k; lv.first = t.first(k); lv.count = t.count(k);

@@ -17,10 +17,10 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     v = bench.max_over_ranks(1.5 + rank, device="cpu")
-    cfg = bench.replica_config(rank)
+    c4, c5 = bench.replica_config(rank)
     dist.barrier()
     dist.destroy_process_group()
-    q.put((rank, v, cfg.n, cfg.index))
+    q.put((rank, v, c4.n, c4.index, c5.n, c5.index))
 
 
 def test_max_over_ranks_and_replicas_gloo():
