@@ -627,7 +627,7 @@ __device__ __forceinline__ double col_norm2(const double* c, int r0, int m) {
     return warp_sum(s);
 }
 
-__global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs, const QrItem* items,
+__global__ void __launch_bounds__(QR_THREADS, 4) qrcp_kernel(const QrcpDesc* descs, const QrItem* items,
                                                           const int2* cta_items, unsigned* barriers,
                                                           double rel_tol) {
     __shared__ double sv[32];
@@ -1024,12 +1024,13 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
                 cta.push_back(make_int2(begin, (int)items.size()));
             }
         } else {
-            int spare = cap - (int)rd.size();
             const int gmax = l2b > 0.0 ? 128 : 64;
+            const int gbase = std::max(1, cap / (int)rd.size());   // every matrix >= cap / count CTAs
+            const int spare = cap - gbase * (int)rd.size();
             for (int i : rd) {
                 int extra = (int)(spare * (work[i] / rtotal));
                 int maxg = std::max(1, std::min(d[i].n, gmax));
-                const int G = std::min(maxg, 1 + extra);
+                const int G = std::min(maxg, gbase + extra);
                 for (int g = 0; g < G; ++g) {
                     cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
                     items.push_back({i, g, G});
@@ -1413,6 +1414,34 @@ static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP, 
         gemm_batched(s, g2, true, false, 1.0, 0.0);
         gemm_batched(s, g3, false, false, -1.0, 1.0);
     }
+}
+
+// The matrices of a batch in two independent halves on two streams: one half's panels
+// (latency-bound, few SMs busy) overlap the other half's trailing-update GEMMs.
+static void qr_blocked_np_2s(cudaStream_t s, const std::vector<QrDesc>& d, int NP, int PW) {
+    if (d.size() < 8 || getenv("SPD_QR_1S")) {
+        qr_blocked_np(s, d, NP, PW);
+        SPD_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    static thread_local cudaStream_t s2 = nullptr;
+    static thread_local cudaEvent_t ev[2];
+    if (!s2) {
+        SPD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        SPD_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        SPD_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    }
+    std::vector<QrDesc> a, b;
+    for (size_t i = 0; i < d.size(); ++i) (i & 1 ? b : a).push_back(d[i]);
+    SPD_CUDA(cudaEventRecord(ev[0], s));
+    SPD_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+    qr_blocked_np(s, a, NP, PW);
+    {
+        AllocStreamScope sc(s2);                      // the half's temporaries are ordered on s2
+        qr_blocked_np(s2, b, NP, PW);
+    }
+    SPD_CUDA(cudaEventRecord(ev[1], s2));
+    SPD_CUDA(cudaStreamWaitEvent(s, ev[1], 0));
     SPD_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1424,8 +1453,8 @@ void qr_unpivoted_batched(cudaStream_t s, const std::vector<QrDesc>& d) {
     // 9.38 s).  env SPD_QR_PW=32 / SPD_QR_NP select the 32-column variants (A/B).
     const int pw = getenv("SPD_QR_PW") ? atoi(getenv("SPD_QR_PW")) : 16;
     const int np = getenv("SPD_QR_NP") ? atoi(getenv("SPD_QR_NP")) : (pw == 16 ? 4 : 2);
-    if (pw == 16) { qr_blocked_np(s, d, std::max(1, std::min(8, np)), 16); return; }
-    if (np >= 1 && np <= 8 && np != 2) { qr_blocked_np(s, d, np); return; }
+    if (pw == 16) { qr_blocked_np_2s(s, d, std::max(1, std::min(8, np)), 16); return; }
+    if (np >= 1 && np <= 8 && np != 2) { qr_blocked_np_2s(s, d, np, QB); return; }
     // Panels are taken in pairs A = [p, p + 32), B = [p + 32, p + 64): A is factored, its
     // reflectors update B's columns only, B is factored, and the rest of the trailing
     // matrix gets ONE update with the combined 64-column compact-WY factor
