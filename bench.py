@@ -560,8 +560,9 @@ def roofline(prof, prof_total_s):
                 "unit": "GB/s", "frac": round(ach / peaks.get("hbm_gbs", 6550.7), 4), "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     tr = load_traffic(nm)
-    if tr:
-        roof["traffic"] = tr.get("gb_per_launch")
+    if tr:                                       # ncu DRAM bytes of every launch of this class in one step,
+        tot = tr.get("dram_read_gb", 0.0) + tr.get("dram_write_gb", 0.0)       # averaged like `achieved`
+        roof["traffic"] = round(tot / max(1.0, p["launches"]), 2) if tot else tr.get("gb_per_launch")
         roof["traffic_unit"] = f"GB per launch (ncu dram read+write, {tr.get('source')})"
     roof["algorithmic_per_launch"] = {"gflop": round(p["flops"] / max(1.0, p["launches"]) / 1e9, 3),
                                       "gb": round(p["bytes"] / max(1.0, p["launches"]) / 1e9, 4)}
