@@ -188,7 +188,7 @@ def h2_build(X, kid, ell, shift, leaf, tol, n_proxy=0):
     return h
 
 
-def h2_matvec(h: H2, x, exclude_level=0, reverse=False):
+def h2_matvec(h: H2, x, exclude_level=0, reverse=False, shuffle=None):
     """y = A x for the H2 matrix A (tree order), x: (N, w).
 
     exclude_level = k > 0 gives the literal Y^(k) = (A - blockdiag_k(A)) x of
@@ -197,7 +197,8 @@ def h2_matvec(h: H2, x, exclude_level=0, reverse=False):
     diagonal parts during multiplication".
     Up pass / coupling / down pass follow eqn:uniformbasis_h2 + eqn:nested.
     reverse=True accumulates the near blocks and the couplings in the reverse list
-    order: the same sum in another order (the drift evidence of reading R24).
+    order, shuffle=<seed> in a seeded random order: the same sum in another order
+    (the drift evidence of reading R24).
     """
     t, lists = h.tree, h.lists
     x = np.asarray(x, dtype=np.float64)
@@ -209,7 +210,12 @@ def h2_matvec(h: H2, x, exclude_level=0, reverse=False):
     keep = (lambda i, j: True) if exclude_level <= 0 else \
         (lambda i, j: lists.lca[(i, j)] > exclude_level)
     # near field (dense leaf blocks, shift on the diagonal)
-    for (a, b) in (reversed(lists.near) if reverse else lists.near):
+    def order(lst):
+        if shuffle is not None:
+            return [lst[q] for q in np.random.default_rng(shuffle).permutation(len(lst))]
+        return reversed(lst) if reverse else lst
+
+    for (a, b) in order(lists.near):
         if keep(a, b):
             ra = np.arange(t.begin[a], t.end[a])
             rb = np.arange(t.begin[b], t.end[b])
@@ -228,7 +234,7 @@ def h2_matvec(h: H2, x, exclude_level=0, reverse=False):
     # coupling: yh_i += K(J_i, J_j) xh_j over Type-3 pairs
     yh = {i: np.zeros((h.rank[i], w)) for i in xh}
     for k in range(1, t.L):
-        for (i, j) in (reversed(lists.type3[k]) if reverse else lists.type3[k]):
+        for (i, j) in order(lists.type3[k]):
             if keep(i, j):
                 yh[i] += h.block(("c", i, j), h.skel[i], h.skel[j], shift=False) @ xh[j]
     # down pass
