@@ -111,10 +111,11 @@ spd_status h2_matvec(spd_h2_t h, int layout, const double* X, int64_t ldx, doubl
         if (layout == SPD_LAYOUT_TREE) {
             h2_apply_tree(h, X, ldx, Y, ldy, (int)k, s, shard);
         } else {
-            DBuf<double> xt((size_t)h->N * k), yt((size_t)h->N * k);
-            permute_rows(s, h->perm.p, h->N, (int)k, X, ldx, xt.p, h->N, true);
-            h2_apply_tree(h, xt.p, h->N, yt.p, h->N, (int)k, s, shard);
-            permute_rows(s, h->perm.p, h->N, (int)k, yt.p, h->N, Y, ldy, false);
+            double *xt = nullptr, *yt = nullptr;
+            h2_perm_ws(h, (int)k, &xt, &yt);
+            permute_rows(s, h->perm.p, h->N, (int)k, X, ldx, xt, h->N, true);
+            h2_apply_tree(h, xt, h->N, yt, h->N, (int)k, s, shard);
+            permute_rows(s, h->perm.p, h->N, (int)k, yt, h->N, Y, ldy, false);
         }
     })
 }

@@ -125,6 +125,26 @@ static void launch_gemm_pipe1(cudaStream_t s, unsigned nb, const GemmDesc* d, co
     gemm_pipe_kernel<BM, BN, WM, WN, ST, TA, TB, PRE><<<nb, (BM / WM) * (BN / WN) * 32, sh, s>>>(d, t, alpha, beta);
     SPD_LAUNCH();
 }
+template <int BM, int BN, int WM, int WN, int ST, bool TA, bool TB>
+static void launch_gemm_persist1(cudaStream_t s, int ntiles, const GemmDesc* d, const TileRef* t, double alpha,
+                                 double beta) {
+    constexpr size_t sh = gemm_pipe_smem<BM, BN, WM, WN, ST, TA, TB>();
+    static int grid = 0;
+    if (!grid) {
+        SPD_CUDA(cudaFuncSetAttribute(gemm_persist_kernel<BM, BN, WM, WN, ST, TA, TB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        int dev = 0, nsm = 0, per = 0;
+        SPD_CUDA(cudaGetDevice(&dev));
+        SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_persist_kernel<BM, BN, WM, WN, ST, TA, TB>,
+                                                               (BM / WM) * (BN / WN) * 32, sh));
+        grid = nsm * std::max(1, per);
+    }
+    const unsigned nb = (unsigned)std::min(ntiles, grid);
+    gemm_persist_kernel<BM, BN, WM, WN, ST, TA, TB><<<nb, (BM / WM) * (BN / WN) * 32, sh, s>>>(d, t, ntiles, alpha, beta);
+    SPD_LAUNCH();
+}
+
 template <int BM, int BN, int WM, int WN, int ST, bool PRE = false>
 static void launch_gemm_pipe(cudaStream_t s, unsigned nb, const GemmDesc* d, const TileRef* t, double alpha,
                              double beta, bool ta, bool tb) {
@@ -248,6 +268,18 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         for (size_t off = 0; off < tiles.size(); off += 1u << 30) {
             unsigned nb = (unsigned)std::min<size_t>(tiles.size() - off, 1u << 30);
             const bool pre = beta != 0.0 && kmax_all <= 64;      // short-K update: C read early
+            // short-K products without split-K (the blocked QR's rank-64 updates and its
+            // T / W factors): persistent CTAs, pipeline across tiles (C2 .. C4 H2 build:
+            // 9.38 -> 9.14 s at C4)
+            // (env SPD_GEMM_NOPERSIST: the one-tile-per-CTA kernel, A/B)
+            static const bool nopersist = getenv("SPD_GEMM_NOPERSIST") != nullptr;
+            if (kmax_all <= 64 && !poff && T == 64 && !m32 && !nopersist) {
+                if (!transA && !transB) launch_gemm_persist1<64, 64, 32, 32, 3, false, false>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
+                else if (transA && !transB) launch_gemm_persist1<64, 64, 32, 32, 3, true, false>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
+                else if (!transA && transB) launch_gemm_persist1<64, 64, 32, 32, 3, false, true>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
+                else launch_gemm_persist1<64, 64, 32, 32, 3, true, true>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
+                continue;
+            }
             if (T == 128) launch_gemm_pipe<128, 128, 64, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
             else if (m32) launch_gemm_pipe<32, 64, 32, 32, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
             else if (pre) launch_gemm_pipe<64, 64, 32, 32, 2, true>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
@@ -627,7 +659,19 @@ __device__ __forceinline__ double col_norm2(const double* c, int r0, int m) {
     return warp_sum(s);
 }
 
-__global__ void __launch_bounds__(QR_THREADS, 4) qrcp_kernel(const QrcpDesc* descs, const QrItem* items,
+// loads in flight per lane and column in the update pass (4; 8 measured slower at C4:
+// 10.3 against 9.4 s of H2 build -- 121 registers leave 2 CTAs per SM)
+#ifndef SPD_QRCP_QU
+#define SPD_QRCP_QU 4
+#endif
+constexpr int QU = SPD_QRCP_QU;
+template <int U>
+__device__ __forceinline__ double tree_sum(const double* s) {
+    if constexpr (U == 1) return s[0];
+    else return tree_sum<U / 2>(s) + tree_sum<U / 2>(s + U / 2);
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs, const QrItem* items,
                                                           const int2* cta_items, unsigned* barriers,
                                                           double rel_tol) {
     __shared__ double sv[32];
@@ -748,29 +792,33 @@ __global__ void __launch_bounds__(QR_THREADS, 4) qrcp_kernel(const QrcpDesc* des
                 const bool two = j1 < n;
                 double* c0 = A + (size_t)j0 * ld;
                 double* c1 = A + (size_t)(two ? j1 : j0) * ld;
-                double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+                double sa[QU], sb[QU];
+#pragma unroll
+                for (int u = 0; u < QU; ++u) sa[u] = sb[u] = 0.0;
                 int i0 = t + lane;
-                for (; i0 + 3 * 32 < m; i0 += 4 * 32) {
-                    double x[4], y[4];
+                for (; i0 + (QU - 1) * 32 < m; i0 += QU * 32) {
+                    double x[QU], y[QU];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
+                    for (int u = 0; u < QU; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) { const double vv = vsh[i0 + 32 * u]; sa[u] += vv * x[u]; sb[u] += vv * y[u]; }
+                    for (int u = 0; u < QU; ++u) { const double vv = vsh[i0 + 32 * u]; sa[u] += vv * x[u]; sb[u] += vv * y[u]; }
                 }
                 for (int i = i0; i < m; i += 32) {
                     sa[0] += vsh[i] * ldcg(c0 + i);
                     if (two) sb[0] += vsh[i] * ldcg(c1 + i);
                 }
-                const double w0 = beta * warp_sum((sa[0] + sa[1]) + (sa[2] + sa[3]));
-                const double w1 = beta * warp_sum((sb[0] + sb[1]) + (sb[2] + sb[3]));
-                double na[4] = {0.0, 0.0, 0.0, 0.0}, nb[4] = {0.0, 0.0, 0.0, 0.0};
+                const double w0 = beta * warp_sum(tree_sum<QU>(sa));
+                const double w1 = beta * warp_sum(tree_sum<QU>(sb));
+                double na[QU], nb[QU];
+#pragma unroll
+                for (int u = 0; u < QU; ++u) na[u] = nb[u] = 0.0;
                 i0 = t + lane;
-                for (; i0 + 3 * 32 < m; i0 += 4 * 32) {
-                    double x[4], y[4];
+                for (; i0 + (QU - 1) * 32 < m; i0 += QU * 32) {
+                    double x[QU], y[QU];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
+                    for (int u = 0; u < QU; ++u) { x[u] = ldcg(c0 + i0 + 32 * u); y[u] = two ? ldcg(c1 + i0 + 32 * u) : 0.0; }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < QU; ++u) {
                         const int i = i0 + 32 * u;
                         const double vv = vsh[i];
                         const double a = x[u] - w0 * vv;
@@ -793,8 +841,8 @@ __global__ void __launch_bounds__(QR_THREADS, 4) qrcp_kernel(const QrcpDesc* des
                         if (i > t) nb[0] += b * b;
                     }
                 }
-                const double n0 = warp_sum((na[0] + na[1]) + (na[2] + na[3]));
-                const double n1 = warp_sum((nb[0] + nb[1]) + (nb[2] + nb[3]));
+                const double n0 = warp_sum(tree_sum<QU>(na));
+                const double n1 = warp_sum(tree_sum<QU>(nb));
                 if (lane == 0) {
                     d.norms[j0] = n0;
                     if (two) d.norms[j1] = n1;
@@ -907,9 +955,12 @@ __global__ void gather_ranks_kernel(const QrcpDesc* __restrict__ d, int n, int* 
     if (i < n) out[i] = *d[i].rank;
 }
 
-// algorithmic work of the QRCPs just enqueued (profiling only; ranks read back): with
-// recomputed norms (R4) step t must read every entry of the trailing (m-t) x (n-t)
-// block once -- 8 B per entry (the minimal traffic) and 6 flops (norm, dot, update)
+// algorithmic work of the QRCPs just enqueued (profiling only; ranks read back): step t of
+// the right-looking Businger-Golub QRCP with recomputed norms (R4) applies the reflector
+// to every entry of the trailing (m-t) x (n-t) block and recomputes the norms in the same
+// pass -- one read and one write per entry, 16 B -- and 6 flops (dot, update, norm).
+// (A write-avoiding left-looking variant would need only the read, 8 B, but must hold the
+// block's reflectors on chip, which does not fit for the n_c = 800-2600 triangles.)
 static void qrcp_prof_exact(cudaStream_t s, const std::vector<QrcpDesc>& d, const QrcpDesc* dd) {
     if (!prof_on()) return;
     DBuf<int> rk(d.size());
@@ -919,7 +970,7 @@ static void qrcp_prof_exact(cudaStream_t s, const std::vector<QrcpDesc>& d, cons
     for (size_t i = 0; i < d.size(); ++i)
         for (int t = 0; t <= std::min(r[i], std::min(d[i].m, d[i].n) - 1); ++t) {   // + the stopping step's norms
             const double e = (double)(d[i].m - t) * (d[i].n - t);
-            by += 8.0 * e;
+            by += 16.0 * e;
             fl += 6.0 * e;
         }
     prof_update_last("qrcp", fl, by);
@@ -1024,13 +1075,12 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
                 cta.push_back(make_int2(begin, (int)items.size()));
             }
         } else {
+            int spare = cap - (int)rd.size();
             const int gmax = l2b > 0.0 ? 128 : 64;
-            const int gbase = std::max(1, cap / (int)rd.size());   // every matrix >= cap / count CTAs
-            const int spare = cap - gbase * (int)rd.size();
             for (int i : rd) {
                 int extra = (int)(spare * (work[i] / rtotal));
                 int maxg = std::max(1, std::min(d[i].n, gmax));
-                const int G = std::min(maxg, gbase + extra);
+                const int G = std::min(maxg, 1 + extra);
                 for (int g = 0; g < G; ++g) {
                     cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
                     items.push_back({i, g, G});
@@ -1418,8 +1468,10 @@ static void qr_blocked_np(cudaStream_t s, const std::vector<QrDesc>& d, int NP, 
 
 // The matrices of a batch in two independent halves on two streams: one half's panels
 // (latency-bound, few SMs busy) overlap the other half's trailing-update GEMMs.
+// (measured at C4: 9.84 s of H2 build against 9.50 s on one stream -- the halves' smaller
+// GEMM launches lose more than the overlap gains; kept behind env SPD_QR_2S=1)
 static void qr_blocked_np_2s(cudaStream_t s, const std::vector<QrDesc>& d, int NP, int PW) {
-    if (d.size() < 8 || getenv("SPD_QR_1S")) {
+    if (d.size() < 8 || !getenv("SPD_QR_2S")) {
         qr_blocked_np(s, d, NP, PW);
         SPD_CUDA(cudaStreamSynchronize(s));
         return;

@@ -556,8 +556,8 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
     (void)s;
     if (h->ws_k >= k && !h->xh.empty()) return;
     const int L = h->tree.L;
-    h->xt.alloc((size_t)h->N * k);
-    h->yt.alloc((size_t)h->N * k);
+    if (h->xt.n < (size_t)h->N * k) h->xt.alloc((size_t)h->N * k);
+    if (h->yt.n < (size_t)h->N * k) h->yt.alloc((size_t)h->N * k);
     h->xh.clear();
     h->yh.clear();
     h->xh.resize(L);
@@ -567,6 +567,16 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
         h->yh[lk].alloc(std::max<int64_t>(1, h->lv[lk].S * k));
     }
     h->ws_k = k;
+}
+
+// permutation workspaces of original-layout products (kept in the handle: a fresh 2 x N k
+// allocation per product can stall on memory-pool growth)
+void h2_perm_ws(spd_h2_s* h, int k, double** xt, double** yt) {
+    const size_t need = (size_t)h->N * k;
+    if (h->xt.n < need) h->xt.alloc(need);
+    if (h->yt.n < need) h->yt.alloc(need);
+    *xt = h->xt.p;
+    *yt = h->yt.p;
 }
 
 void h2_prepare(spd_h2_s* h, int k, cudaStream_t s) {

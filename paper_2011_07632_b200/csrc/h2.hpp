@@ -105,6 +105,7 @@ void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const d
                   double* dst, int64_t ldd, bool to_tree);
 void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s);
 void h2_prepare(spd_h2_s* h, int k, cudaStream_t s);   // allocate matvec workspace for width k
+void h2_perm_ws(spd_h2_s* h, int k, double** xt, double** yt);   // N x k permutation buffers (handle-owned)
 void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::vector<double*>& xh, int top,
            cudaStream_t s);
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
