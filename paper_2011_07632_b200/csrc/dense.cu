@@ -214,6 +214,13 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     for (const auto& g : d) { mmax_all = std::max(mmax_all, g.m); kmax_all = std::max(kmax_all, g.k); }
     const bool m32 = T == 64 && mmax_all <= 32;
     const int TM = m32 ? 32 : T;
+    // n <= 16 everywhere (the blocked QR's in-block products of a 16-column panel: V^T A_s,
+    // V^T V_s with a long K, and the panel update A_s -= V W2): 16-column tiles instead of 64
+    // (a quarter of the DMMA work), K split when long (C4 H2 build 9.14 -> 8.86 s)
+    int nmax_all = 0;
+    for (const auto& g : d) nmax_all = std::max(nmax_all, g.n);
+    const bool n16 = T == 64 && nmax_all <= 16 && !getenv("SPD_GEMM_NO_N16");
+    const int TN = n16 ? 16 : T;
     // output tiles; when they are too few to fill the GPU and K is long (the tall
     // skinny V^T A of the blocked QR), K is split into S slices whose raw partial
     // tiles are summed in slice order by gemm_reduce_kernel (deterministic)
@@ -221,13 +228,15 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
     int kmax = 0;
     for (const auto& g : d) {
         if (g.m <= 0 || g.n <= 0) continue;
-        ntiles += (long long)ceil_div(g.m, TM) * ceil_div(g.n, T);
+        ntiles += (long long)ceil_div(g.m, TM) * ceil_div(g.n, TN);
         kmax = std::max(kmax, g.k);
     }
     // split K when a tile's K loop is long and the tiles are too few for ~8 resident per SM
     int S = 1;
     if (ntiles > 0 && ((ntiles < 2 * 148 && kmax >= 1024) || (ntiles < 4 * 148 && kmax >= 4096)))
         S = (int)std::max<long long>(1, std::min<long long>(kmax / 512, (8 * 148 + ntiles - 1) / ntiles));
+    if (n16 && ntiles > 0 && ntiles < 16 * 148 && kmax >= 512)   // 2-warp tiles: aim at ~16 per SM
+        S = (int)std::max<long long>(S, std::min<long long>(kmax / 256, (16 * 148 + ntiles - 1) / ntiles));
     std::vector<TileRef> tiles;
     std::vector<ReduceDesc> red;
     size_t poff = 0;
@@ -238,7 +247,7 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
         const int kc = Si > 1 ? ceil_div(ceil_div(d[i].k, Si), GK) * GK : std::max(d[i].k, 0);
         const int Seff = Si > 1 ? ceil_div(d[i].k, kc) : 1;
         for (int ks = 0; ks < Seff; ++ks)
-            for (int tn = 0; tn < ceil_div(d[i].n, T); ++tn)
+            for (int tn = 0; tn < ceil_div(d[i].n, TN); ++tn)
                 for (int tm = 0; tm < ceil_div(d[i].m, TM); ++tm) {
                     TileRef tr{i, tm, tn, ks * kc, std::min(d[i].k, (ks + 1) * kc), nullptr, d[i].m};
                     if (Seff > 1) tr.P = (double*)(uintptr_t)(poff + (size_t)ks * d[i].m * d[i].n + 1);  // offset+1, patched below
@@ -273,6 +282,11 @@ void gemm_batched(cudaStream_t s, const std::vector<GemmDesc>& d, bool transA, b
             // 9.38 -> 9.14 s at C4)
             // (env SPD_GEMM_NOPERSIST: the one-tile-per-CTA kernel, A/B)
             static const bool nopersist = getenv("SPD_GEMM_NOPERSIST") != nullptr;
+            if (n16) {
+                if (m32) launch_gemm_pipe<32, 16, 32, 16, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
+                else launch_gemm_pipe<64, 16, 32, 16, 3>(s, nb, dd.p, dt.p + off, alpha, beta, transA, transB);
+                continue;
+            }
             if (kmax_all <= 64 && !poff && T == 64 && !m32 && !nopersist) {
                 if (!transA && !transB) launch_gemm_persist1<64, 64, 32, 32, 3, false, false>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
                 else if (transA && !transB) launch_gemm_persist1<64, 64, 32, 32, 3, true, false>(s, (int)nb, dd.p, dt.p + off, alpha, beta);
