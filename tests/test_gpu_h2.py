@@ -125,6 +125,37 @@ def test_h2_matvec_vs_oracle(spd, name, k):
     assert rel(yt, yo[ho.tree.perm]) <= 1e-9
 
 
+@pytest.mark.parametrize("mode", ["evaluated", "mv_eval", "stored"])
+@pytest.mark.parametrize("k", [7, 64])
+def test_h2_matvec_block_source_paths(spd, mode, k, monkeypatch):
+    """Every source of the kernel blocks of a multi-vector product gives the oracle's
+    product: evaluated on the fly (SPD_STORE_FRAC=0: no store is built), evaluated although
+    a store exists (SPD_MV_EVAL=1), read from the symmetric store (kmode 1/2).  The
+    environment is read on every call (advisor, round 1)."""
+    import torch
+    cfg = CASES["C2s"]
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    _, _, _, ho = built(spd, "C2s")
+    if mode == "evaluated":
+        monkeypatch.setenv("SPD_STORE_FRAC", "0")
+    else:
+        spd.pcg_solve(h, None, cuda(synth.rhs(cfg)), tol=1e-300, maxit=1)     # builds the store
+        assert h.sym_store()[0] > 0
+        if mode == "mv_eval":
+            monkeypatch.setenv("SPD_MV_EVAL", "1")
+    x = synth.multivec(cfg.n, k)
+    y = host(spd.h2_matvec(h, cuda(x)))
+    if mode == "evaluated":
+        assert h.sym_store()[0] == 0
+    yo = np.empty_like(x)
+    yo[ho.tree.perm] = oracle.h2_matvec(ho, x[ho.tree.perm])
+    assert rel(y, yo) <= 1e-9
+    h.release_store()
+    assert h.sym_store()[0] == 0
+    assert rel(host(spd.h2_matvec(h, cuda(x))), yo) <= 1e-9
+
+
 def test_h2_matvec_vs_dense_kernel(spd):
     cfg, X, h, ho = built(spd, "C1s")
     from oracle.kernels import kernel_matrix

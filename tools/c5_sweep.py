@@ -1,5 +1,5 @@
 """C5 multi-vector sweep at full size (diagnostic): useful TF/s per k with kernel blocks
-evaluated on the fly, then again after a k = 1 product built the symmetric store.
+evaluated on the fly (SPD_STORE_FRAC=0), then again after the PCG path built the symmetric store.
 usage: python tools/c5_sweep.py"""
 import os
 import sys
@@ -32,9 +32,11 @@ def sweep(tag):
         del V
 
 
+os.environ["SPD_STORE_FRAC"] = "0"         # the evaluated pass never builds a store
 sweep("evaluated")
+os.environ["SPD_STORE_FRAC"] = "0.25"
 b = torch.tensor(np.random.default_rng(0).standard_normal(cfg.n), device="cuda")
-spd.h2_matvec(h, b)            # k = 1: builds the symmetric store (budget policy)
+spd.pcg_solve(h, None, b, tol=1e-300, maxit=1)   # the PCG path builds the symmetric k = 1 store
 torch.cuda.synchronize()
 print("store", h.sym_store(), flush=True)
 sweep("stored")
