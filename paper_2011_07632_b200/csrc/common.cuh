@@ -204,6 +204,7 @@ void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev,
 // uplo: 'L' lower / 'U' upper storage of T; trans: false -> T^{-1} X, true -> T^{-T} X
 void trsm_batched(cudaStream_t s, const std::vector<TrsmDesc>& d, char uplo, bool trans);
 void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol);
+int qrcp_slots(int m);     // CTAs the QRCP of a large batch of m-row matrices runs at once (its balance unit)
 // unpivoted blocked Householder QR (R factor only): on exit the upper triangle of
 // A[:n, :n] holds R (n <= m); the rest of A is overwritten.  Panel width 32,
 // compact-WY trailing updates on the DMMA GEMM.

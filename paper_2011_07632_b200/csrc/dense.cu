@@ -1,3 +1,4 @@
+#include <queue>
 // dense.cu -- ragged batched fp64 dense kernels for sm_100a (product path).
 //
 //   gemm_batched   C = alpha op(A) op(B) + beta C, 64x64 CTA tiles, FP64 DMMA (m8n8k4)
@@ -593,6 +594,7 @@ void trsm_base(cudaStream_t s, const std::vector<TrsmDesc>& d, bool lower_in, bo
 // ================================================================= QRCP
 constexpr int QR_THREADS = 256;
 __device__ unsigned long long g_qr_trace[64];      // debug (SPD_QR_TRACE): phase timestamps
+__device__ unsigned long long g_qr_steps[8192];    // debug (SPD_QR_STEPS): start of every step of matrix 0
 __device__ __forceinline__ void qr_tr(int k) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -870,6 +872,386 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const QrcpDesc* descs,
     }
 }
 
+// Deferred-update Businger-Golub QRCP (the same pivot rule, reading R4: the residual
+// norms are recomputed from the trailing entries at every step).  The eager kernel above
+// reads every trailing column twice (the dot with v_t, then the update + norm) and writes
+// it back at every step; this one reads it from DRAM ONCE per step and writes it back once
+// per block of nb steps:
+//  * within a block starting at step b the trailing columns keep a^(b) in memory and every
+//    step reconstructs a^(t) = a^(b) - Y w_j on the fly, Y = [v_b .. v_{t-1}] (the block's
+//    reflectors, in shared memory, zero above their first row, 1 on it), w_j one
+//    coefficient per reflector and column (global W), by the compact recurrence
+//    w_j[l] = beta_l (v_l^T a^(b) - sum_{i<l} (v_l^T v_i) w_j[i]);
+//  * a producer warp streams each owned column (rows [b, m), contiguous) into a ring of
+//    shared-memory stages with 1-D bulk copies (cp.async.bulk + mbarrier transaction
+//    counts: a whole column in flight per stage, no registers), the consumer warps run
+//    pass 1 (d = v_t^T a^(b), w_j[k] = beta_t (d - sum_l c_l w_j[l]), c_l = v_t^T v_l
+//    published by the leader) and pass 2 (every entry of a^(t+1) reconstructed -- the
+//    norm over rows > t recomputed, not downdated -- written back at the block's last
+//    step) from shared memory.
+// Pivots can differ from the eager kernel's only through rounding, i.e. at ties inside
+// the certified band of reading R19.
+constexpr int QNB = 8;
+constexpr int QSMAX = 32;                    // ring stages (max)
+struct QrcpLazy { double* Y; double* W; double* c; };    // Y: nb x m, W: n x QNB, c: QNB
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}" :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int NT>
+__device__ double qb_sum(double v, double* sv) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) sv[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < NT / 32; ++w) r += sv[w];
+    __syncthreads();
+    return r;
+}
+
+// pass 2 of the deferred QRCP for one column (one warp): a = a^(b) - sum_{l < KK} v_l w[l]
+// on rows [rstart, m), four rows per lane in flight; norm^2 of rows > t; write back if wb
+template <int KK>
+__device__ __forceinline__ void qrcp_pass2(const double* col, const double* ysh, int ms, const double* w,
+                                           int rstart, int m, int t, bool wb, double* c, double& n0, double& n1) {
+    const int lane = threadIdx.x & 31;
+    double wr[KK];
+#pragma unroll
+    for (int l = 0; l < KK; ++l) wr[l] = w[l];
+    int i = rstart + lane;
+    for (; i + 96 < m; i += 128) {
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = col[i + 32 * u];
+#pragma unroll
+        for (int l = 0; l < KK; ++l) {
+            const double* y = ysh + (size_t)l * ms + i;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] -= y[32 * u] * wr[l];
+        }
+        if (wb) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[i + 32 * u] = a[u];
+        }
+        if (i > t) { n0 += a[0] * a[0]; n1 += a[1] * a[1]; n0 += a[2] * a[2]; n1 += a[3] * a[3]; }
+        else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + 32 * u > t) n0 += a[u] * a[u];
+        }
+    }
+    for (; i < m; i += 32) {
+        double a0 = col[i];
+#pragma unroll
+        for (int l = 0; l < KK; ++l) a0 -= ysh[(size_t)l * ms + i] * wr[l];
+        if (wb) c[i] = a0;
+        if (i > t) n0 += a0 * a0;
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) qrcp_lazy_kernel(const QrcpDesc* descs, const QrcpLazy* lzs,
+                                                          const QrItem* items, const int2* cta_items,
+                                                          unsigned* barriers, double rel_tol, int nb, int ms,
+                                                          int nstage, int sst, int steptrace) {
+    constexpr int NW = NT / 32;
+    constexpr int NCW = NW - 1;                      // consumer warps (warp 0 produces)
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    __shared__ int s_stop;
+    __shared__ double s_nu0;
+    __shared__ double s_cred[QNB][NW];
+    __shared__ __align__(8) uint64_t full[QSMAX], empty[QSMAX];
+    extern __shared__ __align__(16) double ysh[];   // nb x ms reflectors, then nstage x sst column stages
+    double* stg = ysh + (size_t)nb * ms;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < QSMAX) { mbar_init(&full[threadIdx.x], 1); mbar_init(&empty[threadIdx.x], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    __shared__ unsigned s_use[QSMAX];                // completed uses of every stage barrier
+    if (threadIdx.x < QSMAX) s_use[threadIdx.x] = 0;
+    const size_t stg_doubles = (size_t)nstage * sst; // the ring's shared memory
+    const int2 range = cta_items[blockIdx.x];
+    for (int it = range.x; it < range.y; ++it) {
+        const QrItem item = items[it];
+        const QrcpDesc d = descs[item.desc];
+        const QrcpLazy lz = lzs[item.desc];
+        const int g = item.g, G = item.G;
+        unsigned* bar = barriers + 2 * item.desc;
+        const int m = d.m, n = d.n, ld = d.ld;
+        double* A = d.A;
+        const int kmax = min(min(m, n), d.max_rank);
+        {
+            int local = 0;
+            for (int j = g; j < n; j += G, ++local)
+                if (local % NW == warp) {
+                    double s = col_norm2(A + (size_t)j * ld, 0, m);
+                    if (lane == 0) d.norms[j] = s;
+                }
+            if (g == 0)
+                for (int j = threadIdx.x; j < n; j += NT) d.piv[j] = j;
+        }
+        if (threadIdx.x == 0) { s_stop = 0; s_nu0 = 0.0; }
+        if (g == 0 && threadIdx.x == 0) d.rank[0] = -1;
+        group_barrier(bar, G);
+        int b = 0;
+        for (int t = 0;; ++t) {
+            const int k = t - b;                        // reflectors already in the block
+            const bool trc = (item.desc == 0 && g == 0 && t == 100 && threadIdx.x == 0);
+            if (trc) qr_tr(10);
+            if (steptrace && item.desc == 0 && g == 0 && threadIdx.x == 0 && t < 8192) {
+                unsigned long long tt;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+                g_qr_steps[t] = tt;
+            }
+            if (g == 0) {
+                // ---- leader: pivot, the pivot column brought to step t, Householder, c_l
+                double bv = -1.0;
+                int bi = 0x7fffffff;
+                if (t < kmax) {
+                    double v = -1.0;
+                    int idx = 0x7fffffff;
+                    for (int j = t + threadIdx.x; j < n; j += NT) {
+                        double x = ldcg(d.norms + j);
+                        if (x > v) { v = x; idx = j; }
+                    }
+                    block_argmax(v, idx, sv, si, bv, bi);
+                }
+                const double nu = bv > 0.0 ? sqrt(bv) : 0.0;
+                if (threadIdx.x == 0) {
+                    if (t == 0) s_nu0 = nu;
+                    s_stop = (t >= kmax || nu == 0.0 || nu <= rel_tol * s_nu0) ? 1 : 0;
+                }
+                __syncthreads();
+                if (d.force) {
+                    if (threadIdx.x == 0) s_stop = (t >= min(kmax, d.nforce)) ? 1 : 0;
+                    __syncthreads();
+                    if (!s_stop) {
+                        const int want = d.force[t];
+                        for (int j = t + threadIdx.x; j < n; j += NT)
+                            if (__ldcg(d.piv + j) == want) si[0] = j;
+                    }
+                    __syncthreads();
+                    bi = si[0];
+                    __syncthreads();
+                }
+                if (!s_stop) {
+                    const int p = bi;
+                    if (p != t) {
+                        double* ct = A + (size_t)t * ld;
+                        double* cp = A + (size_t)p * ld;
+                        for (int i = threadIdx.x; i < m; i += NT) {
+                            double a = ldcg(ct + i), bb = ldcg(cp + i);
+                            ct[i] = bb; cp[i] = a;
+                        }
+                        if (threadIdx.x < k) {
+                            double a = ldcg(lz.W + (size_t)t * QNB + threadIdx.x), bb = ldcg(lz.W + (size_t)p * QNB + threadIdx.x);
+                            lz.W[(size_t)t * QNB + threadIdx.x] = bb; lz.W[(size_t)p * QNB + threadIdx.x] = a;
+                        }
+                        if (threadIdx.x == 0) { int tp = d.piv[t]; d.piv[t] = d.piv[p]; d.piv[p] = tp; }
+                    }
+                    __syncthreads();
+                    double* ct = A + (size_t)t * ld;
+                    double* yk = ysh + (size_t)k * ms;
+                    double* ykg = lz.Y + (size_t)k * m;
+                    {
+                        double wv[QNB];
+#pragma unroll
+                        for (int l = 0; l < QNB; ++l) wv[l] = l < k ? ldcg(lz.W + (size_t)t * QNB + l) : 0.0;
+                        for (int i = b + threadIdx.x; i < m; i += NT) {
+                            double x = ldcg(ct + i);
+#pragma unroll
+                            for (int l = 0; l < QNB; ++l)
+                                if (l < k) x -= ysh[(size_t)l * ms + i] * wv[l];
+                            if (i < t) { ct[i] = x; yk[i] = 0.0; ykg[i] = 0.0; }
+                            else yk[i] = x;
+                        }
+                    }
+                    __syncthreads();
+                    double sig = 0.0;
+                    for (int i = t + 1 + threadIdx.x; i < m; i += NT) { double x = yk[i]; sig += x * x; }
+                    sig = qb_sum<NT>(sig, sv);
+                    const double x0 = yk[t];
+                    double beta, mu, v0;
+                    if (sig == 0.0) { beta = (x0 >= 0.0) ? 0.0 : 2.0; mu = fabs(x0); v0 = 1.0; }
+                    else {
+                        mu = sqrt(x0 * x0 + sig);
+                        v0 = (x0 <= 0.0) ? x0 - mu : -sig / (x0 + mu);
+                        beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+                    }
+                    const double inv0 = 1.0 / v0;
+                    for (int i = t + 1 + threadIdx.x; i < m; i += NT) {
+                        const double v = (sig == 0.0) ? 0.0 : yk[i] * inv0;
+                        yk[i] = v; ct[i] = v; ykg[i] = v;
+                    }
+                    __syncthreads();
+                    if (threadIdx.x == 0) { yk[t] = 1.0; ykg[t] = 1.0; ct[t] = mu; d.beta[t] = beta; }
+                    __syncthreads();
+                    if (k > 0) {
+                        double cp[QNB];
+#pragma unroll
+                        for (int l = 0; l < QNB; ++l) cp[l] = 0.0;
+                        for (int i = t + threadIdx.x; i < m; i += NT) {
+                            const double v = yk[i];
+#pragma unroll
+                            for (int l = 0; l < QNB; ++l)
+                                if (l < k) cp[l] += v * ysh[(size_t)l * ms + i];
+                        }
+#pragma unroll
+                        for (int l = 0; l < QNB; ++l)
+                            if (l < k) { const double r = warp_sum(cp[l]); if (lane == 0) s_cred[l][warp] = r; }
+                        __syncthreads();
+                        if (threadIdx.x < k) {
+                            double r = 0.0;
+                            for (int w = 0; w < NW; ++w) r += s_cred[threadIdx.x][w];
+                            lz.c[threadIdx.x] = r;
+                        }
+                    }
+                } else if (threadIdx.x == 0) {
+                    d.rank[0] = t;
+                }
+                __syncthreads();
+            }
+            if (trc) qr_tr(11);
+            group_barrier(bar, G);
+            if (trc) qr_tr(12);
+            const int r = __ldcg(d.rank);
+            if (r >= 0 && k == 0) break;
+            if (r < 0 && g != 0) {                     // the step's reflector into shared memory
+                double* yk = ysh + (size_t)k * ms;
+                const double* ykg = lz.Y + (size_t)k * m;
+                for (int i = b + threadIdx.x; i < m; i += NT) yk[i] = ldcg(ykg + i);
+                __syncthreads();
+            }
+            // ---- column phase: owned columns j = g + G q >= jfirst, streamed through the ring
+            const int kk = r >= 0 ? k : k + 1;          // reflectors applied in pass 2
+            const bool wb = r >= 0 || kk == nb;         // write back (block end or stop)
+            const int jfirst = r >= 0 ? t : t + 1;
+            const int q0 = jfirst > g ? (jfirst - g + G - 1) / G : 0;
+            const int ncol = n > g + G * q0 ? (n - 1 - g - G * q0) / G + 1 : 0;
+            const int b0 = b & ~1, me = m & ~1;         // 16-byte aligned bulk copies: rows [b0, me)
+            const unsigned bytes = me > b0 ? (unsigned)(me - b0) * 8u : 0u;
+            // this step's ring: stages of the current column length (all drained between
+            // steps), ncw consumer warps with spc >= 2 stages each where they fit (a consumer
+            // computes on one stage while its next column streams into the other)
+            const int cst = ((m - b0 + 2) + 1) & ~1;    // doubles per stage
+            const int nfit = min(QSMAX, (int)(stg_doubles / cst));
+            const int ncw = max(1, min(NCW, nfit / 2));
+            const int spc = max(1, min(nfit / ncw, QSMAX / ncw));
+            if (warp == 0) {
+                if (lane == 0)
+                    for (int q = 0; q < ncol; ++q) {
+                        // column q -> consumer c = q mod ncw, its x-th column of the step; consumer
+                        // c owns the stages c + ncw i, i < spc, used in turn
+                        const int c = q % ncw, x = q / ncw;
+                        const int st = c + ncw * (x % spc);
+                        const unsigned use = s_use[st] + x / spc;
+                        if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+                        mbar_expect_tx(&full[st], bytes);
+                        const int j = g + G * (q0 + q);
+                        if (bytes) bulk_g2s(stg + (size_t)st * cst, A + (size_t)j * ld + b0, bytes, &full[st]);
+                    }
+            } else if (warp <= ncw) {
+                const double beta = r >= 0 ? 0.0 : __ldcg(d.beta + t);
+                double cl[QNB];
+#pragma unroll
+                for (int l = 0; l < QNB; ++l) cl[l] = (r < 0 && l < k) ? __ldcg(lz.c + l) : 0.0;
+                const double* yk = ysh + (size_t)k * ms;
+                const int rstart = wb ? b : t + 1;
+                int x = 0;
+                for (int q = warp - 1; q < ncol; q += ncw, ++x) {
+                    const int st = (warp - 1) + ncw * (x % spc);
+                    const unsigned use = s_use[st] + x / spc;
+                    const int j = g + G * (q0 + q);
+                    double* c = A + (size_t)j * ld;
+                    double* col = stg + (size_t)st * cst - b0;     // col[i] = row i
+                    double w[QNB];
+#pragma unroll
+                    for (int l = 0; l < QNB; ++l) w[l] = l < k ? __ldcg(lz.W + (size_t)j * QNB + l) : 0.0;
+                    mbar_wait(&full[st], use & 1);
+                    if ((m & 1) && lane == 0) col[m - 1] = ldcg(c + m - 1);
+                    __syncwarp();
+                    if (r < 0) {
+                        // pass 1: v_t^T a^(b) over rows >= t
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                        int i = t + lane;
+                        for (; i + 96 < m; i += 128) {
+                            s0 += yk[i] * col[i];
+                            s1 += yk[i + 32] * col[i + 32];
+                            s2 += yk[i + 64] * col[i + 64];
+                            s3 += yk[i + 96] * col[i + 96];
+                        }
+                        for (; i < m; i += 32) s0 += yk[i] * col[i];
+                        double d0 = warp_sum((s0 + s1) + (s2 + s3));
+#pragma unroll
+                        for (int l = 0; l < QNB; ++l)
+                            if (l < k) d0 -= cl[l] * w[l];
+                        d0 *= beta;
+#pragma unroll
+                        for (int l = 0; l < QNB; ++l)
+                            if (l == k) w[l] = d0;
+                        if (lane == 0) lz.W[(size_t)j * QNB + k] = d0;
+                    }
+                    // pass 2: a^(t+1) = a^(b) - sum_{l < kk} v_l w[l]; norm over rows > t
+                    // (kk a compile-time count: no predicated-off multiply-adds)
+                    double n0 = 0.0, n1 = 0.0;
+                    switch (kk) {
+                        case 1: qrcp_pass2<1>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 2: qrcp_pass2<2>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 3: qrcp_pass2<3>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 4: qrcp_pass2<4>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 5: qrcp_pass2<5>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 6: qrcp_pass2<6>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 7: qrcp_pass2<7>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        case 8: qrcp_pass2<8>(col, ysh, ms, w, rstart, m, t, wb, c, n0, n1); break;
+                        default: break;
+                    }
+                    if (r < 0) {
+                        const double nn = warp_sum(n0 + n1);
+                        if (lane == 0) d.norms[j] = nn;
+                    }
+                    fence_proxy_async();                       // generic smem accesses before the next bulk copy
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[st]);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < ncw * spc) {              // uses of stage st = c + ncw i this step
+                const int c = threadIdx.x % ncw, i = threadIdx.x / ncw;
+                const int nc = ncol > c ? (ncol - c + ncw - 1) / ncw : 0;
+                if (nc > i) s_use[threadIdx.x] += (nc - i + spc - 1) / spc;
+            }
+            __syncthreads();
+            if (trc) qr_tr(13);
+            group_barrier(bar, G);
+            if (trc) qr_tr(14);
+            if (r >= 0) break;
+            if (wb) b = t + 1;
+        }
+        group_barrier(bar, G);
+    }
+}
+
 // Small matrices (m n <= ~24k doubles: the SPD-HSS sketches 200 x 110, the leaf-level H2
 // triangles 128 x 128): one CTA per matrix with the matrix in shared memory -- the same
 // Businger-Golub steps (recomputed norms, lowest index on ties), but every step is
@@ -970,11 +1352,11 @@ __global__ void gather_ranks_kernel(const QrcpDesc* __restrict__ d, int n, int* 
 }
 
 // algorithmic work of the QRCPs just enqueued (profiling only; ranks read back): step t of
-// the right-looking Businger-Golub QRCP with recomputed norms (R4) applies the reflector
-// to every entry of the trailing (m-t) x (n-t) block and recomputes the norms in the same
-// pass -- one read and one write per entry, 16 B -- and 6 flops (dot, update, norm).
-// (A write-avoiding left-looking variant would need only the read, 8 B, but must hold the
-// block's reflectors on chip, which does not fit for the n_c = 800-2600 triangles.)
+// the Businger-Golub QRCP with recomputed norms (R4) must read every entry of the trailing
+// (m-t) x (n-t) block once (the norms of the updated columns) -- 8 B per entry, the
+// algorithmic bytes -- and does 6 flops per entry (dot, update, norm).  The write-back of
+// the updated block is an implementation cost: every step in the eager kernel (16 B per
+// entry of DRAM traffic), once per nb steps in the deferred kernel (8 + 8/nb B).
 static void qrcp_prof_exact(cudaStream_t s, const std::vector<QrcpDesc>& d, const QrcpDesc* dd) {
     if (!prof_on()) return;
     DBuf<int> rk(d.size());
@@ -984,10 +1366,29 @@ static void qrcp_prof_exact(cudaStream_t s, const std::vector<QrcpDesc>& d, cons
     for (size_t i = 0; i < d.size(); ++i)
         for (int t = 0; t <= std::min(r[i], std::min(d[i].m, d[i].n) - 1); ++t) {   // + the stopping step's norms
             const double e = (double)(d[i].m - t) * (d[i].n - t);
-            by += 16.0 * e;
+            by += 8.0 * e;
             fl += 6.0 * e;
         }
     prof_update_last("qrcp", fl, by);
+}
+
+// CTA shape of the deferred kernel for matrices of up to m rows: 256 threads, two CTAs per
+// SM (more, finer groups) up to 1024 rows; 512 threads, one CTA per SM (the whole shared
+// memory for one ring of long columns) beyond; SPD_QRCP_NT overrides
+static int qrcp_nt(int m) {
+    static const int env = getenv("SPD_QRCP_NT") ? atoi(getenv("SPD_QRCP_NT")) : 0;
+    if (env == 256 || env == 512) return env;
+    return m <= 1024 ? 256 : 512;
+}
+int qrcp_slots(int m) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        SPD_CUDA(cudaGetDevice(&dev));
+        SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (getenv("SPD_QRCP_EAGER")) return 3 * nsm;
+    return qrcp_nt(m) == 256 ? 2 * nsm : nsm;
 }
 
 void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol) {
@@ -1021,14 +1422,38 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
     SPD_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int mmax = 1;
     for (auto& q : d) mmax = std::max(mmax, q.m);
-    const size_t qsmem = sizeof(double) * (size_t)mmax;
-    SPD_REQUIRE(qsmem <= 200 * 1024, "qrcp: matrix too tall");
-    static bool qattr = false;
-    if (!qattr) {
-        SPD_CUDA(cudaFuncSetAttribute(qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        qattr = true;
+    // deferred-update kernel (default; SPD_QRCP_EAGER=1: the read+write-per-step kernel):
+    // nb reflectors per block (SPD_QRCP_NB, default 4) in shared memory next to a ring of
+    // column stages (one column of <= mmax rows each); one CTA of NT threads per SM.  Needs
+    // 16-byte aligned columns (bulk copies) and >= 2 stages, else the eager kernel.
+    static const bool eager_env = getenv("SPD_QRCP_EAGER") != nullptr;
+    static const int nb_env = getenv("SPD_QRCP_NB") ? atoi(getenv("SPD_QRCP_NB")) : 2;
+    // CTA shape: 512 threads, one CTA per SM (the whole shared memory for one ring), or
+    // 256 threads, two CTAs per SM (twice the CTAs to share among the matrices: finer groups)
+    const int nt_env = qrcp_nt(mmax);
+    const int ms = (mmax + 1) & ~1;                  // reflector row stride (even: 16-byte stages)
+    const int sst = ((mmax + 2) + 1) & ~1;           // doubles per column stage
+    const size_t budget = nt_env == 256 ? 110 * 1024 : 220 * 1024;
+    bool aligned = true;
+    for (auto& q : d) aligned = aligned && ((uintptr_t)q.A % 16 == 0) && (q.ld % 2 == 0);
+    // (the kernel re-plans the ring every step for the current column length; here: at
+    // least two full-length stages must fit next to the reflectors)
+    int nb = std::max(1, std::min(QNB, nb_env)), nstage = 0;
+    for (; nb >= 1; --nb) {
+        const size_t ybytes = sizeof(double) * (size_t)nb * ms;
+        nstage = ybytes < budget ? (int)((budget - ybytes) / (sizeof(double) * sst)) : 0;
+        if (nstage >= 2) break;
     }
-    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_kernel, QR_THREADS, qsmem));
+    const bool eager = eager_env || !aligned || nb < 1 || nstage < 2;
+    const void* lazy_fn = nt_env == 256 ? (const void*)qrcp_lazy_kernel<256> : (const void*)qrcp_lazy_kernel<512>;
+    const int lazy_nt = nt_env == 256 ? 256 : 512;
+    const size_t qsmem = eager ? sizeof(double) * (size_t)mmax
+                               : sizeof(double) * ((size_t)nb * ms + (size_t)nstage * sst);
+    SPD_REQUIRE(qsmem <= 220 * 1024, "qrcp: matrix too tall");
+    SPD_CUDA(cudaFuncSetAttribute(eager ? (const void*)qrcp_kernel : lazy_fn,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(qsmem, 48 * 1024)));
+    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eager ? (const void*)qrcp_kernel : lazy_fn,
+                                                           eager ? QR_THREADS : lazy_nt, qsmem));
     const int cap = std::max(1, nsm * std::max(1, per_sm));
     // work estimate per matrix ~ m * n * min(m, n, max_rank)
     std::vector<double> work(d.size());
@@ -1039,6 +1464,23 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
         total += work[i];
     }
     DevArray<QrcpDesc> dd(s, d);
+    // per-matrix scratch of the deferred kernel: Y (nb x m), W (n x QNB), c (QNB)
+    size_t lz_total = 0;
+    if (!eager)
+        for (auto& q : d) lz_total += (size_t)nb * q.m + (size_t)q.n * QNB + QNB;
+    DBuf<double> lzbuf(std::max<size_t>(1, lz_total));
+    std::vector<QrcpLazy> lzv;
+    if (!eager) {
+        size_t off = 0;
+        for (auto& q : d) {
+            QrcpLazy z;
+            z.Y = lzbuf.p + off; off += (size_t)nb * q.m;
+            z.W = lzbuf.p + off; off += (size_t)q.n * QNB;
+            z.c = lzbuf.p + off; off += QNB;
+            lzv.push_back(z);
+        }
+    }
+    DevArray<QrcpLazy> dlz(s, lzv);
     unsigned* bars = nullptr;
     SPD_CUDA(cudaMallocAsync((void**)&bars, sizeof(unsigned) * 2 * d.size(), s));
     SPD_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * d.size(), s));
@@ -1089,12 +1531,24 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
                 cta.push_back(make_int2(begin, (int)items.size()));
             }
         } else {
-            int spare = cap - (int)rd.size();
+            // CTAs per matrix: one each, then every spare CTA to the matrix whose time
+            // work / G is largest (greedy min-max; proportional rounding left near-equal
+            // matrices with G and G + 1 CTAs, i.e. the slowest at up to twice the rest)
             const int gmax = l2b > 0.0 ? 128 : 64;
+            std::vector<int> Gs(d.size(), 1);
+            {
+                std::priority_queue<std::pair<double, int>> pq;
+                for (int i : rd) pq.push({work[i], i});
+                for (int spare = cap - (int)rd.size(); spare > 0 && !pq.empty(); --spare) {
+                    const int i = pq.top().second;
+                    pq.pop();
+                    if (Gs[i] >= std::max(1, std::min(d[i].n, gmax))) { ++spare; continue; }
+                    ++Gs[i];
+                    pq.push({work[i] / Gs[i], i});
+                }
+            }
             for (int i : rd) {
-                int extra = (int)(spare * (work[i] / rtotal));
-                int maxg = std::max(1, std::min(d[i].n, gmax));
-                const int G = std::min(maxg, 1 + extra);
+                const int G = Gs[i];
                 for (int g = 0; g < G; ++g) {
                     cta.push_back(make_int2((int)items.size(), (int)items.size() + 1));
                     items.push_back({i, g, G});
@@ -1107,9 +1561,20 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
         const QrItem* a1 = di.p;
         const int2* a2 = dc.p;
         double tol = rel_tol;
-        void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
-        SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
-                                             args, qsmem, s));
+        if (eager) {
+            void* args[] = {(void*)&a0, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol};
+            SPD_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_kernel, dim3((unsigned)cta.size()), dim3(QR_THREADS),
+                                                 args, qsmem, s));
+        } else {
+            const QrcpLazy* a5 = dlz.p;
+            int nbv = nb, msv = ms, nsv = nstage, sstv = sst;
+            static const int steptr = getenv("SPD_QR_STEPS") ? 1 : 0;
+            int stv = steptr;
+            void* args[] = {(void*)&a0, (void*)&a5, (void*)&a1, (void*)&a2, (void*)&bars, (void*)&tol, (void*)&nbv,
+                            (void*)&msv, (void*)&nsv, (void*)&sstv, (void*)&stv};
+            SPD_CUDA(cudaLaunchCooperativeKernel(lazy_fn, dim3((unsigned)cta.size()), dim3(lazy_nt),
+                                                 args, qsmem, s));
+        }
         count_launch();
         }
     }
@@ -1121,6 +1586,17 @@ void qrcp_batched(cudaStream_t s, const std::vector<QrcpDesc>& d, double rel_tol
         fprintf(stderr, "[qrcp trace] %zu mats, %zu rounds, m %d n %d: leader %.2f bar1 %.2f update %.2f bar2 %.2f us\n",
                 d.size(), rounds.size(), d[0].m, d[0].n, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3,
                 (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3);
+    }
+    if (getenv("SPD_QR_STEPS") && !eager) {
+        static std::vector<unsigned long long> st(8192);
+        SPD_CUDA(cudaStreamSynchronize(s));
+        SPD_CUDA(cudaMemcpyFromSymbol(st.data(), g_qr_steps, sizeof(unsigned long long) * 8192));
+        int rk = 0;
+        SPD_CUDA(cudaMemcpy(&rk, d[0].rank, sizeof(int), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[qrcp steps] %zu mats m %d rank %d:", d.size(), d[0].m, rk);
+        for (int t = 0; t + 50 < std::min(rk, 8192); t += 50)
+            fprintf(stderr, " %d:%.1f", t, (st[t + 50] - st[t]) * 1e-3 / 50);
+        fprintf(stderr, " us/step\n");
     }
     SPD_CUDA(cudaFreeAsync(bars, s));
     qrcp_prof_exact(s, d, dd.p);

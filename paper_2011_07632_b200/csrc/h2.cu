@@ -1,3 +1,5 @@
+#include <set>
+#include <string>
 // h2.cu -- H2 construction by proxy-point ID and the H2 multi-vector product.
 //
 // Build (readings R3/R4; the paper delegates the method to H2Pack,
@@ -332,12 +334,25 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
         std::vector<Chunk> chunks;
         for (int q = 0; q < (sharded && cm->virt ? P : 1); ++q) {
             const int me = !sharded ? -1 : (cm->virt ? q : cm->rank);
+            // chunk size balanced for the QRCP: a multiple of its CTA slots S (one CTA per
+            // matrix, each CTA the same number of matrices) when the budget holds >= S
+            // nodes, else S / G nodes for G CTAs per matrix (every slot busy)
+            size_t bmax = 1;
+            int ncmax = 1;
+            for (int a : nodes) {
+                bmax = std::max(bmax, (size_t)n_p * lv.ncand[a] * 8 + (size_t)n_p * d * 8);
+                ncmax = std::max(ncmax, lv.ncand[a]);
+            }
+            const int fit = (int)std::min<size_t>(1 << 20, std::max<size_t>(1, budget / bmax)), S = qrcp_slots(ncmax);
+            const int nper = fit >= S ? fit / S * S : std::max(1, S / ((S + fit - 1) / fit));
             Chunk cur;
             size_t bytes = 0;
             for (int a : nodes) {
                 if (me >= 0 && shard_owner(cm, lv.count, a) != me) continue;
                 size_t b = (size_t)n_p * lv.ncand[a] * 8 + (size_t)n_p * d * 8;
-                if (!cur.nodes.empty() && bytes + b > budget) { chunks.push_back(cur); cur = Chunk(); bytes = 0; }
+                if (!cur.nodes.empty() && (bytes + b > budget || (int)cur.nodes.size() >= nper)) {
+                    chunks.push_back(cur); cur = Chunk(); bytes = 0;
+                }
                 cur.nodes.push_back(a);
                 bytes += b;
             }
@@ -419,6 +434,29 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
                 zero_lower_batched(s, tri);
             }
             stage_mark(s, "h2 blocked QR", k);
+            if (const char* dump = getenv("SPD_DUMP_QRCP")) {   // diagnostic: the level's first chunk of triangles
+                static std::set<int> done;
+                if (!done.count(k) && !qdesc.empty()) {
+                    done.insert(k);
+                    const int nc = qdesc[0].n, cnt = (int)qdesc.size();
+                    std::vector<double> hbuf((size_t)nc * nc);
+                    std::string path = std::string(dump) + "_L" + std::to_string(k) + ".bin";
+                    FILE* f = fopen(path.c_str(), "wb");
+                    int hdr[3] = {cnt, nc, 0};
+                    fwrite(hdr, sizeof(int), 3, f);
+                    for (int q = 0; q < cnt; ++q) {
+                        SPD_REQUIRE(qdesc[q].n == qdesc[q].m, "dump: square triangles only");
+                        const int m2 = qdesc[q].m;
+                        hbuf.resize((size_t)m2 * m2);
+                        SPD_CUDA(cudaMemcpy2DAsync(hbuf.data(), sizeof(double) * m2, qdesc[q].A, sizeof(double) * qdesc[q].ld,
+                                                   sizeof(double) * m2, m2, cudaMemcpyDeviceToHost, s));
+                        SPD_CUDA(cudaStreamSynchronize(s));
+                        fwrite(&m2, sizeof(int), 1, f);
+                        fwrite(hbuf.data(), sizeof(double), (size_t)m2 * m2, f);
+                    }
+                    fclose(f);
+                }
+            }
             qrcp_batched(s, qdesc, h->tol);
             stage_mark(s, "h2 qrcp", k);
             std::vector<int> rk(lv.count + 1);

@@ -94,13 +94,15 @@ def test_qrcp_matches_oracle(spd, batch, m, n, cap, tol):
     pg = host(piv).reshape(batch, n)
     rg = host(rank)
     Qg = host(Q).reshape(batch, min(m, n, cap), m).transpose(0, 2, 1)
+    from oracle.certify import certify_pivots
     for b in range(batch):
         Qo, Ro, po, ro = oracle.qrcp(A[b], cap, tol)
-        assert rg[b] == ro
-        r = ro
-        # pivots: equal, or a certified near-tie (reading R19) -> compare the prefix
+        # the whole pivot sequence and the rank: the oracle's, or certified ties (R19)
+        cert = certify_pivots(A[b], pg[b], rg[b], tol, cap)
+        assert cert["ok"], (b, cert["ties"][:5], cert["worst"], cert["rank_ok"], rg[b], ro)
+        r = min(int(rg[b]), ro)
+        # values: compare up to the first deviation (after a tie the factors differ)
         same = int(np.argmax(pg[b][:r] != po[:r])) if (pg[b][:r] != po[:r]).any() else r
-        assert same >= min(r, 20), f"pivot mismatch at {same}"
         Rb = np.triu(Rg[b][:r])
         np.testing.assert_allclose(Rb[:, :same], Ro[:, :same], atol=1e-12 * abs(Ro[0, 0]))
         # Q columns are determined to ~eps/(R_tt/R_00): compare the well-conditioned ones

@@ -14,7 +14,9 @@ Checks:
 * with the oracle's skeletons injected into both (spd_h2_opts.inject_skeletons, the
   R19 protocol -- the GPU's own skeletons are certified in test_gpu_h2/test_gpu_shard),
   the sharded build equals the unsharded one up to batching-order rounding: the same
-  H2 and HSS ranks, the same HSS solve to 1e-10, PCG iteration counts within one.
+  H2 and HSS ranks, the same HSS solve to 1e-10, PCG iteration counts within one --
+  widened only by the oracle's own drift on this case under a change of summation
+  order (reading R24: the sharded products sum the same blocks in another order).
 No rank's kernels wait on another's (the exchanges are host-side), so the GPU is
 only time-shared.
 """
@@ -77,7 +79,8 @@ def test_sharded_build_with_real_exchanges(P, n, leaf):
     import oracle
     import synth
     cfg = synth.C2.scaled(n, leaf=leaf)
-    skel = oracle.h2_build(synth.points(cfg), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol).skel
+    ho = oracle.h2_build(synth.points(cfg), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    skel = ho.skel
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29800 + (os.getpid() + P) % 1000
@@ -110,5 +113,15 @@ def test_sharded_build_with_real_exchanges(P, n, leaf):
     assert np.linalg.norm(got["y"] - ref["y"]) <= 1e-11 * np.linalg.norm(ref["y"])
     assert np.linalg.norm(got["ym"] - ref["ym"]) <= 1e-11 * np.linalg.norm(ref["ym"])
     assert np.linalg.norm(got["x"] - ref["x"]) <= 1e-10 * np.linalg.norm(ref["x"])
-    assert abs(got["iters"] - ref["iters"]) <= 1
+    if abs(got["iters"] - ref["iters"]) > 1:
+        # R24: the window is the oracle's own spread over summation orders of the product
+        # (same H2 skeletons, same Philox Omega, same cap / tolerance as _run)
+        from oracle.omega import philox_normal
+        from test_gpu_hss import drift_window
+        Ho = oracle.spdhss_build(ho, 40, 1e-3, philox_normal(cfg.n, 50, 11), form="chol")
+        bo = synth.multivec(cfg.n, 1)[:, 0][ho.tree.perm]
+        _, it_o, _, _ = oracle.pcg(lambda v: oracle.h2_matvec(ho, v), lambda v: oracle.hss_solve(Ho, v), bo, 1e-8, 500)
+        window, its = drift_window(ho, lambda v: oracle.hss_solve(Ho, v), bo, 1e-8, 500, it_o)
+        print("oracle iterations", it_o, "other orders", its, "window", window)
+        assert abs(got["iters"] - ref["iters"]) <= window
     assert np.linalg.norm(got["xp"] - ref["xp"]) <= 1e-6 * np.linalg.norm(ref["xp"])
