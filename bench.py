@@ -109,7 +109,7 @@ class ClockSampler:
 # ------------------------------------------------------------------ helpers
 def load_traffic(kernel):
     """DRAM traffic of the dominant kernel from the committed ncu capture (or None)."""
-    path = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02c_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get(kernel)
