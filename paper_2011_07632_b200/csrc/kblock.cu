@@ -35,18 +35,32 @@ __device__ __forceinline__ double kval(const KernelParams& kp, double r2) {
 // evaluated once into shared memory (shared by all column warps) and contracted
 // with the 16 x NC slice of X; the next chunk's X slice and coordinates are
 // prefetched into registers while the current chunk is evaluated/contracted.
+// sources per chunk of the kblock kernel: 32 for the 160-column tile (half the barriers per
+// flop; one CTA per SM), 16 otherwise
+__host__ __device__ constexpr int kb_chunk(int NC) { return NC == 160 ? 32 : 16; }
+__host__ __device__ constexpr int kb_smem_bytes(int NC) {
+    return (int)sizeof(double) * (kb_chunk(NC) * (KB_M + 8) + NC * (kb_chunk(NC) + 4) + 4 * kb_chunk(NC));
+}
+
+template <class F>
+static void kb_attr(F* f, int bytes) {
+    if (bytes > 48 * 1024) SPD_CUDA(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 template <int KID, int NC>
 __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : (NC == 160 ? 1 : 256 / NC)) kblock_kernel(
     KernelParams kp, double shift, int d, const KbBlock* __restrict__ blocks,
     const KbTarget* __restrict__ targets, const KbEntry* __restrict__ entries,
     const KbWork* __restrict__ work, double* __restrict__ partial) {
     constexpr int NT = 2 * NC;                  // threads
+    constexpr int KK = kb_chunk(NC);            // sources per chunk (32 for the 160-column tile)
     constexpr int WN = NC / 32;                 // warps along columns
-    constexpr int XPT = KB_K * NC / NT;         // X values per thread per chunk (= 8)
+    constexpr int XPT = KK * NC / NT;         // X values per thread per chunk (= 8)
     constexpr int EST = NT / KB_M;              // kernel-tile columns kc = tid / 64 + EST u (NC / 32 of them)
-    __shared__ double Ks[KB_K][KB_M + 8];            // row stride = 8 (mod 16) doubles: fragment reads in 2 wavefronts
-    __shared__ double Xs[NC][KB_K + 4];              // kc contiguous: conflict-free writes and reads
-    __shared__ double Sx[4][KB_K];                   // coordinates (RPY: + component row)
+    extern __shared__ double kbsm[];              // dynamic: Ks | Xs | Sx (kb_smem_bytes)
+    double (*Ks)[KB_M + 8] = reinterpret_cast<double (*)[KB_M + 8]>(kbsm);               // row stride = 8 (mod 16) doubles: fragment reads in 2 wavefronts
+    double (*Xs)[KK + 4] = reinterpret_cast<double (*)[KK + 4]>(kbsm + KK * (KB_M + 8));  // kc contiguous: conflict-free writes and reads
+    double (*Sx)[KK] = reinterpret_cast<double (*)[KK]>(kbsm + KK * (KB_M + 8) + NC * (KK + 4));   // coordinates (RPY: + component row)
     const KbWork wk = work[blockIdx.x];
     const KbTarget tg = targets[wk.target];
     const KbBlock tb = blocks[tg.blk];
@@ -75,33 +89,33 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : (NC == 160 ? 1 : 256 / 
             const int ncols = min(NC, en.ncols - c0);
             const bool use_shift = (shift != 0.0) && rid >= 0 && sb.id0 >= 0;
             auto load = [&](int k0) {
-                const int nk = min(KB_K, sb.n - k0);
+                const int nk = min(KK, sb.n - k0);
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
                     const int idx = tid + u * NT;
-                    const int kk = idx % KB_K, j = idx / KB_K;
+                    const int kk = idx % KK, j = idx / KK;
                     xr[u] = (kk < nk && j < ncols) ? __ldg(en.X + k0 + kk + (size_t)(c0 + j) * en.ldx) : 0.0;
                 }
-                if (tid < KB_K * 4) {
-                    const int a = tid / KB_K, c = tid % KB_K;
+                if (tid < KK * 4) {
+                    const int a = tid / KK, c = tid % KK;
                     sr = (a < d && c < nk) ? __ldg(sb.x + (size_t)a * sb.ds + k0 + c) : 0.0;
                 }
             };
             load(0);
-            for (int k0 = 0; k0 < sb.n; k0 += KB_K) {
-                const int nk = min(KB_K, sb.n - k0);
+            for (int k0 = 0; k0 < sb.n; k0 += KK) {
+                const int nk = min(KK, sb.n - k0);
                 __syncthreads();
 #pragma unroll
                 for (int u = 0; u < XPT; ++u) {
                     const int idx = tid + u * NT;
-                    Xs[idx / KB_K][idx % KB_K] = xr[u];
+                    Xs[idx / KK][idx % KK] = xr[u];
                 }
-                if (tid < KB_K * 4) Sx[tid / KB_K][tid % KB_K] = sr;
+                if (tid < KK * 4) Sx[tid / KK][tid % KK] = sr;
                 __syncthreads();
-                if (k0 + KB_K < sb.n) load(k0 + KB_K);          // prefetch the next chunk
+                if (k0 + KK < sb.n) load(k0 + KK);          // prefetch the next chunk
                 if (en.kmode == 0) {
 #pragma unroll
-                    for (int kc = ec0; kc < KB_K; kc += EST) {
+                    for (int kc = ec0; kc < KK; kc += EST) {
                         const double d0 = rx[0] - Sx[0][kc], d1 = rx[1] - Sx[1][kc], d2 = rx[2] - Sx[2][kc];
                         double kv;
                         if constexpr (KID == SPD_K_RPY) kv = rpy_entry(kp, d0, d1, d2, (int)rx[3], (int)Sx[3][kc]);
@@ -111,7 +125,7 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : (NC == 160 ? 1 : 256 / 
                     }
                 } else {                          // stored block (symmetric store): loads only
                     const int r = r0 + er;
-                    constexpr int EPT = (KB_K + EST - 1) / EST;
+                    constexpr int EPT = (KK + EST - 1) / EST;
                     double kv[EPT];
 #pragma unroll
                     for (int c = 0; c < EPT; ++c) {
@@ -119,15 +133,15 @@ __global__ void __launch_bounds__(2 * NC, NC == 32 ? 6 : (NC == 160 ? 1 : 256 / 
                         const double* a = en.kmode == 1
                             ? en.kst + (size_t)(r >> 5) * 32 * en.kld + (size_t)cc * 32 + (r & 31)
                             : en.kst + (size_t)(cc >> 5) * 32 * en.kld + (size_t)r * 32 + (cc & 31);
-                        kv[c] = (kc < KB_K && er < nrows && kc < nk) ? __ldg(a) : 0.0;
+                        kv[c] = (kc < KK && er < nrows && kc < nk) ? __ldg(a) : 0.0;
                     }
 #pragma unroll
                     for (int c = 0; c < EPT; ++c)
-                        if (ec0 + c * EST < KB_K) Ks[ec0 + c * EST][er] = kv[c];
+                        if (ec0 + c * EST < KK) Ks[ec0 + c * EST][er] = kv[c];
                 }
                 __syncthreads();
 #pragma unroll
-                for (int ks = 0; ks < KB_K / 4; ++ks) {
+                for (int ks = 0; ks < KK / 4; ++ks) {
                     double af[4], bf[4];
 #pragma unroll
                     for (int a = 0; a < 4; ++a) af[a] = Ks[ks * 4 + q][wm * 32 + a * 8 + g];
@@ -403,10 +417,10 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     ProfScope prof(s, "kblock_dmma", fl, by);
     const unsigned nb = (unsigned)work.size();
 #define SPD_KB_LAUNCH(KID)                                                                                    \
-    if (NC == 160) kblock_kernel<KID, 160><<<nb, 320, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
-    else if (NC == 128) kblock_kernel<KID, 128><<<nb, 256, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);  \
-    else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); \
-    else kblock_kernel<KID, 32><<<nb, 64, 0, s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
+    if (NC == 160) { kb_attr(kblock_kernel<KID, 160>, kb_smem_bytes(160)); kblock_kernel<KID, 160><<<nb, 320, kb_smem_bytes(160), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); } \
+    else if (NC == 128) { kb_attr(kblock_kernel<KID, 128>, kb_smem_bytes(128)); kblock_kernel<KID, 128><<<nb, 256, kb_smem_bytes(128), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); } \
+    else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, kb_smem_bytes(64), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); \
+    else kblock_kernel<KID, 32><<<nb, 64, kb_smem_bytes(32), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
     switch (kp.id) {
     case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
     case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
