@@ -211,11 +211,15 @@ enum {
     SPD_Q_SHARD_WORK = 31,  /* int64[2]: nodes whose per-node work (H2: proxy ID; HSS:
                                factorisation, QRCP, bases) this process computed, and
                                the number of such nodes; equal unless sharded (§8(e)) */
-    SPD_Q_SYM_STORE = 32    /* int64[2] (H2 handle): bytes of stored symmetric blocks on this
+    SPD_Q_SYM_STORE = 32,   /* int64[2] (H2 handle): bytes of stored symmetric blocks on this
                                process and their number of pieces (0 before the first k = 1
                                product / PCG, or before the first multi-vector product when
                                the store fits SPD_STORE_FRAC = 0.25 of the free memory, and
                                after h2_release_store); sharded: the blocks touching owned nodes */
+    SPD_Q_COMM_BYTES = 33   /* int64[2] (H2 handle): bytes this process has received through the
+                               library's collectives on the handle's communicator so far (broadcast
+                               ranges of the other ranks, all-reduced buffers) and the number of
+                               collective calls; 0 without a real communicator (§8(e) evidence) */
 };
 spd_status spd_query(const void* handle, int what, void* host_buf, size_t bytes);
 

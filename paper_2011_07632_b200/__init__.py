@@ -23,6 +23,7 @@ Q_LIST_COUNTS, Q_NEAR, Q_TYPE3, Q_TYPE1 = 9, 10, 11, 12
 Q_HSS_RANKS, Q_HSS_EXPORT_SIZE, Q_HSS_EXPORT, Q_HSS_PIVOTS, Q_TIMINGS = 20, 21, 22, 23, 30
 Q_SHARD_WORK = 31
 Q_SYM_STORE = 32
+Q_COMM_BYTES = 33
 
 
 class SpdError(RuntimeError):
@@ -226,6 +227,10 @@ class H2:
     def sym_store(self):
         """(bytes, pieces) of the stored symmetric k = 1 blocks on this process."""
         return tuple(int(v) for v in self.query(Q_SYM_STORE, np.int64, 2))
+
+    def comm_bytes(self):
+        """(bytes received through the library's collectives so far, collective calls)."""
+        return tuple(int(v) for v in self.query(Q_COMM_BYTES, np.int64, 2))
 
     def proxies(self, node):
         n_p = 4096 if self.d == 2 else 6144

@@ -282,6 +282,14 @@ spd_status spd_query(const void* handle, int what, void* buf, size_t bytes) {
             std::memcpy(buf, v, sizeof(v));
             return SPD_OK;
         }
+        if (what == SPD_Q_COMM_BYTES) {
+            SPD_REQUIRE(!hss_if_hss(handle), "spd_query: SPD_Q_COMM_BYTES needs an H2 handle");
+            const spd_comm_s* c = ((const spd_h2_s*)handle)->comm;
+            const int64_t v[2] = {c ? c->bytes_in : 0, c ? c->ncoll : 0};
+            need(bytes, sizeof(v));
+            std::memcpy(buf, v, sizeof(v));
+            return SPD_OK;
+        }
         if (what == SPD_Q_SHARD_WORK) {
             const spd_hss_s* H = hss_if_hss(handle);
             const int64_t* sw = H ? hss_shard_work(H) : ((const spd_h2_s*)handle)->shard_work;

@@ -137,6 +137,9 @@ int shard_owner(const spd_comm_s* c, int count, int a) {
 void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::vector<int64_t>& begin,
                        const std::vector<int64_t>& end, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;   // one copy of everything already
+    for (int q = 0; q < c->nranks; ++q)
+        if (q != c->rank && end[q] > begin[q]) c->bytes_in += (end[q] - begin[q]) * (int64_t)elem;
+    c->ncoll += 1;
     if (c->hosted) {
         SPD_CUDA(cudaStreamSynchronize(s));
         for (int q = 0; q < c->nranks; ++q) {
@@ -164,10 +167,13 @@ void comm_bcast_ranges(const spd_comm_s* c, void* buf, size_t elem, const std::v
 void comm_bcast_rows(const spd_comm_s* c, double* buf, int64_t ld, int ncols, const std::vector<int64_t>& begin,
                      const std::vector<int64_t>& end, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
-    if (c->hosted) {
+    if (c->hosted) {                               // (counted per column by comm_bcast_ranges)
         for (int j = 0; j < ncols; ++j) comm_bcast_ranges(c, buf + (size_t)j * ld, sizeof(double), begin, end, s);
         return;
     }
+    for (int q = 0; q < c->nranks; ++q)
+        if (q != c->rank && end[q] > begin[q]) c->bytes_in += (end[q] - begin[q]) * (int64_t)sizeof(double) * ncols;
+    c->ncoll += 1;
     NcclApi& api = nccl();
     constexpr int kGroupOps = 512;                 // bounded group size
     int ops = 0;
@@ -188,11 +194,15 @@ void comm_bcast_rows(const spd_comm_s* c, double* buf, int64_t ld, int ncols, co
 
 void comm_allreduce_sum(const spd_comm_s* c, double* buf, size_t n, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
+    c->bytes_in += (int64_t)(n * sizeof(double));  // the summed buffer (the ring moves ~2x (P-1)/P of it)
+    c->ncoll += 1;
     if (c->hosted) return host_allreduce<double>(c, buf, n, s, c->host.allreduce_sum_f64);
     check(nccl().allreduce(buf, buf, n, NCCL_FLOAT64, NCCL_SUM, c->nccl, s), "ncclAllReduce");
 }
 void comm_allreduce_sum(const spd_comm_s* c, int* buf, size_t n, cudaStream_t s) {
     if (!c || c->nranks <= 1 || c->virt) return;
+    c->bytes_in += (int64_t)(n * sizeof(int));
+    c->ncoll += 1;
     if (c->hosted) return host_allreduce<int>(c, buf, n, s, c->host.allreduce_sum_i32);
     check(nccl().allreduce(buf, buf, n, NCCL_INT32, NCCL_SUM, c->nccl, s), "ncclAllReduce");
 }

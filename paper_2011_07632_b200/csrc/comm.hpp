@@ -9,6 +9,10 @@ struct spd_comm_s {
     void* nccl = nullptr;       // ncclComm_t
     bool hosted = false;        // host-staged collectives through caller callbacks
     spd_host_coll host{};
+    // bytes this process received through the library's collectives (broadcast ranges of
+    // the other ranks, all-reduced buffers): exchange-volume evidence (SPD_Q_COMM_BYTES)
+    mutable int64_t bytes_in = 0;
+    mutable int64_t ncoll = 0;
 };
 
 namespace spd {

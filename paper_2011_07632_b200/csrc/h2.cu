@@ -705,14 +705,14 @@ static void near_descs(const spd_h2_s* h, const double* x, int64_t ldx, double* 
 
 // up pass: xh[l] (S_l x k, ld S_l) = E^T [x_leaf | xh children], levels 1..top
 void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::vector<double*>& xh, int top,
-           cudaStream_t s) {
-    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_up_vec(h, x, xh, top, s); return; }
+           cudaStream_t s, const BasisFilter* f) {
+    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_up_vec(h, x, xh, top, s, f); return; }
     const TreeH& t = h->tree;
     for (int lk = 1; lk <= top; ++lk) {
         const H2Level& lv = h->lv[lk];
         std::vector<GemmDesc> gd;
         for (int a = 0; a < lv.count; ++a) {
-            if (lv.rank[a] == 0) continue;
+            if (lv.rank[a] == 0 || (f && !f->keep(lk, lv.count, a))) continue;
             const int i = lv.first + a;
             GemmDesc g;
             g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
@@ -732,14 +732,14 @@ void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::ve
 
 // down pass: children of level-l nodes += E yh[l] for l = top..2; y_leaf += E yh[1]
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
-             cudaStream_t s) {
-    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_down_vec(h, yh, top, y, s); return; }
+             cudaStream_t s, const BasisFilter* f) {
+    if (k == 1 && !getenv("SPD_BASIS_GEMM")) { h2_down_vec(h, yh, top, y, s, f); return; }
     const TreeH& t = h->tree;
     for (int lk = top; lk >= 1; --lk) {
         const H2Level& lv = h->lv[lk];
         std::vector<GemmDesc> gd;
         for (int a = 0; a < lv.count; ++a) {
-            if (lv.rank[a] == 0) continue;
+            if (lv.rank[a] == 0 || (f && !f->keep(lk, lv.count, a))) continue;
             const int i = lv.first + a;
             GemmDesc g;
             g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
@@ -771,6 +771,43 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         const int o = shard_owner(cm, count, a);
         return o < 0 || o == cm->rank;
     };
+    // sharded basis passes: the up pass over owned nodes of the sharded levels (>= P
+    // nodes), the owners' x^ of those levels exchanged (Type-3 partners of owned nodes and
+    // the redundant levels above read them), then the redundant levels; the down pass over
+    // the redundant levels and the owned nodes of the sharded levels only
+    int ls = 0;                                   // highest sharded level
+    if (shard)
+        for (int lk = 1; lk < L; ++lk) if (t.count(lk) >= cm->nranks) ls = lk;
+    auto up = [&](const double* xin, int64_t ldxin, int kk, const std::vector<double*>& xh) {
+        if (!shard) { h2_up(h, xin, ldxin, kk, xh, L - 1, s); return; }
+        BasisFilter f;
+        f.P = cm->nranks; f.rank = cm->rank; f.lo = 1; f.hi = ls;
+        h2_up(h, xin, ldxin, kk, xh, L - 1, s, &f);
+        const int P = cm->nranks;
+        for (int lk = 1; lk <= ls; ++lk) {
+            const H2Level& lv = h->lv[lk];
+            const int per = lv.count / P;
+            std::vector<int64_t> bq(P), eq(P);
+            for (int q = 0; q < P; ++q) {
+                bq[q] = lv.off[q * per] * kk;
+                eq[q] = lv.off[std::min(lv.count, (q + 1) * per)] * kk;
+            }
+            if (kk == 1) comm_bcast_ranges(cm, xh[lk], sizeof(double), bq, eq, s);
+            else {                                // x^ is S x k column-major: per column
+                for (int q = 0; q < P; ++q) { bq[q] /= kk; eq[q] /= kk; }
+                comm_bcast_rows(cm, xh[lk], lv.S, kk, bq, eq, s);
+            }
+        }
+        BasisFilter g;
+        g.lo = ls + 1;
+        h2_up(h, xin, ldxin, kk, xh, L - 1, s, &g);
+    };
+    auto down = [&](const std::vector<double*>& yh, double* yout, int64_t ldyout, int kk) {
+        if (!shard) { h2_down(h, yh, L - 1, yout, ldyout, kk, s); return; }
+        BasisFilter f;
+        f.P = cm->nranks; f.rank = cm->rank;
+        h2_down(h, yh, L - 1, yout, ldyout, kk, s, &f);
+    };
     auto exchange_rows = [&]() {                  // owners' leaf rows -> every rank
         const int P = cm->nranks, per = nl / P;
         std::vector<int64_t> rb(P), re(P);
@@ -789,10 +826,10 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         if (L > 1) {
             ensure_ws(h, 1, s);
             for (int lk = 1; lk < L; ++lk) { xh[lk] = h->xh[lk].p; yh[lk] = h->yh[lk].p; }
-            h2_up(h, x, ldx, 1, xh, L - 1, s);
+            up(x, ldx, 1, xh);
         }
         h2sym_apply(h, x, y, xh, yh, s);
-        if (L > 1) h2_down(h, yh, L - 1, y, ldy, 1, s);
+        if (L > 1) down(yh, y, ldy, 1);
         if (shard) exchange_rows();
         return;
     }
@@ -821,7 +858,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         yh[lk] = h->yh[lk].p;
         if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].S * k, s));
     }
-    h2_up(h, x, ldx, k, xh, L - 1, s);
+    up(x, ldx, k, xh);
     // near field and the Type-3 couplings of every level in ONE launch (one balanced
     // work list; skeleton blocks carry no ids, so the shift only reaches near blocks)
     for (int lk = 1; lk < L; ++lk) {
@@ -849,7 +886,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         }
     }
     kblock_apply(s, h->kp, h->kern.shift, h->d, blocks, targets, entries);
-    h2_down(h, yh, L - 1, y, ldy, k, s);
+    down(yh, y, ldy, k);
     if (shard) exchange_rows();
 }
 

@@ -106,13 +106,24 @@ void permute_rows(cudaStream_t s, const int64_t* perm, int64_t N, int k, const d
 void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s);
 void h2_prepare(spd_h2_s* h, int k, cudaStream_t s);   // allocate matvec workspace for width k
 void h2_perm_ws(spd_h2_s* h, int k, double** xt, double** yt);   // N x k permutation buffers (handle-owned)
+// which nodes a basis pass covers: levels [lo, hi], and at levels with >= P nodes only
+// those of subtree `rank` (the sharded product; P = 1: every node)
+struct BasisFilter {
+    int lo = 1, hi = 1 << 30, P = 1, rank = 0;
+    bool keep(int level, int count, int a) const {
+        if (level < lo || level > hi) return false;
+        return P <= 1 || count < P || a / (count / P) == rank;
+    }
+};
 void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::vector<double*>& xh, int top,
-           cudaStream_t s);
+           cudaStream_t s, const BasisFilter* f = nullptr);
 void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, int64_t ldy, int k,
-             cudaStream_t s);
+             cudaStream_t s, const BasisFilter* f = nullptr);
 // k = 1 basis passes in interpolative form (h2basis.cu)
-void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s);
-void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s);
+void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s,
+               const BasisFilter* f = nullptr);
+void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s,
+                 const BasisFilter* f = nullptr);
 size_t h2sym_bytes(const spd_h2_s* h);
 void h2sym_build(spd_h2_s* h, double budget_bytes, cudaStream_t s);
 // kernel blocks of multi-vector products from the symmetric store (built on demand when

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(PH_T) basis_down_kernel(const BasisItem* __res
 
 // work items of the up pass, level 1..top (levels[l]); smax_out: largest n_c - s
 std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const double* x, const std::vector<double*>& xh,
-                                                  int top, int* ncmax_out, std::vector<double>* bytes) {
+                                                  int top, int* ncmax_out, std::vector<double>* bytes,
+                                                  const BasisFilter* f) {
     const TreeH& t = h->tree;
     std::vector<std::vector<BasisItem>> out(top + 1);
     int ncmax = 1;
@@ -33,7 +34,7 @@ std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const doubl
         const H2Level& lv = h->lv[lk];
         for (int a = 0; a < lv.count; ++a) {
             const int sr = lv.rank[a];
-            if (sr == 0) continue;
+            if (sr == 0 || (f && !f->keep(lk, lv.count, a))) continue;
             const int i = lv.first + a;
             const double* in;
             if (lk == 1) in = x + t.begin[i];
@@ -54,7 +55,8 @@ std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const doubl
 
 // work items of the down pass, level 1..top (levels[l]); smax_out: largest s
 std::vector<std::vector<BasisItem>> basis_down_plan(const spd_h2_s* h, const std::vector<double*>& yh, int top,
-                                                    double* y, int* smax_out, std::vector<double>* bytes) {
+                                                    double* y, int* smax_out, std::vector<double>* bytes,
+                                                    const BasisFilter* f) {
     const TreeH& t = h->tree;
     std::vector<std::vector<BasisItem>> out(top + 1);
     int smax = 1;
@@ -63,7 +65,7 @@ std::vector<std::vector<BasisItem>> basis_down_plan(const spd_h2_s* h, const std
         const H2Level& lv = h->lv[lk];
         for (int a = 0; a < lv.count; ++a) {
             const int sr = lv.rank[a];
-            if (sr == 0) continue;
+            if (sr == 0 || (f && !f->keep(lk, lv.count, a))) continue;
             const int i = lv.first + a;
             double* o;
             if (lk == 1) o = y + t.begin[i];
@@ -84,10 +86,11 @@ std::vector<std::vector<BasisItem>> basis_down_plan(const spd_h2_s* h, const std
 }
 
 // xh[l] = E^T [x_leaf | xh children] for levels 1..top (k = 1)
-void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s) {
+void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& xh, int top, cudaStream_t s,
+               const BasisFilter* f) {
     int ncmax = 1;
     std::vector<double> by;
-    auto plan = basis_up_plan(h, x, xh, top, &ncmax, &by);
+    auto plan = basis_up_plan(h, x, xh, top, &ncmax, &by, f);
     const size_t smem = sizeof(double) * (ncmax + PH_W * 32);
     if (smem > 48 * 1024)
         SPD_CUDA(cudaFuncSetAttribute(basis_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -101,10 +104,11 @@ void h2_up_vec(const spd_h2_s* h, const double* x, const std::vector<double*>& x
 }
 
 // children of level-l nodes += E yh[l] for l = top..2; y_leaf += E yh[1]  (k = 1)
-void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s) {
+void h2_down_vec(const spd_h2_s* h, const std::vector<double*>& yh, int top, double* y, cudaStream_t s,
+                 const BasisFilter* f) {
     int smax = 1;
     std::vector<double> by;
-    auto plan = basis_down_plan(h, yh, top, y, &smax, &by);
+    auto plan = basis_down_plan(h, yh, top, y, &smax, &by, f);
     const size_t smem = sizeof(double) * (smax + PH_W * 32);
     if (smem > 48 * 1024)
         SPD_CUDA(cudaFuncSetAttribute(basis_down_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -13,6 +13,7 @@
 // chunk) are reduced in chunk order.
 #include "hss.hpp"
 #include "phases.cuh"
+#include "comm.hpp"
 #include <algorithm>
 
 namespace spd {
@@ -85,11 +86,13 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
     };
     HsPhase ph;
     ph.mode = 0;
+    ph.level = 1;
     for (int a = 0; a < l1.count; ++a) {
         const int64_t off = t.begin[l1.first + a];
         if (!l1.m[a]) continue;
         ph.nodes.push_back({l1.Finv.p + l1.F_off[a], l1.P.p + l1.V_off[a], l1.m[a], l1.rank[a], b + off, nullptr,
                             nullptr, z + off, zl[1] + l1.off[a], zs[1] + l1.off[a], nullptr});
+        ph.idx.push_back(a);
     }
     up_items(ph);
     out.push_back(ph);
@@ -100,12 +103,14 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
         const HssLevel& lv = H->lv[l];
         const HssLevel& pv = H->lv[l - 1];
         ph = HsPhase();
+        ph.level = l;
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
             if (!lv.m[a]) continue;
             ph.nodes.push_back({lv.Finv.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a],
                                 zl[l - 1] + pv.off[c1], nullptr, nullptr, ub[l] + pv.off[c1], zl[l] + lv.off[a],
                                 zs[l] + lv.off[a], nullptr});
+            ph.idx.push_back(a);
         }
         up_items(ph);
         out.push_back(ph);
@@ -142,23 +147,27 @@ std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double*
         const HssLevel& pv = H->lv[l - 1];
         ph = HsPhase();
         ph.mode = 1;
+        ph.level = l;
         for (int a = 0; a < lv.count; ++a) {
             const int c1 = 2 * (lv.first + a) + 1 - pv.first;
             if (!lv.m[a]) continue;
             ph.nodes.push_back({lv.Finv.p + lv.F_off[a], lv.P.p + lv.V_off[a], lv.m[a], lv.rank[a],
                                 ub[l] + pv.off[c1], xh_of(l) + lv.off[a], zs[l] + lv.off[a], nullptr, nullptr, nullptr,
                                 zl[l - 1] + pv.off[c1]});
+            ph.idx.push_back(a);
         }
         down_items(ph);
         out.push_back(ph);
     }
     ph = HsPhase();
     ph.mode = 1;
+    ph.level = 1;
     for (int a = 0; a < l1.count; ++a) {
         const int64_t off = t.begin[l1.first + a];
         if (!l1.m[a]) continue;
         ph.nodes.push_back({l1.Finv.p + l1.F_off[a], l1.P.p + l1.V_off[a], l1.m[a], l1.rank[a], z + off,
                             xh_of(1) + l1.off[a], zs[1] + l1.off[a], nullptr, nullptr, nullptr, x + off});
+        ph.idx.push_back(a);
     }
     down_items(ph);
     out.push_back(ph);
@@ -196,8 +205,67 @@ void bj_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, cudaStrea
     for (const auto& ph : bj_solve_plan(H, b, x, z)) launch_phase(s, ph);
 }
 
+// Subtree-sharded solve (real communicator of P ranks): at every level
+// with >= P nodes a rank runs the up and down work of its own subtree's nodes only
+// (shard_owner, the builds' plan); after the up sweep of the highest sharded level the
+// owners' coarse coefficients zh of that level are exchanged (the split-level exchange:
+// sum of its ranks, ~P r doubles), the levels above, the root / top operator run
+// redundantly on every rank, the down sweep again only over owned nodes, and finally the
+// owners' rows of x are exchanged so every rank holds the whole solution (N doubles).
+static void hss_solve_sharded(spd_hss_s* H, std::vector<HsPhase> plan, double* x, const std::vector<double*>& zl,
+                              cudaStream_t s) {
+    const spd_comm_s* c = H->h2->comm;
+    const TreeH& t = H->h2->tree;
+    const int P = c->nranks;
+    auto sharded = [&](int level) { return level >= 1 && H->lv[level].count >= P; };
+    int le = 0;                                       // highest sharded level of the up sweep
+    for (const auto& ph : plan)
+        if (ph.mode == 0 && ph.level > 0 && sharded(ph.level)) le = std::max(le, ph.level);
+    for (auto& ph : plan) {
+        if ((ph.mode == 0 || ph.mode == 1) && ph.level > 0 && sharded(ph.level)) {
+            const int cnt = H->lv[ph.level].count;
+            HsPhase f;
+            f.mode = ph.mode;
+            f.level = ph.level;
+            std::vector<int> remap(ph.nodes.size(), -1);
+            for (size_t q = 0; q < ph.nodes.size(); ++q)
+                if (shard_owner(c, cnt, ph.idx[q]) == c->rank) {
+                    remap[q] = (int)f.nodes.size();
+                    f.nodes.push_back(ph.nodes[q]);
+                    f.idx.push_back(ph.idx[q]);
+                }
+            for (const auto& it : ph.items)
+                if (remap[it.node] >= 0) f.items.push_back({remap[it.node], it.kind, it.tile});
+            launch_phase(s, f);
+        } else {
+            launch_phase(s, ph);
+        }
+        if (ph.mode == 0 && ph.level == le && le > 0) {   // split-level exchange of zh
+            const HssLevel& lv = H->lv[le];
+            std::vector<int64_t> bq(P), eq(P);
+            const int per = lv.count / P;
+            for (int q = 0; q < P; ++q) { bq[q] = lv.off[q * per]; eq[q] = lv.off[std::min(lv.count, (q + 1) * per)]; }
+            comm_bcast_ranges(c, zl[le], sizeof(double), bq, eq, s);
+        }
+    }
+    // the owners' rows of x (their leaves are contiguous in tree order)
+    const HssLevel& l1 = H->lv[1];
+    const int per = l1.count / P;
+    std::vector<int64_t> rb(P), re(P);
+    for (int q = 0; q < P; ++q) {
+        rb[q] = t.begin[l1.first + q * per];
+        re[q] = t.end[l1.first + std::min(l1.count, (q + 1) * per) - 1];
+    }
+    comm_bcast_ranges(c, x, sizeof(double), rb, re, s);
+}
+
 void hss_solve_vec(spd_hss_s* H, const double* b, double* x, double* z, const std::vector<double*>& zl,
                    const std::vector<double*>& zs, const std::vector<double*>& ub, cudaStream_t s) {
+    const spd_comm_s* c = H->h2->comm;
+    if (comm_real(c) && H->lv[1].count >= c->nranks && !getenv("SPD_SOLVE_REPLICATED")) {
+        hss_solve_sharded(H, hss_solve_plan(H, b, x, z, zl, zs, ub), x, zl, s);
+        return;
+    }
     for (const auto& ph : hss_solve_plan(H, b, x, z, zl, zs, ub)) launch_phase(s, ph);
 }
 

@@ -527,10 +527,15 @@ __device__ __forceinline__ void hss_item_warp(const HsNode* __restrict__ nodes, 
 
 // ================================================================= host-side plans (work items)
 std::vector<std::vector<BasisItem>> basis_up_plan(const spd_h2_s* h, const double* x, const std::vector<double*>& xh,
-                                                  int top, int* ncmax_out, std::vector<double>* bytes);
+                                                  int top, int* ncmax_out, std::vector<double>* bytes,
+                                                  const BasisFilter* f = nullptr);
 std::vector<std::vector<BasisItem>> basis_down_plan(const spd_h2_s* h, const std::vector<double*>& yh, int top,
-                                                    double* y, int* smax_out, std::vector<double>* bytes);
-struct HsPhase { int mode = 0; std::vector<HsNode> nodes; std::vector<HsItem> items; };
+                                                    double* y, int* smax_out, std::vector<double>* bytes,
+                                                    const BasisFilter* f = nullptr);
+// level: the tree level of an up (mode 0) / down (mode 1) phase, 0 for the root / top
+// operator; idx: each node's index within its level (the subtree-sharded solve keeps the
+// owned ones)
+struct HsPhase { int mode = 0; std::vector<HsNode> nodes; std::vector<HsItem> items; int level = 0; std::vector<int> idx; };
 std::vector<HsPhase> bj_solve_plan(const spd_hss_s* H, const double* b, double* x, double* z);
 std::vector<HsPhase> hss_solve_plan(const spd_hss_s* H, const double* b, double* x, double* z,
                                     const std::vector<double*>& zl, const std::vector<double*>& zs,

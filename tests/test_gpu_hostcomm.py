@@ -38,14 +38,25 @@ def _run(spd, synth, cfg, comm, skel):
     h = spd.h2_build(X, cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol, comm=comm, inject_skeletons=skel)
     M = spd.spdhss_build(h, 40, 1e-3, seed=11)
     b = torch.tensor(synth.multivec(cfg.n, 1)[:, 0], device="cuda")
+    c0 = h.comm_bytes()
     x = spd.hss_solve(M, b).cpu().numpy()
+    c1 = h.comm_bytes()
     xp, rep = spd.pcg_solve(h, M, b, tol=1e-8, maxit=500)   # sharded k=1 products inside
     xp = xp.cpu().numpy()
     y = spd.h2_matvec(h, b).cpu().numpy()
     Xm = torch.tensor(synth.multivec(cfg.n, 8).T.copy(), device="cuda").t()     # column-major n x 8
     ym = spd.h2_matvec(h, Xm).t().cpu().numpy()        # k >= 2: sharded product + row exchange
     ex = M.export()
-    return {"sym": h.sym_store(), "h2_work": h.shard_work(), "hss_work": M.shard_work(), "h2_ranks": h.ranks(), "hss_ranks": M.ranks(),
+    # rows of the leaves this process owns (subtree sharding: leaf a of L1 -> rank a // (count / P))
+    nodes = h.nodes().reshape(-1, 2)
+    nl = (len(nodes) + 1) // 2
+    P = comm.nranks if comm is not None else 1
+    rk = comm.rank if comm is not None else 0
+    per = nl // P
+    leaves = nodes[nl - 1:]
+    own_rows = int(sum(e - b_ for b_, e in leaves[rk * per:(rk + 1) * per]))
+    return {"solve_bytes": c1[0] - c0[0], "solve_colls": c1[1] - c0[1], "own_rows": own_rows, "n": cfg.n,
+            "sym": h.sym_store(), "h2_work": h.shard_work(), "hss_work": M.shard_work(), "h2_ranks": h.ranks(), "hss_ranks": M.ranks(),
             "x": x, "y": y, "ym": ym, "xp": xp, "iters": rep.iters,
             "sha": "".join(hashlib.sha256(a.tobytes()).hexdigest() for a in (ex, x, y, ym, xp))}
 
@@ -105,6 +116,19 @@ def test_sharded_build_with_real_exchanges(P, n, leaf):
         assert sum(res[r][key][0] for r in range(P)) >= total
     print("P", P, "work", [res[r]["hss_work"] for r in range(P)], "sym", [res[r]["sym"] for r in range(P)], ref["sym"], "x rel",
           np.linalg.norm(got["x"] - ref["x"]) / np.linalg.norm(ref["x"]), "iters", got["iters"], ref["iters"])
+    # the HSS solve is sharded too (§8(e)): a rank receives the other ranks' rows of x and the
+    # coefficients zh of the split level (the highest sharded level at or below the dense
+    # top operator; <= 40 per node here, rank cap 40, so at most the other ranks' leaves'),
+    # nothing else -- against 0 for a replicated solve
+    assert ref["solve_bytes"] == 0
+    for r in range(P):
+        rows = 8 * (res[r]["n"] - res[r]["own_rows"])
+        coef = res[r]["solve_bytes"] - rows
+        print("rank", r, "solve exchange", res[r]["solve_bytes"], "bytes: rows", rows, "coefficients", coef,
+              "collectives", res[r]["solve_colls"])
+        assert res[r]["solve_colls"] == 2
+        nl = (len(res[r]["h2_ranks"]) + 1) // 2
+        assert 0 < coef <= 8 * 40 * (nl - nl // P) and coef % 8 == 0
     # the k = 1 block store is split too: each rank holds less than the whole, together >= it
     assert ref["sym"][0] > 0 and all(res[r]["sym"][0] < ref["sym"][0] for r in range(P))
     assert sum(res[r]["sym"][0] for r in range(P)) >= ref["sym"][0]
