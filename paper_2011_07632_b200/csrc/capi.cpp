@@ -91,6 +91,8 @@ spd_status h2_release_store(spd_h2_t h) {
         SPD_REQUIRE(h != nullptr, "h2_release_store: null handle");
         SPD_CUDA(cudaDeviceSynchronize());
         h->sym = spd::H2SymStore();
+        h->kbc.valid = false;                      // its plan may point into the store
+        h->kbc.plan = spd::KbPlan();
         h->stored_mode = -1;
         h->sym_budget = 0.0;
     })

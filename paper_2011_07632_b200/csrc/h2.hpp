@@ -92,6 +92,18 @@ struct spd_h2_s {
     double sym_budget = 0.0;
     double sym_frac = 1.0;         // fraction of the blocks to store (rest: evaluated, overlapping HBM and FP64)
     spd::H2SymStore sym;
+    // plan of the last multi-column product (kblock.cuh KbPlan), replayed while the width,
+    // the buffers, the sharding and the block store are unchanged
+    struct KbCache {
+        bool valid = false;
+        int k = 0;
+        const double* x = nullptr; double* y = nullptr;
+        int64_t ldx = 0, ldy = 0;
+        bool stored = false, shard = false;
+        const double* store = nullptr;
+        const double* xh1 = nullptr;   // the coefficient workspace the plan points into
+        spd::KbPlan plan;
+    } kbc;
 };
 
 namespace spd {

@@ -12,6 +12,7 @@
 #include "kblock.cuh"
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 namespace spd {
 
@@ -328,14 +329,13 @@ static void kblock_vec(cudaStream_t s, const KernelParams& kp, double shift, int
     SPD_LAUNCH();
 }
 
-void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
-                  const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
-                  const std::vector<KbEntry>& entries) {
+bool kblock_plan(cudaStream_t s, const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
+                 const std::vector<KbEntry>& entries, KbPlan& plan) {
+    plan = KbPlan();
     {
         int maxc = 0;
         for (auto& e : entries) maxc = std::max(maxc, e.ncols);
-        if (maxc == 0) return;
-        if (maxc <= 4) { kblock_vec(s, kp, shift, d, blocks, targets, entries, maxc); return; }
+        if (maxc <= 4) return false;
     }
     int maxc_all = 0;
     for (auto& e : entries) maxc_all = std::max(maxc_all, e.ncols);
@@ -387,7 +387,7 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
                 for (int sg = 0; sg < nseg; ++sg) work.push_back({t, tm, tn, cuts[sg], cuts[sg + 1], nslot++});
             }
     }
-    if (work.empty()) return;
+    if (work.empty()) { plan.ok = true; return true; }
     // heaviest items first (crude LPT over the launch order)
     auto wcost = [&](const KbWork& w) {
         long long c = 0;
@@ -402,7 +402,6 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
         for (auto& o : order) sorted.push_back(work[o.second]);
         work.swap(sorted);
     }
-    DBuf<double> partial(std::max<size_t>(1, (size_t)nslot * KB_M * NC));
     double fl = 0, by = 0;
     for (const auto& tg : targets)
         for (int e = tg.e_begin; e < tg.e_end; ++e) {
@@ -410,17 +409,39 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
             fl += 2.0 * nr * ns * nc;
             by += 8.0 * (ns * nc + 2.0 * nr * nc);
         }
-    DevArray<KbBlock> db(s, blocks);
-    DevArray<KbTarget> dt(s, targets);
-    DevArray<KbEntry> de(s, entries);
-    DevArray<KbWork> dw(s, work);
-    ProfScope prof(s, "kblock_dmma", fl, by);
-    const unsigned nb = (unsigned)work.size();
+    plan.NC = NC;
+    plan.nwork = (int)work.size();
+    plan.nred = (int)red.size();
+    plan.fl = fl;
+    plan.by = by;
+    plan.partial.alloc(std::max<size_t>(1, (size_t)nslot * KB_M * NC));
+    plan.b.upload(blocks, s);
+    plan.t.upload(targets, s);
+    plan.e.upload(entries, s);
+    std::vector<char> wb(sizeof(KbWork) * work.size()), rb(sizeof(KbRed) * std::max<size_t>(1, red.size()));
+    std::memcpy(wb.data(), work.data(), wb.size());
+    if (!red.empty()) std::memcpy(rb.data(), red.data(), sizeof(KbRed) * red.size());
+    plan.w.upload(wb, s);
+    plan.r.upload(rb, s);
+    plan.ok = true;
+    return true;
+}
+
+void kblock_run(cudaStream_t s, const KernelParams& kp, double shift, int d, const KbPlan& plan) {
+    if (!plan.ok || plan.nwork == 0) return;
+    const int NC = plan.NC;
+    const KbBlock* bp = plan.b.p;
+    const KbTarget* tp = plan.t.p;
+    const KbEntry* ep = plan.e.p;
+    const KbWork* wp = (const KbWork*)plan.w.p;
+    double* pp = plan.partial.p;
+    ProfScope prof(s, "kblock_dmma", plan.fl, plan.by);
+    const unsigned nb = (unsigned)plan.nwork;
 #define SPD_KB_LAUNCH(KID)                                                                                    \
-    if (NC == 160) { kb_attr(kblock_kernel<KID, 160>, kb_smem_bytes(160)); kblock_kernel<KID, 160><<<nb, 320, kb_smem_bytes(160), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); } \
-    else if (NC == 128) { kb_attr(kblock_kernel<KID, 128>, kb_smem_bytes(128)); kblock_kernel<KID, 128><<<nb, 256, kb_smem_bytes(128), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); } \
-    else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, kb_smem_bytes(64), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p); \
-    else kblock_kernel<KID, 32><<<nb, 64, kb_smem_bytes(32), s>>>(kp, shift, d, db.p, dt.p, de.p, dw.p, partial.p);
+    if (NC == 160) { kb_attr(kblock_kernel<KID, 160>, kb_smem_bytes(160)); kblock_kernel<KID, 160><<<nb, 320, kb_smem_bytes(160), s>>>(kp, shift, d, bp, tp, ep, wp, pp); } \
+    else if (NC == 128) { kb_attr(kblock_kernel<KID, 128>, kb_smem_bytes(128)); kblock_kernel<KID, 128><<<nb, 256, kb_smem_bytes(128), s>>>(kp, shift, d, bp, tp, ep, wp, pp); } \
+    else if (NC == 64) kblock_kernel<KID, 64><<<nb, 128, kb_smem_bytes(64), s>>>(kp, shift, d, bp, tp, ep, wp, pp); \
+    else kblock_kernel<KID, 32><<<nb, 64, kb_smem_bytes(32), s>>>(kp, shift, d, bp, tp, ep, wp, pp);
     switch (kp.id) {
     case SPD_K_GAUSSIAN: SPD_KB_LAUNCH(SPD_K_GAUSSIAN); break;
     case SPD_K_MATERN32: SPD_KB_LAUNCH(SPD_K_MATERN32); break;
@@ -430,14 +451,27 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
     }
 #undef SPD_KB_LAUNCH
     SPD_LAUNCH();
-    if (!red.empty()) {
-        DevArray<KbRed> dr(s, red);
-        if (NC == 160) kb_reduce_kernel<160><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
-        else if (NC == 128) kb_reduce_kernel<128><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
-        else if (NC == 64) kb_reduce_kernel<64><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
-        else kb_reduce_kernel<32><<<(unsigned)red.size(), 256, 0, s>>>(dr.p, partial.p);
+    if (plan.nred > 0) {
+        const KbRed* rp = (const KbRed*)plan.r.p;
+        const unsigned nr = (unsigned)plan.nred;
+        if (NC == 160) kb_reduce_kernel<160><<<nr, 256, 0, s>>>(rp, pp);
+        else if (NC == 128) kb_reduce_kernel<128><<<nr, 256, 0, s>>>(rp, pp);
+        else if (NC == 64) kb_reduce_kernel<64><<<nr, 256, 0, s>>>(rp, pp);
+        else kb_reduce_kernel<32><<<nr, 256, 0, s>>>(rp, pp);
         SPD_LAUNCH();
     }
+}
+
+void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
+                  const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
+                  const std::vector<KbEntry>& entries) {
+    int maxc = 0;
+    for (auto& e : entries) maxc = std::max(maxc, e.ncols);
+    if (maxc == 0) return;
+    if (maxc <= 4) { kblock_vec(s, kp, shift, d, blocks, targets, entries, maxc); return; }
+    KbPlan plan;
+    kblock_plan(s, blocks, targets, entries, plan);
+    kblock_run(s, kp, shift, d, plan);
 }
 
 }  // namespace spd

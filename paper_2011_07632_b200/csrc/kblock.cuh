@@ -31,4 +31,25 @@ void kblock_apply(cudaStream_t s, const KernelParams& kp, double shift, int d,
                   const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
                   const std::vector<KbEntry>& entries);
 
+// the device-side plan of one multi-column (ncols > 4) kblock product: descriptor arrays,
+// the balanced work list and the split-target partial slots; built once and replayed
+// (h2_matvec keeps the plan of its last product in the handle: repeated products of the
+// same width on the same buffers skip the host-side planning and the uploads)
+struct KbWork;
+struct KbRed;
+struct KbPlan {
+    bool ok = false;
+    int NC = 0, nwork = 0, nred = 0;
+    double fl = 0, by = 0;
+    DBuf<KbBlock> b;
+    DBuf<KbTarget> t;
+    DBuf<KbEntry> e;
+    DBuf<char> w, r;          // KbWork / KbRed arrays (types private to kblock.cu)
+    DBuf<double> partial;
+};
+// false: the product is empty or narrow (ncols <= 4: the vector kernel, not planned)
+bool kblock_plan(cudaStream_t s, const std::vector<KbBlock>& blocks, const std::vector<KbTarget>& targets,
+                 const std::vector<KbEntry>& entries, KbPlan& plan);
+void kblock_run(cudaStream_t s, const KernelParams& kp, double shift, int d, const KbPlan& plan);
+
 }  // namespace spd

@@ -156,6 +156,41 @@ def test_h2_matvec_block_source_paths(spd, mode, k, monkeypatch):
     assert rel(host(spd.h2_matvec(h, cuda(x))), yo) <= 1e-9
 
 
+def test_h2_matvec_replayed_plan(spd, monkeypatch):
+    """h2_matvec keeps the kblock plan of its last multi-column product in the handle and
+    replays it while the width, buffers, sharding and block store are unchanged: the replayed
+    product is bitwise the planned one, also after products of other widths and after the
+    store is built / released, and equals the oracle's."""
+    import torch
+    cfg = CASES["C2s"]
+    X = synth.points(cfg)
+    h = spd.h2_build(torch.tensor(X, device="cuda"), cfg.kernel, cfg.ell, cfg.shift, cfg.leaf, cfg.h2_tol)
+    _, _, _, ho = built(spd, "C2s")
+    monkeypatch.setenv("SPD_STORE_FRAC", "0")
+    xa, xb = synth.multivec(cfg.n, 64), synth.multivec(cfg.n, 16)
+    ya = host(spd.h2_matvec(h, cuda(xa)))
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xa))), ya)          # replayed plan
+    yb = host(spd.h2_matvec(h, cuda(xb)))                                 # another width: new plan
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xa))), ya)
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xa))), ya)
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xb))), yb)
+    x2 = 2.0 * xa - 1.0                                                    # same buffers, other data
+    monkeypatch.setenv("SPD_MV_NOCACHE", "1")
+    y2 = host(spd.h2_matvec(h, cuda(x2)))
+    monkeypatch.delenv("SPD_MV_NOCACHE")
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(x2))), y2)
+    monkeypatch.delenv("SPD_STORE_FRAC")
+    spd.pcg_solve(h, None, cuda(synth.rhs(cfg)), tol=1e-300, maxit=1)     # builds the store
+    ys = host(spd.h2_matvec(h, cuda(xa)))                                 # store: new plan
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xa))), ys)
+    h.release_store()                                  # (the next product may rebuild it on demand)
+    monkeypatch.setenv("SPD_STORE_FRAC", "0")
+    assert np.array_equal(host(spd.h2_matvec(h, cuda(xa))), ya)          # evaluated again: a new plan
+    yo = np.empty_like(xa)
+    yo[ho.tree.perm] = oracle.h2_matvec(ho, xa[ho.tree.perm])
+    assert rel(ya, yo) <= 1e-9 and rel(ys, yo) <= 1e-9
+
+
 def test_h2_matvec_vs_dense_kernel(spd):
     cfg, X, h, ho = built(spd, "C1s")
     from oracle.kernels import kernel_matrix
