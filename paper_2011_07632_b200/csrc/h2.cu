@@ -517,6 +517,7 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             lv.off[a + 1] = lv.off[a] + lv.rank[a];
         }
         lv.S = lv.off[lv.count];
+        lv.Sw = (lv.S + 7) & ~(int64_t)7;
         lv.E_off.assign(lv.count + 1, 0);
         for (int a = 0; a < lv.count; ++a) lv.E_off[a + 1] = lv.E_off[a] + (int64_t)lv.ncand[a] * lv.rank[a];
         lv.E.alloc(std::max<int64_t>(1, lv.E_off[lv.count]));
@@ -601,8 +602,8 @@ static void ensure_ws(spd_h2_s* h, int k, cudaStream_t s) {
     h->xh.resize(L);
     h->yh.resize(L);
     for (int lk = 1; lk < L; ++lk) {
-        h->xh[lk].alloc(std::max<int64_t>(1, h->lv[lk].S * k));
-        h->yh[lk].alloc(std::max<int64_t>(1, h->lv[lk].S * k));
+        h->xh[lk].alloc(std::max<int64_t>(1, h->lv[lk].Sw * k));
+        h->yh[lk].alloc(std::max<int64_t>(1, h->lv[lk].Sw * k));
     }
     h->ws_k = k;
 }
@@ -720,9 +721,9 @@ void h2_up(const spd_h2_s* h, const double* x, int64_t ldx, int k, const std::ve
             else {
                 const H2Level& pv = h->lv[lk - 1];
                 int c1 = 2 * i + 1 - pv.first;
-                g.B = xh[lk - 1] + pv.off[c1]; g.ldb = (int)pv.S;
+                g.B = xh[lk - 1] + pv.off[c1]; g.ldb = (int)pv.Sw;
             }
-            g.C = xh[lk] + lv.off[a]; g.ldc = (int)lv.S;
+            g.C = xh[lk] + lv.off[a]; g.ldc = (int)lv.Sw;
             g.m = lv.rank[a]; g.n = k; g.k = lv.ncand[a];
             gd.push_back(g);
         }
@@ -743,12 +744,12 @@ void h2_down(const spd_h2_s* h, const std::vector<double*>& yh, int top, double*
             const int i = lv.first + a;
             GemmDesc g;
             g.A = lv.E.p + lv.E_off[a]; g.lda = lv.ncand[a];
-            g.B = yh[lk] + lv.off[a]; g.ldb = (int)lv.S;
+            g.B = yh[lk] + lv.off[a]; g.ldb = (int)lv.Sw;
             if (lk == 1) { g.C = y + t.begin[i]; g.ldc = (int)ldy; }
             else {
                 const H2Level& pv = h->lv[lk - 1];
                 int c1 = 2 * i + 1 - pv.first;
-                g.C = yh[lk - 1] + pv.off[c1]; g.ldc = (int)pv.S;
+                g.C = yh[lk - 1] + pv.off[c1]; g.ldc = (int)pv.Sw;
             }
             g.m = lv.ncand[a]; g.n = k; g.k = lv.rank[a];
             gd.push_back(g);
@@ -795,7 +796,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             if (kk == 1) comm_bcast_ranges(cm, xh[lk], sizeof(double), bq, eq, s);
             else {                                // x^ is S x k column-major: per column
                 for (int q = 0; q < P; ++q) { bq[q] /= kk; eq[q] /= kk; }
-                comm_bcast_rows(cm, xh[lk], lv.S, kk, bq, eq, s);
+                comm_bcast_rows(cm, xh[lk], lv.Sw, kk, bq, eq, s);
             }
         }
         BasisFilter g;
@@ -848,7 +849,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
         for (int lk = 1; lk < L; ++lk) {
             xh[lk] = h->xh[lk].p;
             yh[lk] = h->yh[lk].p;
-            if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].S * k, s));
+            if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].Sw * k, s));
         }
         up(x, ldx, k, xh);
         stage_mark(s, "mv up pass", k);
@@ -880,7 +881,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
     for (int lk = 1; lk < L; ++lk) {
         xh[lk] = h->xh[lk].p;
         yh[lk] = h->yh[lk].p;
-        if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].S * k, s));
+        if (h->lv[lk].S) SPD_CUDA(cudaMemsetAsync(yh[lk], 0, sizeof(double) * h->lv[lk].Sw * k, s));
     }
     stage_mark(s, "mv near descs (host)", k);
     up(x, ldx, k, xh);
@@ -902,7 +903,7 @@ void h2_apply_tree(spd_h2_s* h, const double* x, int64_t ldx, double* y, int64_t
             while (e < T3.size() && T3[e].first == i) {
                 const int bj = T3[e].second - lv.first;
                 if (lv.rank[bj] > 0 && lv.rank[a] > 0) {
-                    entries.push_back({b0 + bj, xh[lk] + lv.off[bj], (int)lv.S, yh[lk] + lv.off[a], (int)lv.S, k});
+                    entries.push_back({b0 + bj, xh[lk] + lv.off[bj], (int)lv.Sw, yh[lk] + lv.off[a], (int)lv.Sw, k});
                     if (stored) h2_use_store(h, lk, a, bj, lv.rank[a], lv.rank[bj], entries.back());
                 }
                 ++e;

@@ -13,6 +13,8 @@ struct H2Level {
     std::vector<int> ncand;       // candidates n_c per node
     std::vector<int64_t> off;     // row offset of node i in the level's coefficient space
     int64_t S = 0;                // sum of ranks
+    int64_t Sw = 0;               // leading dimension of the multi-column x^ / y^ workspaces: S rounded
+                                  // up to a multiple of 8 (16-byte aligned columns for TMA, kblock.cu)
     DBuf<int> skel;               // S skeleton tree positions
     DBuf<double> skelX;           // d x S skeleton coordinates (SoA, stride S)
     std::vector<int64_t> E_off;   // offset of E_i (n_c x s_i, col-major) in E

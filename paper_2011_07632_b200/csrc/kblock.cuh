@@ -1,5 +1,6 @@
 // kblock.cuh -- on-the-fly kernel block x multi-vector interface.
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 
 namespace spd {
@@ -22,7 +23,14 @@ struct KbEntry {            // Y[:, :ncols] += K(target, blocks[src]) X[:, :ncol
     // values include the diagonal shift.
     const double* kst = nullptr;
     int kmode = 0, kld = 0;
+    // set by kblock_plan: X staged by TMA through tensor map tmi of the plan (row coordinate
+    // tr of X's first row); -1: X read by plain loads
+    int tmi = -1, tr = 0;
 };
+// TMA tensor maps of one planned product: one 2-D map (rows x columns, 16 x NC boxes,
+// 128-byte swizzle) per X buffer the entries read
+constexpr int KB_NTMA = 16;
+struct KbTma { CUtensorMap map[KB_NTMA]; unsigned box_bytes[KB_NTMA]; };
 struct KbTarget { int blk; int e_begin, e_end; };
 
 // entries of a target must be contiguous; consecutive entries with the same Y
@@ -40,6 +48,9 @@ struct KbRed;
 struct KbPlan {
     bool ok = false;
     int NC = 0, nwork = 0, nred = 0;
+    int ntma = 0;             // tensor maps in use (0: the register-prefetch kernel)
+    bool tma_mix = false;     // some entries without a map (their X slices prefetched through registers)
+    KbTma tma;
     double fl = 0, by = 0;
     DBuf<KbBlock> b;
     DBuf<KbTarget> t;

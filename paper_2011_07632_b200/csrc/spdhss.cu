@@ -179,7 +179,7 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
     // --- far field: up pass once, coupling into per-bucket coefficients, one down pass per bucket
     std::vector<DBuf<double>> xh(L);
     std::vector<double*> xhp(L, nullptr);
-    for (int l = 1; l < L; ++l) { xh[l].alloc(std::max<int64_t>(1, h->lv[l].S * w)); xhp[l] = xh[l].p; }
+    for (int l = 1; l < L; ++l) { xh[l].alloc(std::max<int64_t>(1, h->lv[l].Sw * w)); xhp[l] = xh[l].p; }
     h2_up(h, om, N, w, xhp, L - 1, s);
     // bucket c holds coefficients for levels 1..c-1
     std::vector<std::vector<DBuf<double>>> yb(L + 1);
@@ -192,7 +192,7 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
         yb[c].resize(c);
         ybp[c].assign(L, nullptr);
         for (int l = 1; l < c; ++l) {
-            yb[c][l].alloc(std::max<int64_t>(1, h->lv[l].S * w));
+            yb[c][l].alloc(std::max<int64_t>(1, h->lv[l].Sw * w));
             yb[c][l].zero(s);
             ybp[c][l] = yb[c][l].p;
         }
@@ -217,7 +217,7 @@ static void lca_bucketed_products(spd_hss_s* H, const double* om, DBuf<double>& 
             for (auto& [c, j] : js) {
                 const int b = j - lv.first;
                 if (lv.rank[a] && lv.rank[b]) {
-                    entries.push_back({b, xhp[l] + lv.off[b], (int)lv.S, ybp[c][l] + lv.off[a], (int)lv.S, w});
+                    entries.push_back({b, xhp[l] + lv.off[b], (int)lv.Sw, ybp[c][l] + lv.off[a], (int)lv.Sw, w});
                     if (stored) h2_use_store(h, l, a, b, lv.rank[a], lv.rank[b], entries.back());
                 }
             }
