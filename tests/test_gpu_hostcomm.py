@@ -84,7 +84,7 @@ def _worker(rank, world, port, n, leaf, skel, q):
         q.put((rank, repr(e)))
 
 
-@pytest.mark.parametrize("P,n,leaf", [(2, 4096, 64), (4, 8192, 64)])
+@pytest.mark.parametrize("P,n,leaf", [(2, 4096, 64), (4, 8192, 64), (8, 8192, 64)])
 def test_sharded_build_with_real_exchanges(P, n, leaf):
     sys.path.insert(0, ROOT)
     import oracle
