@@ -349,13 +349,112 @@ __global__ void __launch_bounds__(256) potrf_kernel(const MatDesc* descs, int* i
         for (int i = lane; i < j; i += 32) A[i + (size_t)j * ld] = 0.0;
 }
 
+// Blocked form of the same factorisation: 32-column panels held in shared memory.  A panel
+// first takes the updates of every earlier column j < j0 (left-looking; 4 x 4 register tiles,
+// rows interleaved by 32 so every load of L is coalesced, L read from global / L2), then is
+// factored column by column in shared memory and written back once.  Every entry (i, k)
+// receives a_ik <- fma(-l_ij, l_kj, a_ik) for j = 0 .. k-1 in ascending j exactly like
+// potrf_kernel, so L (and the first failing pivot and its value) is bitwise the same; the
+// trailing matrix is no longer re-read and re-written once per column.
+constexpr int PO_NB = 32;
+__global__ void __launch_bounds__(256) potrf_panel_kernel(const MatDesc* descs, int* info, double* badval) {
+    extern __shared__ double po_sm[];             // panel: (n - j0) rows x 32 columns, ld = n - j0
+    const MatDesc d = descs[blockIdx.x];
+    double* A = d.A;
+    const int n = d.m, ld = d.ld;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ double piv;
+    __shared__ int bad;
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < n && !bad; j0 += PO_NB) {
+        const int nbk = min(PO_NB, n - j0), mr = n - j0;
+        double* P = po_sm;
+        // panel <- A[j0:n, j0:j0+nbk] - L[j0:n, 0:j0] L[j0:j0+nbk, 0:j0]^T
+        const int ngr = (mr + 127) / 128, ntc = (nbk + 3) / 4;
+        for (int task = warp; task < ngr * ntc; task += nw) {
+            const int gr = task % ngr, tc = task / ngr;
+            int ri[4], kc[4];
+            double acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) ri[a] = j0 + gr * 128 + lane + 32 * a;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) kc[b] = j0 + 4 * tc + b;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    acc[a][b] = (ri[a] < n && kc[b] < j0 + nbk) ? A[ri[a] + (size_t)kc[b] * ld] : 0.0;
+            for (int j = 0; j < j0; ++j) {
+                const double* cj = A + (size_t)j * ld;
+                double li[4], lk[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) li[a] = ri[a] < n ? cj[ri[a]] : 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) lk[b] = kc[b] < n ? cj[kc[b]] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] -= li[a] * lk[b];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (ri[a] < n && kc[b] < j0 + nbk) P[(ri[a] - j0) + (size_t)(kc[b] - j0) * mr] = acc[a][b];
+        }
+        __syncthreads();
+        // the panel's own columns, in shared memory (rows r >= jj of column jj)
+        for (int jj = 0; jj < nbk; ++jj) {
+            if (tid == 0) {
+                double a = P[jj + (size_t)jj * mr];
+                if (!(a > 0.0)) {               // not PD (or NaN): record first failure
+                    bad = 1;
+                    if (info) info[blockIdx.x] = j0 + jj + 1;
+                    if (badval) badval[blockIdx.x] = a;
+                    a = 1.0;
+                }
+                piv = sqrt(a);
+                P[jj + (size_t)jj * mr] = piv;
+            }
+            __syncthreads();
+            if (bad) break;
+            const double inv = 1.0 / piv;
+            for (int r = jj + 1 + tid; r < mr; r += blockDim.x) P[r + (size_t)jj * mr] *= inv;
+            __syncthreads();
+            const double* cj = P + (size_t)jj * mr;
+            for (int kk = jj + 1 + warp; kk < nbk; kk += nw) {
+                const double lkj = cj[kk];
+                double* ck = P + (size_t)kk * mr;
+                for (int r = kk + lane; r < mr; r += 32) ck[r] -= cj[r] * lkj;
+            }
+            __syncthreads();
+        }
+        // write the panel back (lower part; the upper triangle is zeroed below)
+        for (int c = warp; c < nbk; c += nw)
+            for (int r = c + lane; r < mr; r += 32) A[(j0 + r) + (size_t)(j0 + c) * ld] = P[r + (size_t)c * mr];
+        __syncthreads();
+    }
+    for (int j = 1 + warp; j < n; j += nw)
+        for (int i = lane; i < j; i += 32) A[i + (size_t)j * ld] = 0.0;
+}
+
 void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev, double* bad_dev) {
     if (d.empty()) return;
     double fl = 0, by = 0;
-    for (auto& m : d) { fl += (double)m.m * m.m * m.m / 3.0; by += 16.0 * m.m * m.m; }
+    int nmax = 0;
+    for (auto& m : d) { fl += (double)m.m * m.m * m.m / 3.0; by += 16.0 * m.m * m.m; nmax = std::max(nmax, m.m); }
     DevArray<MatDesc> dd(s, d);
     ProfScope prof(s, "potrf", fl, by);
-    potrf_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p, info_dev, bad_dev);
+    // panels in shared memory up to 220 KB (n <= 880); SPD_POTRF_GLOBAL=1: the unblocked kernel (A/B, bitwise equal)
+    const size_t smem = sizeof(double) * (size_t)nmax * PO_NB;
+    if (smem <= 220 * 1024 && !getenv("SPD_POTRF_GLOBAL")) {
+        if (smem > 48 * 1024)
+            SPD_CUDA(cudaFuncSetAttribute(potrf_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        potrf_panel_kernel<<<(unsigned)d.size(), 256, smem, s>>>(dd.p, info_dev, bad_dev);
+    } else {
+        potrf_kernel<<<(unsigned)d.size(), 256, 0, s>>>(dd.p, info_dev, bad_dev);
+    }
     SPD_LAUNCH();
 }
 

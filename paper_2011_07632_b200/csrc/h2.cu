@@ -28,6 +28,22 @@ __device__ double halton_dev(long long k, int base) {
     while (k > 0) { den *= base; num = num * base + (k % base); k /= base; }
     return __ddiv_rn((double)num, (double)den);
 }
+// the same radical inverse with a compile-time base: indices below 2^31 (all but a degenerate
+// shell scan) take 32-bit divisions by a constant instead of emulated 64-bit ones; num and den
+// are the same integers (den <= B k < 2^34), so the quotient is bitwise the generic one's
+template <int B>
+__device__ __forceinline__ double halton_fast(long long k) {
+    if (k >= (1LL << 31)) return halton_dev(k, B);
+    unsigned kk = (unsigned)k;
+    unsigned long long num = 0, den = 1;
+    while (kk > 0) {
+        const unsigned q = kk / B;
+        den *= B;
+        num = num * B + (kk - q * B);
+        kk = q;
+    }
+    return __ddiv_rn((double)num, (double)den);
+}
 
 __global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, const double* lo, const double* hi,
                                                     int d, int n_proxy, int m) {
@@ -38,7 +54,6 @@ __global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, cons
     const ProxyDesc pd = descs[blockIdx.x];
     const int i = pd.node;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bases[3] = {2, 3, 5};
     if (tid == 0) {
         double e[3], emax = 0.0, rmax = 0.0;
         for (int a = 0; a < d; ++a) {
@@ -72,7 +87,7 @@ __global__ void __launch_bounds__(256) proxy_kernel(const ProxyDesc* descs, cons
             if (k <= k_last) {
                 bool inside = true;
                 for (int a = 0; a < d; ++a) {
-                    double h = halton_dev(k, bases[a]);
+                    const double h = a == 0 ? halton_fast<2>(k) : (a == 1 ? halton_fast<3>(k) : halton_fast<5>(k));
                     p[a] = __dadd_rn(blo[a], __dmul_rn(h, __dsub_rn(bhi[a], blo[a])));
                     inside = inside && (ilo[a] < p[a] && p[a] < ihi[a]);
                 }

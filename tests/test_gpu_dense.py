@@ -57,6 +57,41 @@ def test_potrf_trsm(spd, n):
         assert rel(host(dX), want) < 1e-12, (uplo, trans)
 
 
+@pytest.mark.parametrize("n,lda", [(1, 1), (31, 40), (32, 32), (33, 33), (100, 128), (129, 129), (256, 256),
+                                   (300, 301), (600, 600)])
+def test_potrf_panel_kernel_bitwise_equals_unblocked(spd, monkeypatch, n, lda):
+    """The shared-memory panel Cholesky (32-column panels, left-looking register tiles) applies
+    the same fused multiply-adds in the same order as the column-by-column kernel
+    (SPD_POTRF_GLOBAL=1): L is bitwise equal, and so are the first failing pivot and its
+    reported column when the matrix is not positive definite."""
+    import ctypes
+    rng = np.random.default_rng(7 * n + lda)
+    G = rng.standard_normal((n, n))
+    A = G @ G.T + 0.5 * n * np.eye(n)
+    out = {}
+    for case in ("pd", "notpd"):
+        M = A.copy()
+        if case == "notpd":
+            j = (2 * n) // 3                          # first negative pivot exactly at column j
+            M[j, j] = (M[j, :j] @ np.linalg.solve(M[:j, :j], M[:j, j]) if j else 0.0) - 1e-3
+        buf = np.zeros((lda, n))                      # column-major, leading dimension lda
+        buf[:n, :] = M
+        for mode in ("panel", "global"):
+            if mode == "global":
+                monkeypatch.setenv("SPD_POTRF_GLOBAL", "1")
+            else:
+                monkeypatch.delenv("SPD_POTRF_GLOBAL", raising=False)
+            dA = cuda(buf)
+            info = ctypes.c_int(-1)
+            spd.lib().spd_test_potrf(ctypes.c_void_p(dA.data_ptr()), n, lda, ctypes.byref(info), spd._stream())
+            out[case, mode] = (info.value, host(dA))
+    assert out["pd", "panel"][0] == 0 and out["pd", "global"][0] == 0
+    assert np.array_equal(out["pd", "panel"][1], out["pd", "global"][1])
+    L = out["pd", "panel"][1][:n, :]
+    assert rel(L, np.linalg.cholesky(A)) < 1e-13
+    assert out["notpd", "panel"][0] == out["notpd", "global"][0] == (2 * n) // 3 + 1
+
+
 def test_potrf_reports_not_pd(spd):
     import ctypes
     A = np.array([[1.0, 2.0], [2.0, 1.0]])
