@@ -421,9 +421,11 @@ void h2_build_impl(spd_h2_s* h, const double* pts_dev, cudaStream_t s) {
             stage_mark(s, "h2 alloc/desc", k);
             {
                 DevArray<ProxyDesc> dp(s, pdesc);
-                ProfScope prof(s, "proxy_points", 0, 0);
-                proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, dim, h->n_proxy, m);
-                SPD_LAUNCH();
+                {
+                    ProfScope prof(s, "proxy_points", 0, 0);     // closed before proxy_matrix starts (per-class times)
+                    proxy_kernel<<<(unsigned)pdesc.size(), 256, 0, s>>>(dp.p, lo_d.p, hi_d.p, dim, h->n_proxy, m);
+                    SPD_LAUNCH();
+                }
                 DevArray<ProxyMatDesc> dm(s, mdesc);
                 double by = 0;
                 for (auto& m : mdesc) by += 8.0 * n_p * m.nc;
