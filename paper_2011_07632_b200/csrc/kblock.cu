@@ -749,6 +749,19 @@ bool kblock_plan(cudaStream_t s, const std::vector<KbBlock>& blocks, const std::
     plan.NC = NC;
     std::vector<KbEntry> ents(entries);
     plan.ntma = kb_tma_maps(blocks, ents, NC, plan.tma);
+    {
+        // a launch whose entries mostly cannot be addressed by the (at most KB_NTMA) maps -- the level
+        // loop's sandwiches, one X buffer per node -- runs the register-staged kernel: the mixed
+        // kernel pays its staging branches for a handful of TMA entries (SPD_KB_TMA_MINSHARE, default 0.5)
+        size_t nt = 0;
+        for (auto& e : ents) nt += e.tmi >= 0;
+        const char* ms = getenv("SPD_KB_TMA_MINSHARE");
+        const double minshare = ms ? atof(ms) : 0.5;
+        if (plan.ntma > 0 && (double)nt < minshare * (double)ents.size()) {
+            for (auto& e : ents) { e.tmi = -1; e.tr = 0; }
+            plan.ntma = 0;
+        }
+    }
     plan.tma_mix = false;
     for (auto& e : ents) plan.tma_mix |= e.tmi < 0;
     if (getenv("SPD_KB_TMA_TRACE")) {
