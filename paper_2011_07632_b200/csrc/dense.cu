@@ -446,9 +446,11 @@ void potrf_batched(cudaStream_t s, const std::vector<MatDesc>& d, int* info_dev,
     for (auto& m : d) { fl += (double)m.m * m.m * m.m / 3.0; by += 16.0 * m.m * m.m; nmax = std::max(nmax, m.m); }
     DevArray<MatDesc> dd(s, d);
     ProfScope prof(s, "potrf", fl, by);
-    // panels in shared memory up to 220 KB (n <= 880); SPD_POTRF_GLOBAL=1: the unblocked kernel (A/B, bitwise equal)
+    // SPD_POTRF_PANEL=1: panels in shared memory up to 220 KB (n <= 880), bitwise equal and 5.7x faster
+    // at C4 (91 -> 16 ms per step) -- NOT the default: with it the 4-process host-comm test hit a PCG
+    // breakdown in 2 of 6 runs against 0 of 5 with the unblocked kernel (unexplained)
     const size_t smem = sizeof(double) * (size_t)nmax * PO_NB;
-    if (smem <= 220 * 1024 && !getenv("SPD_POTRF_GLOBAL")) {
+    if (smem <= 220 * 1024 && getenv("SPD_POTRF_PANEL") && !getenv("SPD_POTRF_GLOBAL")) {
         if (smem > 48 * 1024)
             SPD_CUDA(cudaFuncSetAttribute(potrf_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         potrf_panel_kernel<<<(unsigned)d.size(), 256, smem, s>>>(dd.p, info_dev, bad_dev);

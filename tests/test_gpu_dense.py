@@ -62,7 +62,7 @@ def test_potrf_trsm(spd, n):
 def test_potrf_panel_kernel_bitwise_equals_unblocked(spd, monkeypatch, n, lda):
     """The shared-memory panel Cholesky (32-column panels, left-looking register tiles) applies
     the same fused multiply-adds in the same order as the column-by-column kernel
-    (SPD_POTRF_GLOBAL=1): L is bitwise equal, and so are the first failing pivot and its
+    (the default; the panel kernel is SPD_POTRF_PANEL=1): L is bitwise equal, and so are the first failing pivot and its
     reported column when the matrix is not positive definite."""
     import ctypes
     rng = np.random.default_rng(7 * n + lda)
@@ -78,9 +78,9 @@ def test_potrf_panel_kernel_bitwise_equals_unblocked(spd, monkeypatch, n, lda):
         buf[:n, :] = M
         for mode in ("panel", "global"):
             if mode == "global":
-                monkeypatch.setenv("SPD_POTRF_GLOBAL", "1")
+                monkeypatch.delenv("SPD_POTRF_PANEL", raising=False)
             else:
-                monkeypatch.delenv("SPD_POTRF_GLOBAL", raising=False)
+                monkeypatch.setenv("SPD_POTRF_PANEL", "1")
             dA = cuda(buf)
             info = ctypes.c_int(-1)
             spd.lib().spd_test_potrf(ctypes.c_void_p(dA.data_ptr()), n, lda, ctypes.byref(info), spd._stream())
